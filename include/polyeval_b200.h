@@ -1,0 +1,186 @@
+/*
+ * polyeval-b200 — C ABI of the B200 batch polynomial evaluator.
+ *
+ * Drop-in boundary for the reference's compile-once / evaluate API
+ * (reference: proj/core/include/polyeval/eval.hpp). The reference exposes a
+ * C++ template API, not an FFI; each entry point below names the reference
+ * interface it replaces:
+ *
+ *   pe_program_create      build()/build_multivariate() + compute_lazy_heights()
+ *                          + compile()            tree.hpp:58-77, eval.hpp:57
+ *                          (polynomial from raw terms: Polynomial::canonicalize,
+ *                          polynomial.hpp:34-36; schemes: scheme.hpp:15-57)
+ *   pe_program_destroy     CompiledProgram lifetime (move-only, eval.hpp:32-54)
+ *   pe_eval_f64            Evaluator<DoubleDomain>(domain, program) +
+ *                          evaluate(point) per point   eval.hpp:74-90, ring.hpp:40-48
+ *   pe_eval_i64            Evaluator<BigIntDomain> on a proven int64 range
+ *                                                       eval.hpp:74-90, ring.hpp:30-38
+ *   pe_eval_interval       Evaluator<IntervalDomain>    ring.hpp:50-65, interval.cpp:36-52
+ *   pe_program_info        CompiledProgram fields (register_count, records,
+ *                          exponent_sets, root_child_ends)  eval.hpp:32-54
+ *   pe_program_dot         to_dot(tree)                 tree.hpp:85-88
+ *   pe_last_error          exception what()             error.hpp:11-39
+ *
+ * Conventions:
+ *   - No exceptions cross this boundary; every call returns a pe_status.
+ *     PE_EINVAL   <=> std::invalid_argument (arity, null pointers, bad scheme)
+ *     PE_EOVERFLOW   int64 range proof failed, or a coordinate exceeded the
+ *                    proven bound (the reference BigInt never overflows; this
+ *                    path refuses instead of wrapping — there is no CPU fallback)
+ *     PE_ECUDA       CUDA / JIT failure (message in pe_last_error)
+ *     PE_ELOGIC   <=> std::logic_error
+ *   - pe_last_error() is thread-local and valid until the next call on the
+ *     same thread.
+ *   - A program is immutable after creation and safe to share across host
+ *     threads (the reference's CompiledProgram contract, eval.hpp:59-68).
+ *     Device kernels are specialised and loaded lazily per (domain, device)
+ *     and cached on the handle.
+ *   - Point and result buffers are caller-owned, structure-of-arrays: coords[v]
+ *     points at n values of variable v (variable order of the program).
+ *     Pointers may be device memory (evaluated in place, asynchronously on
+ *     exec->stream) or host memory (staged through pinned buffers with
+ *     copy/compute overlap; the call returns when results are on the host).
+ *     n == 0 is valid and does nothing.
+ */
+#ifndef POLYEVAL_B200_H_
+#define POLYEVAL_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pe_status {
+  PE_OK = 0,
+  PE_EINVAL = 1,
+  PE_EOVERFLOW = 2,
+  PE_ECUDA = 3,
+  PE_ELOGIC = 4,
+} pe_status;
+
+/* Builtin function schemes (reference scheme.hpp:36-41). */
+typedef enum pe_scheme_id {
+  PE_SCHEME_DIRECT = 0,
+  PE_SCHEME_HORNER = 1,
+  PE_SCHEME_ESTRIN = 2,
+  PE_SCHEME_BALANCED = 3,
+} pe_scheme_id;
+
+/* One scheme per variable: `upper` alone when cutoff == 0, else
+ * threshold_combine(upper, lower, cutoff) (reference scheme.hpp:43-47),
+ * i.e. the CLI grammar "upper:lower@cutoff" (tools/scheme_name.cpp:34-53). */
+typedef struct pe_scheme_desc {
+  int32_t upper;
+  int32_t lower;
+  uint64_t cutoff;
+} pe_scheme_desc;
+
+typedef enum pe_coeff_type {
+  PE_COEFF_F64 = 0, /* const double* coeffs */
+  PE_COEFF_I64 = 1, /* const int64_t* coeffs */
+} pe_coeff_type;
+
+typedef struct pe_program pe_program;
+
+/* Execution options. Zero-initialise for defaults (device 0 / current,
+ * default stream, fused fp64). */
+typedef struct pe_exec {
+  int32_t device;       /* CUDA device ordinal; -1 = current device */
+  int32_t strict_f64;   /* pe_eval_f64: 1 = reference op order, bit-exact  */
+  void* stream;         /* cudaStream_t for device-pointer calls; NULL = legacy default */
+  int32_t synchronize;  /* device-pointer calls: 1 = wait for completion */
+  int32_t reserved;
+  /* pe_eval_i64 only: caller-asserted per-variable bounds |x_v| <= bound[v]
+   * (nvars entries; NULL = derive from the data with a device max-reduction). */
+  const uint64_t* i64_bounds;
+} pe_exec;
+
+/* Compiles a polynomial given as raw terms: `exponents` is nterms x nvars
+ * (row-major), `coeffs` nterms values of `coeff_type`. Terms are
+ * canonicalised (sorted, like terms merged, zeros dropped). One scheme per
+ * variable; nvars == 1 uses build(), nvars > 1 build_multivariate(). */
+pe_status pe_program_create(const uint32_t* exponents, const void* coeffs,
+                            size_t nterms, uint32_t nvars,
+                            const pe_scheme_desc* schemes,
+                            pe_coeff_type coeff_type, pe_program** out);
+
+void pe_program_destroy(pe_program* program);
+
+typedef struct pe_program_info_t {
+  uint32_t nvars;
+  uint32_t register_count;     /* root program: 1 + max lazy height */
+  uint32_t max_registers;      /* max over nested programs */
+  uint64_t records;            /* all programs */
+  uint64_t programs;           /* root + nested */
+  uint64_t walk_adds;          /* reference op counts per point (eval_test.cpp:182-216) */
+  uint64_t walk_muls;
+  uint64_t power_muls;         /* memoized-halving multiplications per point */
+  uint64_t terms;              /* canonical terms */
+  uint32_t root_children;      /* root_child_ends.size() */
+  uint32_t exponent_set_sizes[8]; /* first 8 variables */
+} pe_program_info_t;
+
+pe_status pe_program_info(const pe_program* program, pe_program_info_t* info);
+
+/* Writes the exponent set of variable v (sorted) into out[0..cap); *count
+ * receives the set size. */
+pe_status pe_program_exponents(const pe_program* program, uint32_t v,
+                               uint32_t* out, size_t cap, size_t* count);
+
+/* Flat record dump of the root program (records x 5 int32: power_slot or -1,
+ * lazy_slot, parent_slot or -1, reads_register, has_sub). */
+pe_status pe_program_records(const pe_program* program, int32_t* out,
+                             size_t cap, size_t* count);
+
+/* DOT text of the root tree (reference to_dot). Writes at most cap bytes
+ * including the NUL; *len receives the full length. */
+pe_status pe_program_dot(const pe_program* program, char* out, size_t cap,
+                         size_t* len);
+
+/* Specialised kernel statistics for a domain (0 f64, 1 f64 strict, 2 i64,
+ * 3 interval): FP64 / int64 arithmetic instructions per point, and the PTX
+ * text size. Generates (but does not load) the kernel. */
+pe_status pe_program_kernel_stats(const pe_program* program, int32_t domain,
+                                  uint64_t* fp_ops, uint64_t* int_ops,
+                                  uint64_t* ptx_bytes);
+
+/* Writes the generated PTX for `domain` (debug / inspection). */
+pe_status pe_program_ptx(const pe_program* program, int32_t domain, char* out,
+                         size_t cap, size_t* len);
+
+/* Compiles the domain's kernel to an sm_100a cubin without a GPU (build and
+ * CI check); *cubin_bytes receives the image size. */
+pe_status pe_program_compile_only(const pe_program* program, int32_t domain,
+                                  uint64_t* cubin_bytes);
+
+/* Batch evaluation. coords: nvars pointers, each to n values. */
+pe_status pe_eval_f64(const pe_program* program, const double* const* coords,
+                      size_t n, double* out, const pe_exec* exec);
+
+pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords,
+                      size_t n, int64_t* out, const pe_exec* exec);
+
+/* Interval points [lo[v][i], hi[v][i]]; results [out_lo[i], out_hi[i]].
+ * Endpoints must be non-NaN with lo <= hi (reference Interval ctor). */
+pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
+                           const double* const* hi, size_t n, double* out_lo,
+                           double* out_hi, const pe_exec* exec);
+
+/* Waits for all work this library queued on `exec` (device + stream). */
+pe_status pe_synchronize(const pe_exec* exec);
+
+/* Number of kernels this library launched in this process (evidence counter). */
+uint64_t pe_launch_count(void);
+
+const char* pe_last_error(void);
+
+/* Library / ABI version. */
+const char* pe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POLYEVAL_B200_H_ */

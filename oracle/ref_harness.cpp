@@ -1,0 +1,288 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// C harness over the *unmodified* reference library (compiled from
+// /root/reference/proj/core/src by oracle/Makefile into oracle/_ref/). It
+// drives the reference's own public API: Polynomial::canonicalize ->
+// build / build_multivariate -> compute_lazy_heights -> compile ->
+// Evaluator<D>::evaluate, one point per call (eval.hpp:74-90), one Evaluator
+// session per host thread over a contiguous shard (the reference's documented
+// concurrency contract, eval.hpp:59-68).
+//
+// fp64 coefficients: the reference Polynomial holds BigInt only,
+// so each coefficient c is encoded as k = c * 2^S (S the smallest shift making
+// every coefficient integral; BigInt::from_double_integral throws otherwise)
+// and evaluated through ScaledDoubleDomain / ScaledIntervalDomain, whose
+// from_integer(k) = ldexp(k.to_double(), -S) is exact. Everything else (walk,
+// power tables, interval rounding) is the reference's code.
+#include <polyeval/bigint.hpp>
+#include <polyeval/eval.hpp>
+#include <polyeval/interval.hpp>
+#include <polyeval/polynomial.hpp>
+#include <polyeval/ring.hpp>
+#include <polyeval/scheme.hpp>
+#include <polyeval/tree.hpp>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+using namespace polyeval;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ScaledDoubleDomain {
+  using Value = double;
+  static constexpr bool exact = false;
+  int shift = 0;
+  Value zero() const { return 0.0; }
+  Value add(const Value& a, const Value& b) const { return a + b; }
+  Value mul(const Value& a, const Value& b) const { return a * b; }
+  Value from_integer(const BigInt& c) const { return std::ldexp(c.to_double(), -shift); }
+};
+
+struct ScaledIntervalDomain {
+  using Value = Interval;
+  static constexpr bool exact = false;
+  int shift = 0;
+  Value zero() const { return Interval(); }
+  Value add(const Value& a, const Value& b) const { return interval_add(a, b); }
+  Value mul(const Value& a, const Value& b) const { return interval_mul(a, b); }
+  Value from_integer(const BigInt& c) const {
+    if (shift == 0) return IntervalDomain{}.from_integer(c);
+    const double v = std::ldexp(c.to_double(), -shift);  // exact by construction
+    return Interval(v, v);
+  }
+};
+
+struct RefProgram {
+  bool integer = false;
+  int shift = 0;
+  std::size_t nvars = 0;
+  std::unique_ptr<EvaluationTree> tree;
+  std::unique_ptr<CompiledProgram> program;
+};
+
+FunctionScheme scheme_of(int up, int lo, std::uint64_t cutoff) {
+  auto b = [](int id) { return builtin_scheme(static_cast<BuiltinScheme>(id)); };
+  if (cutoff == 0) return b(up);
+  return threshold_combine(b(up), b(lo), cutoff);
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+template <typename D, typename In, typename Out, typename Conv>
+void run_sharded(const RefProgram& rp, D domain, std::size_t n, int threads, In&& point_of,
+                 Out* out, Conv&& conv) {
+  threads = std::max(1, threads);
+  const std::size_t per = (n + threads - 1) / threads;
+  std::vector<std::exception_ptr> errors(threads);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      try {
+        Evaluator<D> session(domain, *rp.program);
+        std::vector<typename D::Value> point(rp.nvars);
+        const std::size_t lo = t * per, hi = std::min(n, lo + per);
+        for (std::size_t i = lo; i < hi; ++i) {
+          point_of(i, point);
+          out[i] = conv(session.evaluate(std::span<const typename D::Value>(point)));
+        }
+      } catch (...) {
+        errors[t] = std::current_exception();
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (auto& e : errors) {
+    if (e) std::rethrow_exception(e);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_create(const std::uint32_t* exps, const void* coeffs, std::size_t nterms,
+               std::uint32_t nvars, const int* upper, const int* lower,
+               const std::uint64_t* cutoff, int coeff_is_int, void** out) {
+  return guarded([&] {
+    auto rp = std::make_unique<RefProgram>();
+    rp->integer = coeff_is_int != 0;
+    rp->nvars = nvars;
+    std::vector<std::string> vars;
+    for (std::uint32_t v = 0; v < nvars; ++v) {
+      vars.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
+    }
+    int shift = 0;
+    if (!rp->integer) {
+      const double* c = static_cast<const double*>(coeffs);
+      for (std::size_t t = 0; t < nterms; ++t) {
+        if (c[t] == 0.0) continue;
+        int e = 0;
+        std::frexp(c[t], &e);
+        shift = std::max(shift, 53 - e);
+      }
+    }
+    rp->shift = shift;
+    std::vector<Term> raw(nterms);
+    for (std::size_t t = 0; t < nterms; ++t) {
+      if (rp->integer) {
+        raw[t].coefficient = BigInt(static_cast<const std::int64_t*>(coeffs)[t]);
+      } else {
+        raw[t].coefficient =
+            BigInt::from_double_integral(std::ldexp(static_cast<const double*>(coeffs)[t], shift));
+      }
+      raw[t].exponents.assign(exps + t * nvars, exps + (t + 1) * nvars);
+    }
+    Polynomial p = Polynomial::canonicalize(std::move(raw), vars);
+    std::vector<FunctionScheme> schemes;
+    for (std::uint32_t v = 0; v < nvars; ++v) schemes.push_back(scheme_of(upper[v], lower[v], cutoff[v]));
+    EvaluationTree tree = nvars == 1 ? build(p, schemes[0], 0) : build_multivariate(p, schemes);
+    compute_lazy_heights(tree);
+    rp->program = std::make_unique<CompiledProgram>(compile(tree));
+    rp->tree = std::make_unique<EvaluationTree>(std::move(tree));
+    *out = rp.release();
+    return 0;
+  });
+}
+
+void ref_destroy(void* h) { delete static_cast<RefProgram*>(h); }
+
+int ref_dot(void* h, char* buf, std::size_t cap, std::size_t* len) {
+  return guarded([&] {
+    const std::string dot = to_dot(*static_cast<RefProgram*>(h)->tree);
+    *len = dot.size();
+    if (buf && cap) {
+      const std::size_t k = std::min(cap - 1, dot.size());
+      std::memcpy(buf, dot.data(), k);
+      buf[k] = 0;
+    }
+    return 0;
+  });
+}
+
+// records x 5: power_slot|-1, lazy_slot, parent_slot|-1, reads_register, has_sub
+int ref_records(void* h, std::int32_t* out, std::size_t cap, std::size_t* count,
+                std::uint32_t* register_count) {
+  return guarded([&] {
+    const CompiledProgram& p = *static_cast<RefProgram*>(h)->program;
+    *count = p.records.size();
+    *register_count = p.register_count;
+    for (std::size_t i = 0; i < p.records.size() && (i + 1) * 5 <= cap; ++i) {
+      const auto& r = p.records[i];
+      out[5 * i] = r.power_slot ? static_cast<std::int32_t>(*r.power_slot) : -1;
+      out[5 * i + 1] = static_cast<std::int32_t>(r.lazy_slot);
+      out[5 * i + 2] = r.parent_slot ? static_cast<std::int32_t>(*r.parent_slot) : -1;
+      out[5 * i + 3] = r.reads_register ? 1 : 0;
+      out[5 * i + 4] = r.sub ? 1 : 0;
+    }
+    return 0;
+  });
+}
+
+int ref_exponents(void* h, std::uint32_t v, std::uint32_t* out, std::size_t cap, std::size_t* count) {
+  return guarded([&] {
+    const CompiledProgram& p = *static_cast<RefProgram*>(h)->program;
+    const auto& e = p.exponent_sets.at(v).exponents;
+    *count = e.size();
+    for (std::size_t i = 0; i < e.size() && i < cap; ++i) out[i] = e[i];
+    return 0;
+  });
+}
+
+int ref_eval_f64(void* h, const double* const* coords, std::size_t n, double* out, int threads) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    auto pt = [&](std::size_t i, std::vector<double>& p) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = coords[v][i];
+    };
+    auto id = [](double x) { return x; };
+    if (rp.integer) {
+      run_sharded(rp, DoubleDomain{}, n, threads, pt, out, id);
+    } else {
+      run_sharded(rp, ScaledDoubleDomain{rp.shift}, n, threads, pt, out, id);
+    }
+    return 0;
+  });
+}
+
+int ref_eval_interval(void* h, const double* const* lo, const double* const* hi, std::size_t n,
+                      double* out_lo, double* out_hi, int threads) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    auto pt = [&](std::size_t i, std::vector<Interval>& p) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = Interval(lo[v][i], hi[v][i]);
+    };
+    std::vector<Interval> res(n);
+    auto id = [](const Interval& x) { return x; };
+    run_sharded(rp, ScaledIntervalDomain{rp.integer ? 0 : rp.shift}, n, threads, pt, res.data(), id);
+    for (std::size_t i = 0; i < n; ++i) {
+      out_lo[i] = res[i].lo;
+      out_hi[i] = res[i].hi;
+    }
+    return 0;
+  });
+}
+
+// BigIntDomain; results must fit int64 (reported as an error otherwise).
+int ref_eval_i64(void* h, const std::int64_t* const* coords, std::size_t n, std::int64_t* out,
+                 int threads) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    if (!rp.integer) throw std::invalid_argument("integer evaluation needs integer coefficients");
+    auto pt = [&](std::size_t i, std::vector<BigInt>& p) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = BigInt(coords[v][i]);
+    };
+    const BigInt lo = BigInt(INT64_MIN), hi = BigInt(INT64_MAX);
+    auto conv = [&](const BigInt& b) -> std::int64_t {
+      if (b < lo || b > hi) throw std::overflow_error("result does not fit int64");
+      // decimal round trip keeps the harness independent of BigInt internals
+      return std::stoll(b.to_decimal());
+    };
+    run_sharded(rp, BigIntDomain{}, n, threads, pt, out, conv);
+    return 0;
+  });
+}
+
+// evaluate_parallel (intra-point threading, eval.hpp:97-140) for `n` points
+int ref_eval_parallel_f64(void* h, const double* const* coords, std::size_t n, double* out,
+                          unsigned workers) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    std::vector<double> p(rp.nvars);
+    if (rp.integer) {
+      Evaluator<DoubleDomain> s(DoubleDomain{}, *rp.program);
+      for (std::size_t i = 0; i < n; ++i) {
+        for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = coords[v][i];
+        out[i] = s.evaluate_parallel(std::span<const double>(p), workers);
+      }
+    } else {
+      Evaluator<ScaledDoubleDomain> s(ScaledDoubleDomain{rp.shift}, *rp.program);
+      for (std::size_t i = 0; i < n; ++i) {
+        for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = coords[v][i];
+        out[i] = s.evaluate_parallel(std::span<const double>(p), workers);
+      }
+    }
+    return 0;
+  });
+}
+
+}  // extern "C"

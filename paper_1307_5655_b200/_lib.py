@@ -1,0 +1,127 @@
+"""ctypes binding of the C ABI in include/polyeval_b200.h.
+
+The shared library is built in-tree (paper_1307_5655_b200/_lib/
+libpolyeval_b200.so, see csrc/Makefile and __graft_entry__.build()). There is
+no CPU fallback: importing this module without the library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libpolyeval_b200.so")
+
+PE_OK, PE_EINVAL, PE_EOVERFLOW, PE_ECUDA, PE_ELOGIC = 0, 1, 2, 3, 4
+
+DOMAIN_F64, DOMAIN_F64_STRICT, DOMAIN_I64, DOMAIN_INTERVAL = 0, 1, 2, 3
+
+COEFF_F64, COEFF_I64 = 0, 1
+
+
+class pe_scheme_desc(C.Structure):
+    _fields_ = [("upper", C.c_int32), ("lower", C.c_int32), ("cutoff", C.c_uint64)]
+
+
+class pe_exec(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("strict_f64", C.c_int32),
+        ("stream", C.c_void_p),
+        ("synchronize", C.c_int32),
+        ("reserved", C.c_int32),
+        ("i64_bounds", C.POINTER(C.c_uint64)),
+    ]
+
+
+class pe_program_info_t(C.Structure):
+    _fields_ = [
+        ("nvars", C.c_uint32),
+        ("register_count", C.c_uint32),
+        ("max_registers", C.c_uint32),
+        ("records", C.c_uint64),
+        ("programs", C.c_uint64),
+        ("walk_adds", C.c_uint64),
+        ("walk_muls", C.c_uint64),
+        ("power_muls", C.c_uint64),
+        ("terms", C.c_uint64),
+        ("root_children", C.c_uint32),
+        ("exponent_set_sizes", C.c_uint32 * 8),
+    ]
+
+
+# (name, restype, argtypes) — must match include/polyeval_b200.h exactly.
+EXPORTS = [
+    ("pe_program_create", C.c_int,
+     [C.POINTER(C.c_uint32), C.c_void_p, C.c_size_t, C.c_uint32,
+      C.POINTER(pe_scheme_desc), C.c_int, C.POINTER(C.c_void_p)]),
+    ("pe_program_destroy", None, [C.c_void_p]),
+    ("pe_program_info", C.c_int, [C.c_void_p, C.POINTER(pe_program_info_t)]),
+    ("pe_program_exponents", C.c_int,
+     [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("pe_program_records", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_int32), C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("pe_program_dot", C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("pe_program_kernel_stats", C.c_int,
+     [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+      C.POINTER(C.c_uint64)]),
+    ("pe_program_ptx", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("pe_program_compile_only", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]),
+    ("pe_eval_f64", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_eval_i64", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_eval_interval", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p,
+      C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_synchronize", C.c_int, [C.POINTER(pe_exec)]),
+    ("pe_launch_count", C.c_uint64, []),
+    ("pe_last_error", C.c_char_p, []),
+    ("pe_version", C.c_char_p, []),
+]
+
+_lib = None
+
+
+def lib():
+    """Loads the library once; raises ImportError if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"polyeval-b200 native library missing at {LIB_PATH}; "
+            "run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+    handle = C.CDLL(LIB_PATH)
+    for name, res, args in EXPORTS:
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = handle
+    return _lib
+
+
+class PolyEvalError(RuntimeError):
+    """Base class; subclasses mirror the reference exception taxonomy."""
+
+
+class CudaError(PolyEvalError):
+    pass
+
+
+class LogicError(PolyEvalError):
+    """std::logic_error analogue (e.g. register hygiene / internal)."""
+
+
+def check(status: int) -> None:
+    if status == PE_OK:
+        return
+    msg = lib().pe_last_error().decode(errors="replace")
+    if status == PE_EINVAL:
+        raise ValueError(msg)
+    if status == PE_EOVERFLOW:
+        raise OverflowError(msg)
+    if status == PE_ECUDA:
+        raise CudaError(msg)
+    raise LogicError(msg)

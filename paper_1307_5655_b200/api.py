@@ -1,0 +1,353 @@
+"""Host-side mirror of the reference's compile-once / evaluate API.
+
+Reference interface (proj/core/include/polyeval/):
+  scheme.hpp:15-57   FunctionScheme, builtin_scheme, threshold_combine
+  polynomial.hpp     Polynomial (canonical sparse terms)
+  tree.hpp:58-88     build / build_multivariate / compute_lazy_heights / to_dot
+  eval.hpp:32-57     CompiledProgram, compile(tree)
+  eval.hpp:69-90     Evaluator<D>(domain, program).evaluate(point)
+  ring.hpp:30-65     BigIntDomain / DoubleDomain / IntervalDomain
+
+Differences, by design: `evaluate` takes a *batch* of points (structure of
+arrays, one array per variable) and runs on the GPU through the C ABI; the
+BigInt domain is the exact int64 path with a host overflow proof
+(OverflowError instead of wrapping). Errors follow the reference taxonomy:
+ValueError <=> std::invalid_argument, LogicError <=> std::logic_error.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ----------------------------------------------------------------- schemes
+
+class BuiltinScheme(enum.IntEnum):
+    direct = 0
+    horner = 1
+    estrin = 2
+    balanced = 3
+
+
+@dataclass(frozen=True)
+class FunctionScheme:
+    """A scheme is `upper` alone (cutoff 0) or threshold_combine(upper, lower, cutoff)."""
+    upper: BuiltinScheme
+    lower: BuiltinScheme = BuiltinScheme.horner
+    cutoff: int = 0
+
+    @property
+    def name(self) -> str:
+        if self.cutoff == 0:
+            return self.upper.name
+        return f"{self.upper.name}:{self.lower.name}@{self.cutoff}"
+
+    def split(self, k: int) -> int:
+        """Python restatement of the split function (reference scheme.cpp:10-34)."""
+        which = self.upper if (self.cutoff == 0 or k > self.cutoff) else self.lower
+        if which == BuiltinScheme.direct:
+            return k
+        if which == BuiltinScheme.horner:
+            return 1
+        if which == BuiltinScheme.estrin:
+            return 1 << (k.bit_length() - 1) if k > 0 else 0
+        return (k + 1) // 2
+
+    def desc(self) -> L.pe_scheme_desc:
+        return L.pe_scheme_desc(int(self.upper), int(self.lower), int(self.cutoff))
+
+
+def builtin_scheme(which) -> FunctionScheme:
+    if isinstance(which, str):
+        which = BuiltinScheme[which]
+    return FunctionScheme(BuiltinScheme(which))
+
+
+def threshold_combine(upper: FunctionScheme, lower: FunctionScheme, cutoff: int) -> FunctionScheme:
+    if cutoff < 1:
+        raise ValueError("threshold cutoff must be >= 1")
+    if upper.cutoff or lower.cutoff:
+        raise ValueError("nested threshold schemes are not expressible across the C ABI")
+    return FunctionScheme(upper.upper, lower.upper, int(cutoff))
+
+
+def scheme_from_name(name: str) -> FunctionScheme:
+    """'name' or 'upper:lower@N' (reference tools/scheme_name.cpp:34-53)."""
+    if ":" not in name:
+        return builtin_scheme(name)
+    up, rest = name.split(":", 1)
+    if "@" not in rest:
+        raise ValueError(f"bad scheme name {name!r}")
+    lo, cut = rest.split("@", 1)
+    if not cut.isdigit() or int(cut) < 1:
+        raise ValueError(f"bad scheme cutoff in {name!r}")
+    return threshold_combine(builtin_scheme(up), builtin_scheme(lo), int(cut))
+
+
+# ----------------------------------------------------------------- polynomial
+
+@dataclass
+class Polynomial:
+    """Raw terms: exponents (T, V) uint32 and coefficients (T,) float64|int64.
+
+    Canonicalisation (sort, merge like terms, drop zeros) happens in the
+    native front-end at compile time (reference polynomial.cpp:13-33).
+    """
+    exponents: np.ndarray
+    coefficients: np.ndarray
+    variables: tuple = ("x",)
+
+    def __post_init__(self):
+        self.exponents = np.ascontiguousarray(np.asarray(self.exponents, dtype=np.uint32))
+        if self.exponents.ndim == 1:
+            self.exponents = self.exponents.reshape(-1, 1)
+        c = np.asarray(self.coefficients)
+        if c.dtype.kind in "iu":
+            c = c.astype(np.int64)
+        else:
+            c = c.astype(np.float64)
+        self.coefficients = np.ascontiguousarray(c)
+        if self.exponents.shape[0] != self.coefficients.shape[0]:
+            raise ValueError("one coefficient per term")
+        if len(self.variables) != self.exponents.shape[1]:
+            self.variables = tuple("xyz"[i] if self.exponents.shape[1] <= 3 else f"x{i}"
+                                   for i in range(self.exponents.shape[1]))
+
+    @property
+    def nvars(self) -> int:
+        return self.exponents.shape[1]
+
+    @classmethod
+    def univariate(cls, coeffs_high_to_low, dtype=None) -> "Polynomial":
+        """Dense univariate from coefficients c_d..c_0 (highest degree first)."""
+        c = np.asarray(coeffs_high_to_low, dtype=dtype)
+        d = len(c) - 1
+        return cls(np.arange(d, -1, -1, dtype=np.uint32).reshape(-1, 1), c, ("x",))
+
+
+# ----------------------------------------------------------------- program
+
+class CompiledProgram:
+    """Owns a native pe_program (immutable, shareable across threads)."""
+
+    def __init__(self, poly: Polynomial, schemes: Sequence[FunctionScheme]):
+        lib = L.lib()
+        if len(schemes) != poly.nvars:
+            raise ValueError("need exactly one scheme per variable")
+        self.poly = poly
+        self.schemes = tuple(schemes)
+        self.integer = poly.coefficients.dtype == np.int64
+        descs = (L.pe_scheme_desc * poly.nvars)(*[s.desc() for s in schemes])
+        h = C.c_void_p()
+        st = lib.pe_program_create(
+            poly.exponents.ctypes.data_as(C.POINTER(C.c_uint32)),
+            poly.coefficients.ctypes.data_as(C.c_void_p), poly.coefficients.shape[0],
+            poly.nvars, descs, L.COEFF_I64 if self.integer else L.COEFF_F64, C.byref(h))
+        L.check(st)
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                L.lib().pe_program_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def nvars(self) -> int:
+        return self.poly.nvars
+
+    def info(self) -> dict:
+        inf = L.pe_program_info_t()
+        L.check(L.lib().pe_program_info(self._h, C.byref(inf)))
+        return {
+            "nvars": inf.nvars, "register_count": inf.register_count,
+            "max_registers": inf.max_registers, "records": inf.records,
+            "programs": inf.programs, "walk_adds": inf.walk_adds, "walk_muls": inf.walk_muls,
+            "power_muls": inf.power_muls, "terms": inf.terms,
+            "root_children": inf.root_children,
+            "exponent_set_sizes": list(inf.exponent_set_sizes)[: inf.nvars],
+        }
+
+    def exponent_set(self, v: int) -> list:
+        n = C.c_size_t()
+        L.check(L.lib().pe_program_exponents(self._h, v, None, 0, C.byref(n)))
+        buf = (C.c_uint32 * max(1, n.value))()
+        L.check(L.lib().pe_program_exponents(self._h, v, buf, n.value, C.byref(n)))
+        return list(buf)[: n.value]
+
+    def records(self) -> np.ndarray:
+        """(records, 5): power_slot|-1, lazy_slot, parent_slot|-1, reads_register, has_sub."""
+        n = C.c_size_t()
+        L.check(L.lib().pe_program_records(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(5 * max(1, n.value), dtype=np.int32)
+        L.check(L.lib().pe_program_records(
+            self._h, buf.ctypes.data_as(C.POINTER(C.c_int32)), buf.size, C.byref(n)))
+        return buf[: 5 * n.value].reshape(-1, 5)
+
+    def dot(self) -> str:
+        n = C.c_size_t()
+        L.check(L.lib().pe_program_dot(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        L.check(L.lib().pe_program_dot(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def ptx(self, domain: int) -> str:
+        n = C.c_size_t()
+        L.check(L.lib().pe_program_ptx(self._h, domain, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        L.check(L.lib().pe_program_ptx(self._h, domain, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def kernel_stats(self, domain: int) -> dict:
+        fp, it, nb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        L.check(L.lib().pe_program_kernel_stats(self._h, domain, C.byref(fp), C.byref(it),
+                                                C.byref(nb)))
+        return {"fp_ops": fp.value, "int_ops": it.value, "ptx_bytes": nb.value}
+
+    def compile_only(self, domain: int) -> int:
+        nb = C.c_uint64()
+        L.check(L.lib().pe_program_compile_only(self._h, domain, C.byref(nb)))
+        return nb.value
+
+
+def compile(poly: Polynomial, schemes) -> CompiledProgram:  # noqa: A001 (reference name)
+    """build/build_multivariate + compute_lazy_heights + compile in one call."""
+    if isinstance(schemes, FunctionScheme):
+        schemes = [schemes] * poly.nvars
+    return CompiledProgram(poly, schemes)
+
+
+# ----------------------------------------------------------------- domains
+
+class DoubleDomain:
+    """fp64; strict=True replays the reference op order bit-exactly."""
+    def __init__(self, strict: bool = False):
+        self.strict = bool(strict)
+
+
+class IntervalDomain:
+    """Reference IntervalDomain: RN op + one nextafter step outward."""
+
+
+class BigIntDomain:
+    """Exact integer domain on a host-proven int64 range."""
+
+
+def _is_torch_cuda(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+class Evaluator:
+    """Batch evaluation session (reference Evaluator<D>, eval.hpp:69-90)."""
+
+    def __init__(self, domain, program: CompiledProgram, device: int = -1):
+        self.domain = domain
+        self.program = program
+        self.device = device
+        if isinstance(domain, BigIntDomain) and not program.integer:
+            raise ValueError("BigIntDomain needs integer coefficients")
+
+    def _exec(self, stream=None, sync=True, bounds=None) -> L.pe_exec:
+        ex = L.pe_exec()
+        ex.device = self.device
+        ex.strict_f64 = 1 if isinstance(self.domain, DoubleDomain) and self.domain.strict else 0
+        ex.stream = stream
+        ex.synchronize = 1 if sync else 0
+        if bounds is not None:
+            arr = (C.c_uint64 * len(bounds))(*[int(b) for b in bounds])
+            ex.i64_bounds = arr
+            self._keep = arr
+        return ex
+
+    def _soa(self, points, dtype):
+        if isinstance(points, np.ndarray) and points.ndim == 2:
+            if points.shape[1] != self.program.nvars:
+                raise ValueError("evaluation point arity mismatch")
+            points = [points[:, v] for v in range(points.shape[1])]
+        if len(points) != self.program.nvars:
+            raise ValueError("evaluation point arity mismatch")
+        cols = []
+        for p in points:
+            if _is_torch_cuda(p):
+                if not p.is_contiguous():
+                    p = p.contiguous()
+                cols.append(p)
+            else:
+                cols.append(np.ascontiguousarray(np.asarray(p, dtype=dtype)))
+        n = {int(c.shape[0]) for c in cols}
+        if len(n) != 1:
+            raise ValueError("all coordinate arrays must have the same length")
+        return cols, n.pop()
+
+    @staticmethod
+    def _ptr(a):
+        return a.data_ptr() if _is_torch_cuda(a) else a.ctypes.data
+
+    def evaluate(self, points, out=None, stream=None, bounds=None):
+        """points: per-variable arrays (numpy -> host staged, torch CUDA ->
+        in place); IntervalDomain takes (lo_arrays, hi_arrays)."""
+        lib = L.lib()
+        if isinstance(self.domain, IntervalDomain):
+            lo, hi = points
+            lo_c, n = self._soa(lo, np.float64)
+            hi_c, n2 = self._soa(hi, np.float64)
+            if n != n2:
+                raise ValueError("lo/hi length mismatch")
+            dev = _is_torch_cuda(lo_c[0])
+            if out is None:
+                out = (self._alloc(n, "f64", dev, lo_c[0]), self._alloc(n, "f64", dev, lo_c[0]))
+            lo_p = (C.c_void_p * len(lo_c))(*[self._ptr(a) for a in lo_c])
+            hi_p = (C.c_void_p * len(hi_c))(*[self._ptr(a) for a in hi_c])
+            ex = self._exec(self._stream(stream, dev))
+            L.check(lib.pe_eval_interval(self.program.handle, lo_p, hi_p, n, self._ptr(out[0]),
+                                         self._ptr(out[1]), C.byref(ex)))
+            return out
+        integer = isinstance(self.domain, BigIntDomain)
+        cols, n = self._soa(points, np.int64 if integer else np.float64)
+        dev = _is_torch_cuda(cols[0])
+        if out is None:
+            out = self._alloc(n, "i64" if integer else "f64", dev, cols[0])
+        ptrs = (C.c_void_p * len(cols))(*[self._ptr(a) for a in cols])
+        ex = self._exec(self._stream(stream, dev), bounds=bounds)
+        fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
+        L.check(fn(self.program.handle, ptrs, n, self._ptr(out), C.byref(ex)))
+        return out
+
+    @staticmethod
+    def _stream(stream, dev):
+        if stream is not None:
+            return stream
+        if dev:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        return None
+
+    @staticmethod
+    def _alloc(n, kind, dev, like):
+        if dev:
+            import torch
+            dt = torch.int64 if kind == "i64" else torch.float64
+            return torch.empty(n, dtype=dt, device=like.device)
+        return np.empty(n, dtype=np.int64 if kind == "i64" else np.float64)
+
+
+def evaluate(program: CompiledProgram, points, domain):
+    """One-shot convenience wrapper (reference eval.hpp:262-268)."""
+    return Evaluator(domain, program).evaluate(points)
+
+
+def launch_count() -> int:
+    return int(L.lib().pe_launch_count())

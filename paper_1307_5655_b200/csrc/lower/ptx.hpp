@@ -1,0 +1,55 @@
+// PTX emission for a lowered stream: one specialised sm_100a kernel per
+// (program, domain). The kernel body is the straight-line walk; the frame
+// around it (thread -> point mapping, SoA coordinate loads, power DAG,
+// stores, domain checks) is fixed and hand-written below.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "lower/stream.hpp"
+
+namespace polyeval::lower {
+
+enum class Domain : int {
+  F64 = 0,        // DoubleDomain, FMA-fused (tolerance contract)
+  F64Strict = 1,  // DoubleDomain, reference op sequence, bit-exact
+  I64 = 2,        // BigIntDomain restricted to a proven int64 range, exact
+  Interval = 3,   // IntervalDomain, reference op sequence, bit-exact
+};
+
+const char* domain_name(Domain d);
+
+/// Where the coefficient words of a kernel live. Warp-uniform reads from the
+/// constant bank fold into the FP64 instruction operand (c[0x3][imm]); the
+/// 64 KB bank holds 8K words, kernel parameters another ~4K (c[0x0]); beyond
+/// that coefficients stream from global memory through L1 (one LDG each).
+struct CoefTiers {
+  static constexpr std::uint32_t kConstCap = 8000;
+  static constexpr std::uint32_t kParamCap = 3900;
+};
+
+struct KernelImage {
+  std::string entry;               // kernel symbol
+  std::string ptx;                 // full module text
+  Domain domain = Domain::F64;
+  std::uint32_t nvars = 0;
+  std::uint32_t n_in = 0;          // pointer params for coordinates
+  std::uint32_t n_out = 0;         // pointer params for results
+  bool has_flag = false;           // u64 device pointer to a u32 status word
+  bool has_bounds = false;         // nvars x u64 coordinate bounds (int64)
+  std::vector<std::uint64_t> param_words;   // param-tier coefficient words
+  std::vector<std::uint64_t> global_words;  // global-tier coefficient words
+  std::uint32_t const_words = 0;
+  std::uint32_t block = 128;
+  // instruction counts per point (roofline bookkeeping)
+  std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
+  std::uint64_t int_ops = 0;       // int64 add/mul/mad per point
+  std::uint64_t hash = 0;          // FNV-1a of `ptx`
+};
+
+template <typename C>
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain);
+
+}  // namespace polyeval::lower

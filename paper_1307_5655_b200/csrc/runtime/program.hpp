@@ -1,0 +1,69 @@
+// The program handle behind the C ABI: front-end result (tree + compiled
+// program, reference semantics) plus lazily generated per-domain kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "front/compile.hpp"
+#include "lower/ptx.hpp"
+
+namespace polyeval::rt {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+/// One specialised kernel: generated PTX, its cubin, and the loaded handle.
+struct Artifact {
+  lower::KernelImage image;
+  std::vector<char> cubin;
+  double compile_seconds = 0.0;
+  cudaLibrary_t library = nullptr;
+  cudaKernel_t kernel = nullptr;
+  std::map<int, void*> global_coefs;  // per device: global-tier coefficient words
+};
+
+struct Program {
+  std::uint32_t nvars = 0;
+  bool integer = false;  // coefficient type int64 (else fp64)
+  std::uint64_t nterms = 0;
+  std::vector<std::string> variables;
+
+  std::unique_ptr<EvaluationTree<double>> tree_f;
+  std::unique_ptr<CompiledProgram<double>> prog_f;
+  std::unique_ptr<EvaluationTree<std::int64_t>> tree_i;
+  std::unique_ptr<CompiledProgram<std::int64_t>> prog_i;
+  std::vector<Term<std::int64_t>> terms_i;  // canonical terms (int64 proof)
+
+  ProgramStats stats;
+  // int64: largest B such that all |x_v| <= B is provably wrap-free;
+  // variables absent from the polynomial get UINT64_MAX.
+  std::vector<std::uint64_t> i64_uniform_bound;
+
+  mutable std::mutex mu;
+  mutable std::array<std::unique_ptr<Artifact>, 4> artifacts;
+
+  /// Generated (and compiled) artifact for a domain; thread-safe.
+  Artifact& artifact(lower::Domain d, bool need_cubin) const;
+  /// Loaded kernel handle + global-tier coefficients on `device`.
+  Artifact& loaded(lower::Domain d, int device) const;
+};
+
+/// Overflow proof for the exact int64 path: every intermediate of the walk
+/// (fused or strict) is a partial sum of terms c_t * prod x_v^(a_tv - s_v),
+/// bounded by M = sum_t |c_t| prod_v max(1, X_v)^a_tv; powers are bounded by
+/// max(1, X_v)^max_e. Wrap-free iff M < 2^63 and every power < 2^63.
+bool i64_proof_holds(const Program& p, const std::uint64_t* bounds);
+
+}  // namespace polyeval::rt
