@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 batch polynomial evaluator (BASELINE.json metric).
+
+Default workload = BASELINE configs[1] (C2): dense univariate d1000 and d1023,
+fp64 coefficients U[-1,1], Estrin vs balanced, 1e7 points U[-1,1] per GPU.
+One step = the four (degree, scheme) programs each evaluated over the rank's
+1e7 points (4e7 point evaluations per GPU). Other configs: --config c1|c3|c4|c5.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+
+Under torchrun (N > 1) every rank evaluates its own 1e7-point shard of the
+N x 1e7 global batch (weak scaling, no data-path collective); timing is CUDA
+events on the launching stream bracketed by barrier + synchronize, max over
+ranks. `--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified reference library through its Evaluator API, all
+host threads) on the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--points", type=int, default=0, help="override points per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workloads
+
+def workloads(cfg: str):
+    from paper_1307_5655_b200 import workloads as W
+    if cfg == "c2":
+        return W.c2_all()
+    return [W.ALL[cfg]()]
+
+
+def metric_info(cfg: str):
+    return {
+        "c1": "C1: Horner dense d1000 fp64, 1e5 points U[-1,1] (launch-bound, parity case)",
+        "c2": "C2: dense d1000 + d1023 fp64 U[-1,1], Estrin vs balanced, 1e7 points U[-1,1]",
+        "c3": "C3: bivariate total-degree-40 int64 (861 terms), Horner/Horner, 1e7 points in [-2,2]^2",
+        "c4": "C4: trivariate sparse 10k terms N(0,1), balanced x3, 1e8 points U[-1,1]^3",
+        "c5": "C5: Estrin d200 interval, 1e8 intervals [x, x+1e-6]",
+    }[cfg]
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 — clocks are evidence, not a dependency
+            self._nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- dist
+
+def dist_setup(ngpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- CPU legs
+
+def cpu_reference_rate(wls, sample_points: int, threads: int, pts_cache=None):
+    """points/s of the unmodified reference (oracle/_ref) on `threads` host
+    threads, one Evaluator session per thread over contiguous shards."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    total_pts, total_s = 0, 0.0
+    for wl in wls:
+        ref = pyoracle.Reference(wl.poly, wl.schemes)
+        if wl.domain == "interval":
+            lo, hi = wl.points(sample_points)
+            t = time.perf_counter()
+            ref.eval_interval(lo, hi, threads)
+        elif wl.domain == "i64":
+            pts = wl.points(sample_points)
+            t = time.perf_counter()
+            ref.eval_i64(pts, threads)
+        else:
+            pts = wl.points(sample_points)
+            t = time.perf_counter()
+            ref.eval_f64(pts, threads)
+        total_s += time.perf_counter() - t
+        total_pts += sample_points
+    return total_pts / total_s, total_s
+
+
+def calibrate_sample(wls, threads, budget_s):
+    rate, _ = cpu_reference_rate(wls, 256 * threads, threads)
+    n = int(rate * budget_s / 1)  # total points over all programs
+    per = max(threads * 64, n // len(wls))
+    return per
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- reference arm
+
+def run_reference_arm(args, world, rank):
+    wls = workloads(args.config)
+    if rank != 0:
+        return
+    threads = host_threads()
+    per_step = calibrate_sample(wls, threads, budget_s=max(1.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_reference_rate(wls, per_step, threads)
+    t0 = time.perf_counter()
+    pts = 0
+    for _ in range(args.steps):
+        cpu_reference_rate(wls, per_step, threads)
+        pts += per_step * len(wls)
+    el = time.perf_counter() - t0
+    value = pts / el
+    terms = float(np.mean([wl.poly.coefficients.shape[0] for wl in wls]))
+    line = {
+        "impl": "reference",
+        "metric": "points/s", "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": {"c3": "int64", "c5": "f64-interval"}.get(args.config, "f64"),
+        "data": "synthetic (seeded PCG64, explicit transforms)",
+        "config": {"workload": metric_info(args.config), "programs": [w.name for w in wls],
+                   "points_per_step": per_step * len(wls)},
+        "term_evals_per_s": value * terms,
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{per_step} points per program per step, {len(wls)} programs, "
+                                   "unmodified reference Evaluator<D>, one session per thread"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- native arm
+
+def run_native(args, world, rank, local):
+    import torch
+    import paper_1307_5655_b200 as pe
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    wls = workloads(args.config)
+    n = args.points or wls[0].n_points
+    domain = wls[0].domain
+
+    # programs + kernels (compile is setup, outside the timed region)
+    t_setup = time.perf_counter()
+    progs = [pe.compile(w.poly, w.schemes) for w in wls]
+    if domain == "interval":
+        evs = [pe.Evaluator(pe.IntervalDomain(), p, device=local) for p in progs]
+    elif domain == "i64":
+        evs = [pe.Evaluator(pe.BigIntDomain(), p, device=local) for p in progs]
+    else:
+        evs = [pe.Evaluator(pe.DoubleDomain(), p, device=local) for p in progs]
+
+    # per-rank shard of the global batch: distinct seeded points per rank
+    if domain == "interval":
+        lo, hi = wls[0].points(n, offset_tag=7919 * rank)
+        x_lo = [torch.from_numpy(a).to(dev) for a in lo]
+        x_hi = [torch.from_numpy(a).to(dev) for a in hi]
+        host_in = ([torch.from_numpy(a).pin_memory() for a in lo],
+                   [torch.from_numpy(a).pin_memory() for a in hi])
+        inputs = (x_lo, x_hi)
+        outs = [(torch.empty(n, dtype=torch.float64, device=dev),
+                 torch.empty(n, dtype=torch.float64, device=dev)) for _ in wls]
+        bytes_in = 16 * n * wls[0].poly.nvars
+        bytes_out = 16 * n
+    else:
+        pts = wls[0].points(n, offset_tag=7919 * rank)
+        inputs = [torch.from_numpy(a).to(dev) for a in pts]
+        host_in = [torch.from_numpy(a).pin_memory() for a in pts]
+        dt = torch.int64 if domain == "i64" else torch.float64
+        outs = [torch.empty(n, dtype=dt, device=dev) for _ in wls]
+        bytes_in = 8 * n * wls[0].poly.nvars
+        bytes_out = 8 * n
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    for e, o in zip(evs, outs):  # JIT + load + first launch
+        e.evaluate(inputs, out=o, stream=sptr)
+    torch.cuda.synchronize(dev)
+    setup_s = time.perf_counter() - t_setup
+
+    # FP64 / int64-MAD pipe peak on this GPU (roofline denominator)
+    import ctypes as C
+    from paper_1307_5655_b200 import _lib as L
+    peak, sms = C.c_double(), C.c_int32()
+    L.check(L.lib().pe_measure_peak(local, 1 if domain == "i64" else 0, C.byref(peak), C.byref(sms)))
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(events=None):
+        for i, (e, o) in enumerate(zip(evs, outs)):
+            if events is not None:
+                events[i][0].record(stream)
+            e.evaluate(inputs, out=o, stream=sptr)
+            if events is not None:
+                events[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    launches0 = pe.launch_count()
+    per_launch_ms = [[] for _ in wls]
+    t_total = 0.0
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()  # outside the timed interval: L2 cold at each step
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in wls]
+            barrier(world)
+            torch.cuda.synchronize(dev)
+            step(ev)
+            torch.cuda.synchronize(dev)
+            barrier(world)
+            ms = [a.elapsed_time(b) for a, b in ev]
+            for i, m in enumerate(ms):
+                per_launch_ms[i].append(m)
+            t_total += ev[0][0].elapsed_time(ev[-1][1])
+    launches = pe.launch_count() - launches0
+    t_total = max_over_ranks(t_total, world)
+    ms_step = t_total / args.steps
+    pts_step = n * len(wls) * world
+    value = pts_step / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (longest average launch)
+    avg = [statistics.mean(x) for x in per_launch_ms]
+    top = int(np.argmax(avg))
+    st = progs[top].kernel_stats(
+        {"f64": pe.DOMAIN_F64, "i64": pe.DOMAIN_I64, "interval": pe.DOMAIN_INTERVAL}[domain])
+    info = progs[top].info()
+    if domain == "f64":
+        algo_per_pt = info["walk_muls"] + info["power_muls"]
+        unit_ops = "DFMA"
+    elif domain == "i64":
+        algo_per_pt = info["walk_muls"]  # int64 MADs (adds fused)
+        unit_ops = "int64 MAD"
+    else:
+        algo_per_pt = 2 * info["walk_adds"] + 4 * (info["walk_muls"] + info["power_muls"])
+        unit_ops = "fp64 add/mul (interval endpoints)"
+    achieved = algo_per_pt * n / (avg[top] * 1e-3)  # ops/s
+    nominal = sms.value * 64 * 1.965e9
+    roofline = {
+        "bound": "fp64" if domain != "i64" else "int64_mad",
+        "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "Tops/s",
+        "frac": achieved / peak.value,
+        "peak_source": "measured live: pe_measure_peak microbenchmark (8 independent chains/thread, "
+                       "full occupancy) on this GPU; nominal FP64 FMA pipe = "
+                       f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes",
+        "ops": f"{algo_per_pt} {unit_ops} per point (SURVEY 8d F) x {n} points per launch",
+        "kernel": f"pe_walk_{domain} [{wls[top].name}]",
+        "issued_fp64_per_point": st["fp_ops"], "issued_int64_per_point": st["int_ops"],
+        "hbm_frac": (bytes_in + bytes_out) / (avg[top] * 1e-3) / 1e9 /
+                    json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else None,
+        "traffic": None,
+        "per_program_ms": {w.name: round(a, 4) for w, a in zip(wls, avg)},
+    }
+
+    # e2e through the public API with HOST (pinned) buffers: H2D + walk + D2H
+    e2e = None
+    if not args.no_e2e:
+        if domain == "interval":
+            hout = [(torch.empty(n, dtype=torch.float64).pin_memory(),
+                     torch.empty(n, dtype=torch.float64).pin_memory()) for _ in wls]
+            hin = (tuple(a.numpy() for a in host_in[0]), tuple(a.numpy() for a in host_in[1]))
+        else:
+            dt = torch.int64 if domain == "i64" else torch.float64
+            hout = [torch.empty(n, dtype=dt).pin_memory() for _ in wls]
+            hin = [a.numpy() for a in host_in]
+
+        def e2e_step():
+            for e, o in zip(evs, hout):
+                if domain == "interval":
+                    e.evaluate(hin, out=(o[0].numpy(), o[1].numpy()))
+                else:
+                    e.evaluate(hin, out=o.numpy())
+
+        e2e_step()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps // 2)):
+            e2e_step()
+        el = time.perf_counter() - t0
+        el = max_over_ranks(el, world)
+        k = max(1, args.steps // 2)
+        e2e = {"value": pts_step / (el / k), "unit": "points/s",
+               "h2d_bytes_per_step": bytes_in * len(wls), "d2h_bytes_per_step": bytes_out * len(wls),
+               "path": "pe_eval_* with pinned host buffers (3-slot chunked H2D/walk/D2H pipeline)"}
+
+    # CPU baseline: the unmodified reference on this box's host cores (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = host_threads()
+            per = calibrate_sample(wls, threads, args.cpu_seconds)
+            rate, secs = cpu_reference_rate(wls, per, threads)
+            cpu = {"value": rate, "unit": "points/s", "cores": threads, "kind": "reference",
+                   "sample": f"{per} points per program x {len(wls)} programs "
+                             f"({secs:.1f} s), unmodified reference Evaluator<D> per thread"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "points/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    terms = float(np.mean([wl.poly.coefficients.shape[0] for wl in wls]))
+    line = {
+        "metric": "points/s", "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"c3": "int64", "c5": "f64-interval"}.get(args.config, "f64"),
+        "data": "synthetic (seeded PCG64, explicit transforms; SURVEY 8d)",
+        "config": {"workload": metric_info(args.config), "programs": [w.name for w in wls],
+                   "points_per_gpu": n, "point_evals_per_step": pts_step,
+                   "parallelism": f"points sharded, {world} rank(s), no collective",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "term_evals_per_s": value * terms,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks.summary(),
+        "setup_s": setup_s,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        # CPU arm: rank 0 alone runs it, other ranks exit without work
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    try:
+        run_native(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -168,6 +168,11 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
                            const double* const* hi, size_t n, double* out_lo,
                            double* out_hi, const pe_exec* exec);
 
+/* Roofline denominator microbenchmark on `device`: kind 0 = DFMA/s
+ * (FP64 FMA pipe), kind 1 = 64-bit integer multiply-adds/s. *sms receives the
+ * SM count. Synchronous; for bench.py, not a hot-path call. */
+pe_status pe_measure_peak(int32_t device, int32_t kind, double* ops_per_s, int32_t* sms);
+
 /* Waits for all work this library queued on `exec` (device + stream). */
 pe_status pe_synchronize(const pe_exec* exec);
 

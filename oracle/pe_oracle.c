@@ -250,6 +250,9 @@ static otree* build_multi_at(oterm* t, size_t n, uint32_t nv, uint32_t depth,
       g[m].e[depth] = 0;
       ++m;
     }
+    uint32_t** gown = (uint32_t**)malloc((m ? m : 1) * sizeof(uint32_t*));
+    const size_t graw = m;
+    for (size_t i = 0; i < m; ++i) gown[i] = g[i].e;
     m = canonicalize(g, m, nv);
     pr[k].exp = ex[k];
     int constant = m == 0;
@@ -264,7 +267,8 @@ static otree* build_multi_at(oterm* t, size_t n, uint32_t nv, uint32_t depth,
       pr[k].sub = build_multi_at(g, m, nv, depth + 1, schemes);
       if (!pr[k].sub) return NULL;
     }
-    for (size_t i = 0; i < m; ++i) free(g[i].e);
+    for (size_t i = 0; i < graw; ++i) free(gown[i]);
+    free(gown);
   }
   free(g);
   otree* tr = tree_from_proto(pr, nex, &schemes[depth], depth);
@@ -453,6 +457,8 @@ void* oracle_create(const uint32_t* exps, const void* coeffs, size_t nterms, uin
     t[i].e = (uint32_t*)malloc(nvars * sizeof(uint32_t));
     memcpy(t[i].e, exps + i * nvars, nvars * sizeof(uint32_t));
   }
+  uint32_t** owned = (uint32_t**)malloc((nterms ? nterms : 1) * sizeof(uint32_t*));
+  for (size_t i = 0; i < nterms; ++i) owned[i] = t[i].e; /* canonicalize permutes/merges */
   size_t n = canonicalize(t, nterms, nvars);
   otree* tr;
   if (nvars == 1) {
@@ -484,7 +490,8 @@ void* oracle_create(const uint32_t* exps, const void* coeffs, size_t nterms, uin
       tr = build_multi_at(t, n, nvars, 0, sch);
     }
   }
-  for (size_t i = 0; i < nterms; ++i) free(t[i].e);
+  for (size_t i = 0; i < nterms; ++i) free(owned[i]);
+  free(owned);
   free(t);
   free(sch);
   if (!tr) return NULL;

@@ -75,6 +75,8 @@ EXPORTS = [
     ("pe_eval_interval", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p,
       C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_measure_peak", C.c_int,
+     [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     ("pe_synchronize", C.c_int, [C.POINTER(pe_exec)]),
     ("pe_launch_count", C.c_uint64, []),
     ("pe_last_error", C.c_char_p, []),

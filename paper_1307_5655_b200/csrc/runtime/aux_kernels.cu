@@ -52,3 +52,75 @@ extern "C" cudaError_t pe_launch_max_abs_i64(const long long* x, size_t n,
   max_abs_i64_kernel<<<grid, 256, 0, stream>>>(x, n, out);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Pipe-peak microbenchmarks: the roofline denominators for the FP64-bound
+// (C1/C2/C4/C5) and int64-MAD-bound (C3) walks. MEASURED_PEAKS.json carries
+// only HBM and bf16 peaks, so bench.py measures these live on the same GPU.
+// Each thread runs 8 independent dependency chains (enough ILP to saturate the
+// pipe at full occupancy); the result is folded into a store so nothing is
+// dead-code eliminated.
+namespace {
+
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = fma(r[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += r[k];
+  if (s == 1234.5) out[0] = s;  // never true in practice; keeps the chains live
+}
+
+__global__ void __launch_bounds__(256) imad64_peak_kernel(long long* out, int iters, long long a,
+                                                          long long b) {
+  long long r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = threadIdx.x + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = r[k] * a + b;
+  }
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s ^= r[k];
+  if (s == 0x123456789LL) out[0] = s;
+}
+
+}  // namespace
+
+// ops/s for one (warm) launch; 1 op = one DFMA / one 64-bit multiply-add
+extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s) {
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  void* buf = nullptr;
+  cudaError_t e = cudaMalloc(&buf, 64);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  float best_ms = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(t0);
+    if (kind == 0) {
+      dfma_peak_kernel<<<blocks, threads>>>(static_cast<double*>(buf), iters, 0.999999, 1e-7);
+    } else {
+      imad64_peak_kernel<<<blocks, threads>>>(static_cast<long long*>(buf), iters,
+                                              0x5851F42D4C957F2DLL, 0x14057B7EF767814FLL);
+    }
+    cudaEventRecord(t1);
+    cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    if (rep > 0 && ms < best_ms) best_ms = ms;  // rep 0 is the warm-up
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(buf);
+  *ops_per_s = static_cast<double>(blocks) * threads * iters * 8 / (best_ms * 1e-3);
+  return e;
+}
