@@ -196,7 +196,8 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   for (auto& v : vals) args.push_back(&v);
   if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
   const std::uint64_t block = img.block;
-  const std::uint64_t grid = (la.n + block - 1) / block;
+  const std::uint64_t tile = block * img.lanes;
+  const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
   check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.kernel),
                               dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),

@@ -1,10 +1,17 @@
 // PTX emitter: lowered stream -> sm_100a kernel text.
 //
-// Thread i evaluates point i (SoA coordinates, one coalesced 8-byte load per
-// variable per thread). The power DAG and the walk are straight-line code over
-// PTX virtual registers; ptxas performs the physical register allocation,
-// which is exactly the job the reference's lazy heights do for its heap
-// register file (tree.hpp:68-77). Per-domain arithmetic:
+// Each thread evaluates P points ("lanes") of one CTA tile: point
+// tile_base + lane * blockDim + tid, so every coordinate load and result
+// store of a warp is one coalesced 256-byte access. The walk is emitted once
+// per lane, interleaved op by op: a coefficient is loaded from the constant
+// bank once and feeds P independent FMAs, which (a) divides the per-thread
+// constant-load traffic — the MIO-queue limiter of a one-point-per-thread walk
+// (profiles/) — by P and (b) gives the FP64 pipe P independent dependency
+// chains. The power DAG and the walk are straight-line code over PTX virtual
+// registers; ptxas does the physical allocation, which is the job the
+// reference's lazy heights do for its heap register file (tree.hpp:68-77).
+//
+// Per-domain arithmetic:
 //   F64 / F64Strict  add.rn / mul.rn / fma.rn (strict streams contain no FMA,
 //                    and .rn instructions are never contracted by ptxas)
 //   I64              add.s64 / mul.lo.s64 / mad.lo.s64 (wrap-free: the host
@@ -15,6 +22,7 @@
 #include "lower/ptx.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -32,6 +40,19 @@ const char* domain_name(Domain d) {
     case Domain::Interval: return "interval";
   }
   return "?";
+}
+
+std::uint32_t default_lanes(Domain d, std::uint64_t ops, std::uint32_t powers) {
+  if (const char* env = std::getenv("PE_LANES")) {
+    const int v = std::atoi(env);
+    if (v >= 1 && v <= 8) return static_cast<std::uint32_t>(v);
+  }
+  (void)ops;
+  if (d == Domain::Interval) return 1;
+  // very wide programs already carry many independent chains and large power
+  // tables; keep register pressure in check
+  if (powers > 32) return 2;
+  return 4;
 }
 
 namespace {
@@ -66,12 +87,13 @@ IvCoef inject(std::int64_t c) {
 template <typename C>
 class Emitter {
  public:
-  Emitter(const Stream<C>& s, Domain d) : s_(s), d_(d) {}
+  Emitter(const Stream<C>& s, Domain d, std::uint32_t lanes) : s_(s), d_(d), P_(lanes) {}
 
   KernelImage run() {
     KernelImage img;
     img.domain = d_;
     img.nvars = s_.nvars;
+    img.lanes = P_;
     const bool iv = d_ == Domain::Interval;
     const bool i64 = d_ == Domain::I64;
     img.n_in = iv ? 2 * s_.nvars : s_.nvars;
@@ -87,7 +109,6 @@ class Emitter {
     img.param_words.assign(words_.begin() + n_const_, words_.begin() + n_const_ + n_param_);
     img.global_words.assign(words_.begin() + n_const_ + n_param_, words_.end());
 
-    body_.str("");
     emit_prologue();
     emit_powers();
     emit_walk();
@@ -96,8 +117,8 @@ class Emitter {
     std::ostringstream m;
     img.entry = std::string("pe_walk_") + domain_name(d_);
     m << "//\n// polyeval-b200 generated kernel: domain=" << domain_name(d_)
-      << " nvars=" << s_.nvars << " ops=" << s_.ops.size()
-      << " powers=" << s_.powers.size() << "\n//\n";
+      << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
+      << " lanes=" << P_ << "\n//\n";
     m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
     if (n_const_ > 0) {
       m << ".const .align 8 .b64 pe_coef[" << n_const_ << "] = {";
@@ -137,8 +158,6 @@ class Emitter {
  private:
   // ---------------- coefficient words ----------------
   void assign_words() {
-    // word table: f64/i64 one word per coefficient slot; interval lo/hi,
-    // shared when equal.
     coef_lo_.resize(s_.coefs.size());
     coef_hi_.resize(s_.coefs.size());
     std::unordered_map<std::uint64_t, std::uint32_t> dedup;
@@ -174,10 +193,11 @@ class Emitter {
     n_global_ = n - n_const_ - n_param_;
   }
 
-  const char* ty() const { return d_ == Domain::I64 ? "s64" : "f64"; }
   const char* ldty() const { return d_ == Domain::I64 ? "b64" : "f64"; }
+  const char* rty() const { return d_ == Domain::I64 ? "s64" : "f64"; }
+  static std::string ln(std::uint32_t lane) { return "_" + std::to_string(lane); }
 
-  // Loads coefficient word w into a fresh register, returns its name.
+  // Loads coefficient word w into a fresh register (shared by all lanes).
   std::string load_word(std::uint32_t w) {
     std::string r = "%c" + std::to_string(n_creg_++);
     if (w < n_const_) {
@@ -185,42 +205,51 @@ class Emitter {
     } else if (w < n_const_ + n_param_) {
       body_ << "  ld.param." << ldty() << " " << r << ", [pe_pcoef+" << 8 * (w - n_const_) << "];\n";
     } else {
-      body_ << "  ld.global.nc." << ldty() << " " << r << ", [%rd20+" << 8 * (w - n_const_ - n_param_)
-            << "];\n";
+      body_ << "  ld.global.nc." << ldty() << " " << r << ", [%rd20+"
+            << 8 * (w - n_const_ - n_param_) << "];\n";
     }
     return r;
   }
 
   // ---------------- operands ----------------
-  std::string reg(std::uint32_t id, bool hi = false) const {
-    if (d_ == Domain::Interval) return (hi ? "%vh" : "%vl") + std::to_string(id);
-    return "%v" + std::to_string(id);
+  std::string reg(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
+    if (d_ == Domain::Interval) return (hi ? "%vh" : "%vl") + std::to_string(id) + ln(lane);
+    return "%v" + std::to_string(id) + ln(lane);
   }
-  std::string pw(std::uint32_t id, bool hi = false) const {
-    if (d_ == Domain::Interval) return (hi ? "%ph" : "%pl") + std::to_string(id);
-    return "%q" + std::to_string(id);
+  std::string pw(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
+    if (d_ == Domain::Interval) return (hi ? "%ph" : "%pl") + std::to_string(id) + ln(lane);
+    return "%q" + std::to_string(id) + ln(lane);
   }
-  // scalar operand text (f64 / i64)
-  std::string opnd(const Operand& o) {
+  std::string xr(std::uint32_t v, std::uint32_t lane, bool hi = false) const {
+    if (d_ == Domain::Interval) return (hi ? "%xh" : "%xl") + std::to_string(v) + ln(lane);
+    return "%x" + std::to_string(v) + ln(lane);
+  }
+
+  // Coefficients are loaded once per op (before the lane loop) and shared.
+  struct Loaded {
+    std::string lo, hi;
+  };
+  Loaded load(const Operand& o) {
+    if (!o.is(Operand::Coef)) return {};
+    const std::string lo = load_word(coef_lo_[o.id]);
+    const std::string hi = coef_hi_[o.id] == coef_lo_[o.id] ? lo : load_word(coef_hi_[o.id]);
+    return {lo, hi};
+  }
+  std::string opnd(const Operand& o, const Loaded& l, std::uint32_t lane) const {
     switch (o.kind) {
-      case Operand::Reg: return reg(o.id);
-      case Operand::Pow: return pw(o.id);
-      case Operand::Coef: return load_word(coef_lo_[o.id]);
+      case Operand::Reg: return reg(o.id, lane);
+      case Operand::Pow: return pw(o.id, lane);
+      case Operand::Coef: return l.lo;
       case Operand::Zero: return d_ == Domain::I64 ? "0" : "0d0000000000000000";
       default: throw std::logic_error("bad operand");
     }
   }
-  // interval operand: pair of register texts
-  std::pair<std::string, std::string> iv(const Operand& o) {
+  std::pair<std::string, std::string> ivop(const Operand& o, const Loaded& l,
+                                           std::uint32_t lane) const {
     switch (o.kind) {
-      case Operand::Reg: return {reg(o.id, false), reg(o.id, true)};
-      case Operand::Pow: return {pw(o.id, false), pw(o.id, true)};
-      case Operand::Coef: {
-        const std::string lo = load_word(coef_lo_[o.id]);
-        const std::string hi =
-            coef_hi_[o.id] == coef_lo_[o.id] ? lo : load_word(coef_hi_[o.id]);
-        return {lo, hi};
-      }
+      case Operand::Reg: return {reg(o.id, lane, false), reg(o.id, lane, true)};
+      case Operand::Pow: return {pw(o.id, lane, false), pw(o.id, lane, true)};
+      case Operand::Coef: return {l.lo, l.hi};
       case Operand::Zero: return {"0d0000000000000000", "0d0000000000000000"};
       default: throw std::logic_error("bad operand");
     }
@@ -229,95 +258,122 @@ class Emitter {
   // ---------------- frame ----------------
   void emit_prologue() {
     const bool iv = d_ == Domain::Interval;
-    const std::uint32_t nin = iv ? 2 * s_.nvars : s_.nvars;
-    // thread -> point
+    // tile base = ctaid * (ntid * P) + tid; lane k at base + k * ntid
     body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
-          << "  mul.wide.u32 %rd1, %r1, %r2;\n  cvt.u64.u32 %rd2, %r3;\n"
-          << "  add.u64 %rd1, %rd1, %rd2;\n  ld.param.u64 %rd3, [pe_n];\n"
+          << "  mul.wide.u32 %rd1, %r1, %r2;\n  mul.lo.u64 %rd1, %rd1, " << P_ << ";\n"
+          << "  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
+          << "  ld.param.u64 %rd3, [pe_n];\n"
           << "  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n"
-          << "  shl.b64 %rd4, %rd1, 3;\n";
+          << "  sub.u64 %rd12, %rd3, 1;\n";  // last valid index (loads clamp to it)
     if (n_global_ > 0) {
       body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
     }
-    // coordinates (SoA): one coalesced 8-byte load per variable (per endpoint)
-    for (std::uint32_t i = 0; i < nin; ++i) {
-      std::string dst;
-      if (iv) {
-        dst = (i % 2 == 0 ? "%xl" : "%xh") + std::to_string(i / 2);
-      } else {
-        dst = "%x" + std::to_string(i);
-      }
-      body_ << "  ld.param.u64 %rd5, [pe_in" << i << "];\n  cvta.to.global.u64 %rd5, %rd5;\n"
-            << "  add.u64 %rd5, %rd5, %rd4;\n  ld.global.nc." << ldty() << " " << dst
-            << ", [%rd5];\n";
+    decls_ << "  .reg .b64 %ix<" << P_ << ">;\n  .reg .pred %pv<" << P_ << ">;\n";
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      body_ << "  cvt.u64.u32 %rd13, %r2;\n  mul.lo.u64 %rd13, %rd13, " << k << ";\n"
+            << "  add.u64 %rd13, %rd1, %rd13;\n  setp.lt.u64 %pv" << k << ", %rd13, %rd3;\n"
+            << "  min.u64 %rd13, %rd13, %rd12;\n  shl.b64 %ix" << k << ", %rd13, 3;\n";
     }
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        if (iv) {
+          decls_ << "  .reg .f64 " << xr(v, k, false) << ", " << xr(v, k, true) << ";\n";
+        } else {
+          decls_ << "  .reg ." << ldty() << " " << xr(v, k) << ";\n";
+        }
+      }
+    }
+    const std::uint32_t nin = iv ? 2 * s_.nvars : s_.nvars;
+    for (std::uint32_t i = 0; i < nin; ++i) {
+      body_ << "  ld.param.u64 %rd5, [pe_in" << i << "];\n  cvta.to.global.u64 %rd5, %rd5;\n";
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        const std::string dst = iv ? xr(i / 2, k, i % 2 == 1) : xr(i, k);
+        body_ << "  add.u64 %rd6, %rd5, %ix" << k << ";\n  ld.global.nc." << ldty() << " " << dst
+              << ", [%rd6];\n";
+      }
+    }
+    int label = 0;
     if (iv) {
-      decls_ << "  .reg .f64 %xl<" << s_.nvars << ">, %xh<" << s_.nvars << ">;\n";
       // Reference Interval(lo, hi) rejects NaN endpoints and lo > hi
       // (interval.cpp:21-26): flag and continue, the host reports EINVAL.
       for (std::uint32_t v = 0; v < s_.nvars; ++v) {
-        body_ << "  setp.le.f64 %p2, %xl" << v << ", %xh" << v << ";\n"
-              << "  @%p2 bra $Lok" << v << ";\n"
-              << "  ld.param.u64 %rd6, [pe_flag];\n  cvta.to.global.u64 %rd6, %rd6;\n"
-              << "  st.global.u32 [%rd6], 2;\n$Lok" << v << ":\n";
+        for (std::uint32_t k = 0; k < P_; ++k, ++label) {
+          body_ << "  setp.le.f64 %p2, " << xr(v, k, false) << ", " << xr(v, k, true) << ";\n"
+                << "  @%p2 bra $Lok" << label << ";\n"
+                << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n"
+                << "  @%pv" << k << " st.global.u32 [%rd7], 2;\n$Lok" << label << ":\n";
+        }
       }
-    } else {
-      decls_ << "  .reg ." << (d_ == Domain::I64 ? "b64" : "f64") << " %x<" << s_.nvars
-             << ">;\n";
     }
     if (d_ == Domain::I64) {
       // |x_v| <= bound_v, the range the host overflow proof assumed
       for (std::uint32_t v = 0; v < s_.nvars; ++v) {
-        body_ << "  ld.param.u64 %rd7, [pe_bound" << v << "];\n"
-              << "  abs.s64 %rd8, %x" << v << ";\n"
-              << "  setp.gt.u64 %p2, %rd8, %rd7;\n"
-              << "  @!%p2 bra $Lbok" << v << ";\n"
-              << "  ld.param.u64 %rd6, [pe_flag];\n  cvta.to.global.u64 %rd6, %rd6;\n"
-              << "  st.global.u32 [%rd6], 1;\n$Lbok" << v << ":\n";
+        body_ << "  ld.param.u64 %rd8, [pe_bound" << v << "];\n";
+        for (std::uint32_t k = 0; k < P_; ++k, ++label) {
+          body_ << "  abs.s64 %rd9, " << xr(v, k) << ";\n"
+                << "  setp.gt.u64 %p2, %rd9, %rd8;\n"
+                << "  @!%p2 bra $Lbok" << label << ";\n"
+                << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n"
+                << "  @%pv" << k << " st.global.u32 [%rd7], 1;\n$Lbok" << label << ":\n";
+        }
       }
     }
   }
 
   void emit_powers() {
     const std::size_t np = s_.powers.size();
-    if (np == 0) return;
-    if (d_ == Domain::Interval) {
-      decls_ << "  .reg .f64 %pl<" << np << ">, %ph<" << np << ">;\n";
-    } else {
-      decls_ << "  .reg ." << (d_ == Domain::I64 ? "s64" : "f64") << " %q<" << np << ">;\n";
+    for (std::size_t i = 0; i < np; ++i) {
+      const auto id = static_cast<std::uint32_t>(i);
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        if (d_ == Domain::Interval) {
+          decls_ << "  .reg .f64 " << pw(id, k, false) << ", " << pw(id, k, true) << ";\n";
+        } else {
+          decls_ << "  .reg ." << rty() << " " << pw(id, k) << ";\n";
+        }
+      }
     }
     for (std::size_t i = 0; i < np; ++i) {
       const Power& p = s_.powers[i];
-      if (p.exponent == 1) {
-        if (d_ == Domain::Interval) {
-          body_ << "  mov.f64 %pl" << i << ", %xl" << p.var << ";\n  mov.f64 %ph" << i << ", %xh"
-                << p.var << ";\n";
-        } else {
-          body_ << "  mov." << (d_ == Domain::I64 ? "b64" : "f64") << " %q" << i << ", %x" << p.var
-                << ";\n";
+      const auto id = static_cast<std::uint32_t>(i);
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        if (p.exponent == 1) {
+          if (d_ == Domain::Interval) {
+            body_ << "  mov.f64 " << pw(id, k, false) << ", " << xr(p.var, k, false) << ";\n"
+                  << "  mov.f64 " << pw(id, k, true) << ", " << xr(p.var, k, true) << ";\n";
+          } else {
+            body_ << "  mov." << ldty() << " " << pw(id, k) << ", " << xr(p.var, k) << ";\n";
+          }
+          continue;
         }
-        continue;
-      }
-      if (d_ == Domain::Interval) {
-        iv_mul(pw(static_cast<std::uint32_t>(i), false), pw(static_cast<std::uint32_t>(i), true),
-               {pw(p.lo, false), pw(p.lo, true)}, {pw(p.hi, false), pw(p.hi, true)});
-      } else if (d_ == Domain::I64) {
-        body_ << "  mul.lo.s64 %q" << i << ", %q" << p.lo << ", %q" << p.hi << ";\n";
-        ++int_ops_;
-      } else {
-        body_ << "  mul.rn.f64 %q" << i << ", %q" << p.lo << ", %q" << p.hi << ";\n";
-        ++fp_ops_;
+        if (d_ == Domain::Interval) {
+          iv_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
+                 {pw(p.hi, k, false), pw(p.hi, k, true)}, k == 0);
+        } else if (d_ == Domain::I64) {
+          body_ << "  mul.lo.s64 " << pw(id, k) << ", " << pw(p.lo, k) << ", " << pw(p.hi, k) << ";\n";
+          if (k == 0) ++int_ops_;
+        } else {
+          body_ << "  mul.rn.f64 " << pw(id, k) << ", " << pw(p.lo, k) << ", " << pw(p.hi, k) << ";\n";
+          if (k == 0) ++fp_ops_;
+        }
       }
     }
   }
 
   void emit_walk() {
-    if (s_.nregs > 0) {
-      if (d_ == Domain::Interval) {
-        decls_ << "  .reg .f64 %vl<" << s_.nregs << ">, %vh<" << s_.nregs << ">;\n";
-      } else {
-        decls_ << "  .reg ." << ty() << " %v<" << s_.nregs << ">;\n";
+    for (std::uint32_t id = 0; id < s_.nregs; ++id) {
+      std::ostringstream line;
+      line << "  .reg .f64 ";
+      if (d_ == Domain::I64) line.str("  .reg .s64 ");
+      line.seekp(0, std::ios_base::end);
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        if (d_ == Domain::Interval) {
+          line << (k ? ", " : "") << reg(id, k, false) << ", " << reg(id, k, true);
+        } else {
+          line << (k ? ", " : "") << reg(id, k);
+        }
       }
+      line << ";\n";
+      decls_ << line.str();
     }
     for (const Op& op : s_.ops) {
       if (d_ == Domain::Interval) {
@@ -329,59 +385,49 @@ class Emitter {
   }
 
   void emit_scalar_op(const Op& op) {
-    const std::string d = reg(op.dst);
-    if (d_ == Domain::I64) {
+    const Loaded la = load(op.a), lb = load(op.b), lc = load(op.c);
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      const std::string d = reg(op.dst, k);
+      const std::string a = opnd(op.a, la, k), b = opnd(op.b, lb, k);
+      if (d_ == Domain::I64) {
+        switch (op.kind) {
+          case OpKind::Add:
+            if (op.a.is(Operand::Zero)) {
+              body_ << "  mov.b64 " << d << ", " << b << ";\n";
+            } else {
+              body_ << "  add.s64 " << d << ", " << a << ", " << b << ";\n";
+              if (k == 0) ++int_ops_;
+            }
+            break;
+          case OpKind::Mul:
+            body_ << "  mul.lo.s64 " << d << ", " << a << ", " << b << ";\n";
+            if (k == 0) ++int_ops_;
+            break;
+          case OpKind::Fma:
+            body_ << "  mad.lo.s64 " << d << ", " << a << ", " << b << ", " << opnd(op.c, lc, k)
+                  << ";\n";
+            if (k == 0) ++int_ops_;
+            break;
+        }
+        continue;
+      }
       switch (op.kind) {
-        case OpKind::Add: {
-          if (op.a.is(Operand::Zero)) {
-            body_ << "  mov.b64 " << d << ", " << opnd(op.b) << ";\n";
-          } else {
-            const std::string a = opnd(op.a), b = opnd(op.b);
-            body_ << "  add.s64 " << d << ", " << a << ", " << b << ";\n";
-            ++int_ops_;
-          }
+        case OpKind::Add:
+          body_ << "  add.rn.f64 " << d << ", " << a << ", " << b << ";\n";
           break;
-        }
-        case OpKind::Mul: {
-          const std::string a = opnd(op.a), b = opnd(op.b);
-          body_ << "  mul.lo.s64 " << d << ", " << a << ", " << b << ";\n";
-          ++int_ops_;
+        case OpKind::Mul:
+          body_ << "  mul.rn.f64 " << d << ", " << a << ", " << b << ";\n";
           break;
-        }
-        case OpKind::Fma: {
-          const std::string a = opnd(op.a), b = opnd(op.b), c = opnd(op.c);
-          body_ << "  mad.lo.s64 " << d << ", " << a << ", " << b << ", " << c << ";\n";
-          ++int_ops_;
+        case OpKind::Fma:
+          body_ << "  fma.rn.f64 " << d << ", " << a << ", " << b << ", " << opnd(op.c, lc, k) << ";\n";
           break;
-        }
       }
-      return;
+      if (k == 0) ++fp_ops_;
     }
-    switch (op.kind) {
-      case OpKind::Add: {
-        const std::string a = opnd(op.a), b = opnd(op.b);
-        body_ << "  add.rn.f64 " << d << ", " << a << ", " << b << ";\n";
-        break;
-      }
-      case OpKind::Mul: {
-        const std::string a = opnd(op.a), b = opnd(op.b);
-        body_ << "  mul.rn.f64 " << d << ", " << a << ", " << b << ";\n";
-        break;
-      }
-      case OpKind::Fma: {
-        const std::string a = opnd(op.a), b = opnd(op.b), c = opnd(op.c);
-        body_ << "  fma.rn.f64 " << d << ", " << a << ", " << b << ", " << c << ";\n";
-        break;
-      }
-    }
-    ++fp_ops_;
   }
 
   // ---------------- interval primitives ----------------
-  std::string tmp_f() {
-    std::string r = "%tf" + std::to_string(n_tf_++);
-    return r;
-  }
+  std::string tmp_f() { return "%tf" + std::to_string(n_tf_++); }
   std::string tmp_u() { return "%tu" + std::to_string(n_tu_++); }
   std::string tmp_p() { return "%tp" + std::to_string(n_tp_++); }
 
@@ -409,7 +455,7 @@ class Emitter {
   // interval_add (reference interval.cpp:36-41)
   void iv_add(const std::string& dlo, const std::string& dhi,
               const std::pair<std::string, std::string>& a,
-              const std::pair<std::string, std::string>& b, bool a_is_zero) {
+              const std::pair<std::string, std::string>& b, bool a_is_zero, bool count) {
     if (a_is_zero) {
       // 0.0 + v == v up to the sign of zero, and nextafter maps +-0 alike
       next(dlo, b.first, false);
@@ -418,7 +464,7 @@ class Emitter {
       const std::string lo = tmp_f(), hi = tmp_f();
       body_ << "  add.rn.f64 " << lo << ", " << a.first << ", " << b.first << ";\n"
             << "  add.rn.f64 " << hi << ", " << a.second << ", " << b.second << ";\n";
-      fp_ops_ += 2;
+      if (count) fp_ops_ += 2;
       next(dlo, lo, false);
       next(dhi, hi, true);
     }
@@ -432,7 +478,6 @@ class Emitter {
           << "  setp.eq.f64 " << pz << ", " << x << ", 0d0000000000000000;\n"
           << "  setp.eq.or.f64 " << pz << ", " << y << ", 0d0000000000000000, " << pz << ";\n"
           << "  selp.f64 " << r << ", 0d0000000000000000, " << r << ", " << pz << ";\n";
-    fp_ops_ += 1;
     return r;
   }
 
@@ -440,9 +485,10 @@ class Emitter {
   // std::min / std::max initializer-list scan order, then one step outward.
   void iv_mul(const std::string& dlo, const std::string& dhi,
               const std::pair<std::string, std::string>& a,
-              const std::pair<std::string, std::string>& b) {
+              const std::pair<std::string, std::string>& b, bool count) {
     const std::string p1 = eprod(a.first, b.first), p2 = eprod(a.first, b.second),
                       p3 = eprod(a.second, b.first), p4 = eprod(a.second, b.second);
+    if (count) fp_ops_ += 4;
     const std::string mn = tmp_f(), mx = tmp_f();
     body_ << "  mov.f64 " << mn << ", " << p1 << ";\n  mov.f64 " << mx << ", " << p1 << ";\n";
     for (const std::string* p : {&p2, &p3, &p4}) {
@@ -457,31 +503,43 @@ class Emitter {
   }
 
   void emit_iv_op(const Op& op) {
-    const std::string dlo = reg(op.dst, false), dhi = reg(op.dst, true);
-    switch (op.kind) {
-      case OpKind::Add:
-        iv_add(dlo, dhi, iv(op.a), iv(op.b), op.a.is(Operand::Zero));
-        break;
-      case OpKind::Mul:
-        iv_mul(dlo, dhi, iv(op.a), iv(op.b));
-        break;
-      case OpKind::Fma:
-        throw std::logic_error("interval streams are strict (no FMA)");
+    const Loaded la = load(op.a), lb = load(op.b);
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      const std::string dlo = reg(op.dst, k, false), dhi = reg(op.dst, k, true);
+      switch (op.kind) {
+        case OpKind::Add:
+          iv_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero), k == 0);
+          break;
+        case OpKind::Mul:
+          iv_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), k == 0);
+          break;
+        case OpKind::Fma:
+          throw std::logic_error("interval streams are strict (no FMA)");
+      }
     }
   }
 
   void emit_epilogue() {
     const bool iv = d_ == Domain::Interval;
-    if (iv) {
-      std::pair<std::string, std::string> r = this->iv(s_.result);
-      body_ << "  ld.param.u64 %rd9, [pe_out0];\n  cvta.to.global.u64 %rd9, %rd9;\n"
-            << "  add.u64 %rd9, %rd9, %rd4;\n  st.global.f64 [%rd9], " << r.first << ";\n"
-            << "  ld.param.u64 %rd10, [pe_out1];\n  cvta.to.global.u64 %rd10, %rd10;\n"
-            << "  add.u64 %rd10, %rd10, %rd4;\n  st.global.f64 [%rd10], " << r.second << ";\n";
-    } else {
-      const std::string r = opnd(s_.result);
-      body_ << "  ld.param.u64 %rd9, [pe_out0];\n  cvta.to.global.u64 %rd9, %rd9;\n"
-            << "  add.u64 %rd9, %rd9, %rd4;\n  st.global." << ldty() << " [%rd9], " << r << ";\n";
+    const Loaded lr = load(s_.result);
+    for (std::uint32_t o = 0; o < (iv ? 2u : 1u); ++o) {
+      body_ << "  ld.param.u64 %rd9, [pe_out" << o << "];\n  cvta.to.global.u64 %rd9, %rd9;\n";
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        std::string val;
+        if (iv) {
+          auto r = ivop(s_.result, lr, k);
+          val = o == 0 ? r.first : r.second;
+        } else {
+          val = opnd(s_.result, lr, k);
+        }
+        if (val.rfind('%', 0) != 0) {  // immediate zero: stage through a register
+          const std::string t = tmp_u();
+          body_ << "  mov.b64 " << t << ", 0;\n";
+          val = t;
+        }
+        body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  @%pv" << k << " st.global."
+              << ldty() << " [%rd10], " << val << ";\n";
+      }
     }
     body_ << "$Ldone:\n  ret;\n";
     if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
@@ -492,6 +550,7 @@ class Emitter {
 
   const Stream<C>& s_;
   Domain d_;
+  std::uint32_t P_;
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
@@ -503,12 +562,15 @@ class Emitter {
 }  // namespace
 
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain) {
-  Emitter<C> e(stream, domain);
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain, std::uint32_t lanes) {
+  if (lanes == 0) {
+    lanes = default_lanes(domain, stream.ops.size(), static_cast<std::uint32_t>(stream.powers.size()));
+  }
+  Emitter<C> e(stream, domain, lanes);
   return e.run();
 }
 
-template KernelImage emit_ptx(const Stream<double>&, Domain);
-template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain);
+template KernelImage emit_ptx(const Stream<double>&, Domain, std::uint32_t);
+template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, std::uint32_t);
 
 }  // namespace polyeval::lower

@@ -43,13 +43,18 @@ struct KernelImage {
   std::vector<std::uint64_t> global_words;  // global-tier coefficient words
   std::uint32_t const_words = 0;
   std::uint32_t block = 128;
+  std::uint32_t lanes = 1;         // points per thread (tile = block * lanes)
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
   std::uint64_t int_ops = 0;       // int64 add/mul/mad per point
   std::uint64_t hash = 0;          // FNV-1a of `ptx`
 };
 
+/// Points per thread for a domain (PE_LANES overrides, 1..8).
+std::uint32_t default_lanes(Domain d, std::uint64_t ops, std::uint32_t powers);
+
+/// lanes == 0 selects default_lanes().
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain);
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain, std::uint32_t lanes = 0);
 
 }  // namespace polyeval::lower

@@ -1,0 +1,77 @@
+"""Lowering + PTX emission + in-process ptxas (no GPU needed).
+
+Checks that every config's specialised kernel compiles for sm_100a in every
+applicable domain, and that the fused fp64 stream issues exactly the
+algorithmic work F of SURVEY §8d (one DFMA per powered record + the power
+table), i.e. every add of the reference walk was fused or folded.
+"""
+import numpy as np
+import pytest
+
+import paper_1307_5655_b200 as pe
+from paper_1307_5655_b200 import workloads as W
+
+CASES = {
+    "c1": W.c1, "c2e1000": lambda: W.c2(1000, "estrin"), "c2b1000": lambda: W.c2(1000, "balanced"),
+    "c2e1023": lambda: W.c2(1023, "estrin"), "c3": W.c3, "c4": W.c4, "c5": W.c5,
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_kernels_compile_for_sm100a(name):
+    wl = CASES[name]()
+    prog = pe.compile(wl.poly, wl.schemes)
+    if wl.domain == "i64":
+        doms = [pe.DOMAIN_I64, pe.DOMAIN_F64, pe.DOMAIN_INTERVAL]
+    elif wl.domain == "interval":
+        doms = [pe.DOMAIN_INTERVAL, pe.DOMAIN_F64]
+    else:
+        doms = [pe.DOMAIN_F64] + ([pe.DOMAIN_F64_STRICT] if name != "c4" else [])
+    for d in doms:
+        assert prog.compile_only(d) > 1000
+        ptx = prog.ptx(d)
+        assert ".target sm_100a" in ptx
+
+
+@pytest.mark.parametrize("name", ["c1", "c2e1000", "c2b1000", "c2e1023", "c4"])
+def test_fused_fp64_issues_exactly_F(name):
+    wl = CASES[name]()
+    prog = pe.compile(wl.poly, wl.schemes)
+    inf = prog.info()
+    st = prog.kernel_stats(pe.DOMAIN_F64)
+    assert st["fp_ops"] == inf["walk_muls"] + inf["power_muls"]
+
+
+def test_int64_fused_issues_one_mad_per_record():
+    wl = W.c3()
+    prog = pe.compile(wl.poly, wl.schemes)
+    inf = prog.info()
+    assert prog.kernel_stats(pe.DOMAIN_I64)["int_ops"] == inf["walk_muls"] + inf["power_muls"]
+
+
+def test_strict_fp64_replays_reference_op_counts():
+    wl = W.c2(1000, "balanced")
+    prog = pe.compile(wl.poly, wl.schemes)
+    inf = prog.info()
+    # strict = the reference sequence: every walk add and mul + power table
+    assert prog.kernel_stats(pe.DOMAIN_F64_STRICT)["fp_ops"] == \
+        inf["walk_adds"] + inf["walk_muls"] + inf["power_muls"]
+
+
+def test_i64_domain_rejects_fp_coefficients():
+    wl = W.c2(1000, "estrin")
+    prog = pe.compile(wl.poly, wl.schemes)
+    with pytest.raises(ValueError):
+        prog.kernel_stats(pe.DOMAIN_I64)
+
+
+def test_coefficient_tiers_large_program():
+    # > 8000 distinct coefficient words spill from the constant bank into the
+    # parameter tier and then global memory; the kernel must still build
+    rng = np.random.default_rng(11)
+    n = 14_000
+    p = pe.Polynomial(np.arange(n - 1, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, n))
+    prog = pe.compile(p, pe.builtin_scheme("estrin"))
+    ptx = prog.ptx(pe.DOMAIN_F64)
+    assert "pe_pcoef" in ptx and "ld.global.nc.f64" in ptx
+    assert prog.compile_only(pe.DOMAIN_F64) > 0
