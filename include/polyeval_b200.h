@@ -91,7 +91,8 @@ typedef struct pe_exec {
   int32_t strict_f64;   /* pe_eval_f64: 1 = reference op order, bit-exact  */
   void* stream;         /* cudaStream_t for device-pointer calls; NULL = legacy default */
   int32_t synchronize;  /* device-pointer calls: 1 = wait for completion */
-  int32_t reserved;
+  int32_t i64_int_pipe; /* pe_eval_i64: 1 = always use the int64 IMAD kernel
+                           (default picks exact-on-FP64 when the 2^53 proof holds) */
   /* pe_eval_i64 only: caller-asserted per-variable bounds |x_v| <= bound[v]
    * (nvars entries; NULL = derive from the data with a device max-reduction). */
   const uint64_t* i64_bounds;

@@ -25,6 +25,7 @@ from ._lib import (  # noqa: F401
     DOMAIN_F64_STRICT,
     DOMAIN_I64,
     DOMAIN_INTERVAL,
+    DOMAIN_I64F,
     CudaError,
     LogicError,
     PolyEvalError,

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libpolyeval_b200.so")
 
 PE_OK, PE_EINVAL, PE_EOVERFLOW, PE_ECUDA, PE_ELOGIC = 0, 1, 2, 3, 4
 
-DOMAIN_F64, DOMAIN_F64_STRICT, DOMAIN_I64, DOMAIN_INTERVAL = 0, 1, 2, 3
+DOMAIN_F64, DOMAIN_F64_STRICT, DOMAIN_I64, DOMAIN_INTERVAL, DOMAIN_I64F = 0, 1, 2, 3, 4
 
 COEFF_F64, COEFF_I64 = 0, 1
 
@@ -29,7 +29,7 @@ class pe_exec(C.Structure):
         ("strict_f64", C.c_int32),
         ("stream", C.c_void_p),
         ("synchronize", C.c_int32),
-        ("reserved", C.c_int32),
+        ("i64_int_pipe", C.c_int32),
         ("i64_bounds", C.POINTER(C.c_uint64)),
     ]
 

@@ -243,7 +243,14 @@ class IntervalDomain:
 
 
 class BigIntDomain:
-    """Exact integer domain on a host-proven int64 range."""
+    """Exact integer domain on a host-proven int64 range.
+
+    By default the runtime evaluates on the FP64 FMA pipe whenever the host
+    proves every intermediate stays below 2^53 (exact), else with int64
+    multiply-adds; int_pipe=True forces the int64 kernel."""
+
+    def __init__(self, int_pipe: bool = False):
+        self.int_pipe = bool(int_pipe)
 
 
 def _is_torch_cuda(x) -> bool:
@@ -266,6 +273,7 @@ class Evaluator:
         ex.strict_f64 = 1 if isinstance(self.domain, DoubleDomain) and self.domain.strict else 0
         ex.stream = stream
         ex.synchronize = 1 if sync else 0
+        ex.i64_int_pipe = 1 if isinstance(self.domain, BigIntDomain) and self.domain.int_pipe else 0
         if bounds is not None:
             arr = (C.c_uint64 * len(bounds))(*[int(b) for b in bounds])
             ex.i64_bounds = arr

@@ -66,8 +66,8 @@ void check_cuda(cudaError_t e, const char* what) {
   }
 }
 
-bool i64_proof_holds(const Program& p, const std::uint64_t* bounds) {
-  const u128 limit = static_cast<u128>(1) << 63;
+bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bits) {
+  const u128 limit = static_cast<u128>(1) << limit_bits;
   std::vector<u128> base(p.nvars);
   for (std::uint32_t v = 0; v < p.nvars; ++v) base[v] = std::max<u128>(1, bounds[v]);
   u128 m = 0;
@@ -84,6 +84,8 @@ bool i64_proof_holds(const Program& p, const std::uint64_t* bounds) {
   }
   if (m >= limit) return false;
   for (std::uint32_t v = 0; v < p.nvars; ++v) {
+    // coordinates themselves must be exact in the working type
+    if (limit_bits < 63 && static_cast<u128>(bounds[v]) > limit) return false;
     if (sat_pow(base[v], max_e[v]) >= limit) return false;
   }
   return true;
@@ -91,21 +93,25 @@ bool i64_proof_holds(const Program& p, const std::uint64_t* bounds) {
 
 namespace {
 
-std::vector<std::uint64_t> uniform_bounds(const Program& p) {
+std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits) {
   std::vector<std::uint64_t> out(p.nvars, UINT64_MAX);
   std::vector<bool> present(p.nvars, false);
   for (const auto& t : p.terms_i) {
     for (std::uint32_t v = 0; v < p.nvars; ++v) present[v] = present[v] || t.exponents[v] > 0;
   }
-  std::uint64_t lo = 0, hi = (1ull << 62);
+  // the exact-FP64 path converts coordinates to double: they must be < 2^53
+  // even for variables absent from the polynomial
+  const std::uint64_t absent = limit_bits == 53 ? (1ull << 53) : UINT64_MAX;
+  for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = absent;
+  std::uint64_t lo = 0, hi = limit_bits == 53 ? (1ull << 53) : (1ull << 62);
   std::vector<std::uint64_t> probe(p.nvars);
   auto ok = [&](std::uint64_t b) {
     for (std::uint32_t v = 0; v < p.nvars; ++v) probe[v] = present[v] ? b : 0;
-    return i64_proof_holds(p, probe.data());
+    return i64_proof_holds(p, probe.data(), limit_bits);
   };
   if (!ok(0)) {
     lo = 0;
-    for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? 0 : UINT64_MAX;
+    for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? 0 : absent;
     // even X = 1 overflows: every evaluation is refused
     return out;
   }
@@ -113,7 +119,7 @@ std::vector<std::uint64_t> uniform_bounds(const Program& p) {
     const std::uint64_t mid = lo + (hi - lo + 1) / 2;
     if (ok(mid)) lo = mid; else hi = mid - 1;
   }
-  for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? lo : UINT64_MAX;
+  for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? lo : absent;
   return out;
 }
 
@@ -129,7 +135,7 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
       auto s = strict ? lower::lower_strict(*prog_i) : lower::lower_fused(*prog_i);
       a->image = lower::emit_ptx(s, d);
     } else {
-      if (d == lower::Domain::I64) {
+      if (d == lower::Domain::I64 || d == lower::Domain::I64F) {
         throw std::invalid_argument("pe_eval_i64 needs a program with int64 coefficients");
       }
       auto s = strict ? lower::lower_strict(*prog_f) : lower::lower_fused(*prog_f);
@@ -445,7 +451,8 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
     if (p.integer) {
       build_program(p, exponents, static_cast<const std::int64_t*>(coeffs), nterms, nvars, schemes,
                     p.tree_i, p.prog_i);
-      p.i64_uniform_bound = uniform_bounds(p);
+      p.i64_uniform_bound = uniform_bounds(p, 63);
+      p.i53_uniform_bound = uniform_bounds(p, 53);
     } else {
       const double* c = static_cast<const double*>(coeffs);
       for (size_t t = 0; t < nterms; ++t) {
@@ -545,7 +552,7 @@ pe_status pe_program_dot(const pe_program* program, char* out, size_t cap, size_
 }
 
 static lower::Domain to_domain(int32_t d) {
-  if (d < 0 || d > 3) throw std::invalid_argument("unknown domain");
+  if (d < 0 || d > 4) throw std::invalid_argument("unknown domain");
   return static_cast<lower::Domain>(d);
 }
 
@@ -675,16 +682,34 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
     MemKind kind;
     const int dev = resolve_device(exec, out, &kind);
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
-    const Artifact& a = p.loaded(lower::Domain::I64, dev);
     std::vector<const void*> ins(coords, coords + p.nvars);
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool caller_bounds = exec && exec->i64_bounds;
+    const bool force_int = exec && exec->i64_int_pipe;
     std::vector<std::uint64_t> bounds =
         caller_bounds ? std::vector<std::uint64_t>(exec->i64_bounds, exec->i64_bounds + p.nvars)
                       : p.i64_uniform_bound;
     if (caller_bounds && !i64_proof_holds(p, bounds.data())) {
       return fail(PE_EOVERFLOW, "int64 range proof fails for the asserted coordinate bounds");
     }
+    // Tier 1: every intermediate provably below 2^53 -> exact integer
+    // arithmetic on the FP64 FMA pipe (one DFMA per record instead of a
+    // 3-IMAD 64-bit multiply-add). Same bits as the int64 kernel.
+    const std::vector<std::uint64_t> b53 = caller_bounds ? bounds : p.i53_uniform_bound;
+    if (!force_int && i64_proof_holds(p, b53.data(), 53)) {
+      const Artifact& af = p.loaded(lower::Domain::I64F, dev);
+      Flag flag(s);
+      LaunchArgs la;
+      la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
+      la.bounds = b53;
+      run_batch(af, dev, kind, n, ins, {out}, la, s, false);
+      if (flag.read() == 0) return PE_OK;
+      if (caller_bounds) {
+        return fail(PE_EOVERFLOW, "a coordinate exceeds the asserted int64 bound");
+      }
+    }
+    // Tier 2: int64 multiply-adds, wrap-free by the 2^63 proof.
+    const Artifact& a = p.loaded(lower::Domain::I64, dev);
     for (int attempt = 0; attempt < 2; ++attempt) {
       Flag flag(s);
       LaunchArgs la;

@@ -38,21 +38,41 @@ const char* domain_name(Domain d) {
     case Domain::F64Strict: return "f64strict";
     case Domain::I64: return "i64";
     case Domain::Interval: return "interval";
+    case Domain::I64F: return "i64f";
   }
   return "?";
 }
 
-std::uint32_t default_lanes(Domain d, std::uint64_t ops, std::uint32_t powers) {
-  if (const char* env = std::getenv("PE_LANES")) {
-    const int v = std::atoi(env);
-    if (v >= 1 && v <= 8) return static_cast<std::uint32_t>(v);
-  }
+KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
+                          std::uint64_t distinct_coefs) {
+  // Measured on B200 (profiles/r1_shape_sweep.txt): the fp64 walk of a
+  // one-point-per-thread kernel is bound by per-thread constant loads (MIO);
+  // P points per thread share each coefficient load. One 512-thread CTA per
+  // SM (ptxas capped at 128 registers) beats several 128-thread CTAs.
+  KernelShape s;
   (void)ops;
-  if (d == Domain::Interval) return 1;
-  // very wide programs already carry many independent chains and large power
-  // tables; keep register pressure in check
-  if (powers > 32) return 2;
-  return 4;
+  if (d == Domain::Interval) {
+    s = {1, 512, 32};  // integer-pipe bound; no coefficient pressure
+  } else if (powers > 32) {
+    // very wide programs (large power tables): registers are the limit
+    s = {1, 512, 32};
+  } else if (distinct_coefs < 64) {
+    // few distinct coefficients: ptxas encodes them as immediates or keeps
+    // them in uniform registers; independent sub-chains give enough ILP
+    s = {1, 128, 0};
+  } else {
+    s = {4, 512, 0};
+  }
+  auto env = [](const char* name, std::uint32_t lo, std::uint32_t hi, std::uint32_t& out) {
+    if (const char* e = std::getenv(name)) {
+      const long v = std::atol(e);
+      if (v >= static_cast<long>(lo) && v <= static_cast<long>(hi)) out = static_cast<std::uint32_t>(v);
+    }
+  };
+  env("PE_LANES", 1, 8, s.lanes);
+  env("PE_BLOCK", 32, 1024, s.block);
+  env("PE_SYNC", 0, 1u << 20, s.sync_every);
+  return s;
 }
 
 namespace {
@@ -87,15 +107,17 @@ IvCoef inject(std::int64_t c) {
 template <typename C>
 class Emitter {
  public:
-  Emitter(const Stream<C>& s, Domain d, std::uint32_t lanes) : s_(s), d_(d), P_(lanes) {}
+  Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
+      : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every) {}
 
   KernelImage run() {
     KernelImage img;
     img.domain = d_;
     img.nvars = s_.nvars;
     img.lanes = P_;
+    img.block = block_;
     const bool iv = d_ == Domain::Interval;
-    const bool i64 = d_ == Domain::I64;
+    const bool i64 = d_ == Domain::I64 || d_ == Domain::I64F;
     img.n_in = iv ? 2 * s_.nvars : s_.nvars;
     img.n_out = iv ? 2 : 1;
     img.has_flag = iv || i64;
@@ -174,10 +196,12 @@ class Emitter {
         const IvCoef c = inject(s_.coefs[k]);
         coef_lo_[k] = word(bits_of(c.lo));
         coef_hi_[k] = word(bits_of(c.hi));
-      } else if (d_ == Domain::I64) {
+      } else if (d_ == Domain::I64 || d_ == Domain::I64F) {
         std::uint64_t w;
         if constexpr (std::is_same_v<C, std::int64_t>) {
-          w = static_cast<std::uint64_t>(s_.coefs[k]);
+          // I64F: |c| <= M < 2^53 by the host proof, so the double is exact
+          w = d_ == Domain::I64 ? static_cast<std::uint64_t>(s_.coefs[k])
+                                : bits_of(static_cast<double>(s_.coefs[k]));
         } else {
           throw std::invalid_argument("int64 domain needs integer coefficients");
         }
@@ -193,8 +217,12 @@ class Emitter {
     n_global_ = n - n_const_ - n_param_;
   }
 
+  // coefficient words / arithmetic registers
   const char* ldty() const { return d_ == Domain::I64 ? "b64" : "f64"; }
   const char* rty() const { return d_ == Domain::I64 ? "s64" : "f64"; }
+  // coordinates and results in memory
+  bool int_io() const { return d_ == Domain::I64 || d_ == Domain::I64F; }
+  const char* ioty() const { return int_io() ? "b64" : "f64"; }
   static std::string ln(std::uint32_t lane) { return "_" + std::to_string(lane); }
 
   // Loads coefficient word w into a fresh register (shared by all lanes).
@@ -223,6 +251,11 @@ class Emitter {
   std::string xr(std::uint32_t v, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) return (hi ? "%xh" : "%xl") + std::to_string(v) + ln(lane);
     return "%x" + std::to_string(v) + ln(lane);
+  }
+  // integer coordinate as loaded (I64: the arithmetic register itself)
+  std::string xi(std::uint32_t v, std::uint32_t lane) const {
+    if (d_ == Domain::I64F) return "%xi" + std::to_string(v) + ln(lane);
+    return xr(v, lane);
   }
 
   // Coefficients are loaded once per op (before the lane loop) and shared.
@@ -262,9 +295,13 @@ class Emitter {
     body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
           << "  mul.wide.u32 %rd1, %r1, %r2;\n  mul.lo.u64 %rd1, %rd1, " << P_ << ";\n"
           << "  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
-          << "  ld.param.u64 %rd3, [pe_n];\n"
-          << "  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n"
-          << "  sub.u64 %rd12, %rd3, 1;\n";  // last valid index (loads clamp to it)
+          << "  ld.param.u64 %rd3, [pe_n];\n";
+    if (sync_every_ == 0) {
+      // no CTA barriers: threads past the end leave immediately; with
+      // barriers every thread stays (clamped loads, predicated stores)
+      body_ << "  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n";
+    }
+    body_ << "  sub.u64 %rd12, %rd3, 1;\n";  // last valid index (loads clamp to it)
     if (n_global_ > 0) {
       body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
     }
@@ -278,6 +315,8 @@ class Emitter {
       for (std::uint32_t k = 0; k < P_; ++k) {
         if (iv) {
           decls_ << "  .reg .f64 " << xr(v, k, false) << ", " << xr(v, k, true) << ";\n";
+        } else if (d_ == Domain::I64F) {
+          decls_ << "  .reg .f64 " << xr(v, k) << ";\n  .reg .b64 " << xi(v, k) << ";\n";
         } else {
           decls_ << "  .reg ." << ldty() << " " << xr(v, k) << ";\n";
         }
@@ -287,9 +326,13 @@ class Emitter {
     for (std::uint32_t i = 0; i < nin; ++i) {
       body_ << "  ld.param.u64 %rd5, [pe_in" << i << "];\n  cvta.to.global.u64 %rd5, %rd5;\n";
       for (std::uint32_t k = 0; k < P_; ++k) {
-        const std::string dst = iv ? xr(i / 2, k, i % 2 == 1) : xr(i, k);
-        body_ << "  add.u64 %rd6, %rd5, %ix" << k << ";\n  ld.global.nc." << ldty() << " " << dst
+        const std::string dst = iv ? xr(i / 2, k, i % 2 == 1) : int_io() ? xi(i, k) : xr(i, k);
+        body_ << "  add.u64 %rd6, %rd5, %ix" << k << ";\n  ld.global.nc." << ioty() << " " << dst
               << ", [%rd6];\n";
+        if (d_ == Domain::I64F) {
+          // exact: |x| <= bound < 2^53 is checked below before any result is used
+          body_ << "  cvt.rn.f64.s64 " << xr(i, k) << ", " << xi(i, k) << ";\n";
+        }
       }
     }
     int label = 0;
@@ -305,12 +348,12 @@ class Emitter {
         }
       }
     }
-    if (d_ == Domain::I64) {
+    if (int_io()) {
       // |x_v| <= bound_v, the range the host overflow proof assumed
       for (std::uint32_t v = 0; v < s_.nvars; ++v) {
         body_ << "  ld.param.u64 %rd8, [pe_bound" << v << "];\n";
         for (std::uint32_t k = 0; k < P_; ++k, ++label) {
-          body_ << "  abs.s64 %rd9, " << xr(v, k) << ";\n"
+          body_ << "  abs.s64 %rd9, " << xi(v, k) << ";\n"
                 << "  setp.gt.u64 %p2, %rd9, %rd8;\n"
                 << "  @!%p2 bra $Lbok" << label << ";\n"
                 << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n"
@@ -375,7 +418,12 @@ class Emitter {
       line << ";\n";
       decls_ << line.str();
     }
+    std::uint64_t since_sync = 0;
     for (const Op& op : s_.ops) {
+      if (sync_every_ && ++since_sync == sync_every_) {
+        body_ << "  bar.sync 0;\n";
+        since_sync = 0;
+      }
       if (d_ == Domain::Interval) {
         emit_iv_op(op);
       } else {
@@ -536,9 +584,13 @@ class Emitter {
           const std::string t = tmp_u();
           body_ << "  mov.b64 " << t << ", 0;\n";
           val = t;
+        } else if (d_ == Domain::I64F) {  // exact integer-valued double -> int64
+          const std::string t = tmp_u();
+          body_ << "  cvt.rni.s64.f64 " << t << ", " << val << ";\n";
+          val = t;
         }
         body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  @%pv" << k << " st.global."
-              << ldty() << " [%rd10], " << val << ";\n";
+              << ioty() << " [%rd10], " << val << ";\n";
       }
     }
     body_ << "$Ldone:\n  ret;\n";
@@ -551,6 +603,8 @@ class Emitter {
   const Stream<C>& s_;
   Domain d_;
   std::uint32_t P_;
+  std::uint32_t block_;
+  std::uint32_t sync_every_;
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
@@ -562,15 +616,24 @@ class Emitter {
 }  // namespace
 
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain, std::uint32_t lanes) {
-  if (lanes == 0) {
-    lanes = default_lanes(domain, stream.ops.size(), static_cast<std::uint32_t>(stream.powers.size()));
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape) {
+  std::unordered_map<std::uint64_t, int> distinct;
+  for (const auto& c : stream.coefs) {
+    std::uint64_t w;
+    std::memcpy(&w, &c, 8);
+    distinct.emplace(w, 0);
   }
-  Emitter<C> e(stream, domain, lanes);
+  const KernelShape def = default_shape(domain, stream.ops.size(),
+                                        static_cast<std::uint32_t>(stream.powers.size()),
+                                        distinct.size());
+  if (shape.lanes == 0) shape.lanes = def.lanes;
+  if (shape.block == 0) shape.block = def.block;
+  if (shape.sync_every == 0) shape.sync_every = def.sync_every;
+  Emitter<C> e(stream, domain, shape);
   return e.run();
 }
 
-template KernelImage emit_ptx(const Stream<double>&, Domain, std::uint32_t);
-template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, std::uint32_t);
+template KernelImage emit_ptx(const Stream<double>&, Domain, KernelShape);
+template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, KernelShape);
 
 }  // namespace polyeval::lower

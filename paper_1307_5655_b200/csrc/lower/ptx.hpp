@@ -17,6 +17,10 @@ enum class Domain : int {
   F64Strict = 1,  // DoubleDomain, reference op sequence, bit-exact
   I64 = 2,        // BigIntDomain restricted to a proven int64 range, exact
   Interval = 3,   // IntervalDomain, reference op sequence, bit-exact
+  I64F = 4,       // BigIntDomain on a range proven below 2^53: the same exact
+                  // integer results, computed on the FP64 FMA pipe (every
+                  // intermediate is an integer of magnitude < 2^53, hence a
+                  // double, hence every DFMA/DMUL is exact)
 };
 
 const char* domain_name(Domain d);
@@ -50,11 +54,26 @@ struct KernelImage {
   std::uint64_t hash = 0;          // FNV-1a of `ptx`
 };
 
-/// Points per thread for a domain (PE_LANES overrides, 1..8).
-std::uint32_t default_lanes(Domain d, std::uint64_t ops, std::uint32_t powers);
+/// Launch shape of a specialised kernel.
+///  lanes       points per thread (P)
+///  block       threads per CTA; `.maxntid block` caps ptxas at 65536/block
+///              registers, so one CTA fills an SM's register file
+///  sync_every  walk ops between CTA barriers (0 = none). Straight-line walks
+///              are larger than the instruction caches; a barrier every few
+///              KB of code keeps all warps of the CTA inside one code window,
+///              so each instruction line is fetched once per SM, not per warp.
+struct KernelShape {
+  std::uint32_t lanes = 0;
+  std::uint32_t block = 0;
+  std::uint32_t sync_every = 0;
+};
 
-/// lanes == 0 selects default_lanes().
+/// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC
+/// environment variables override (tuning only).
+KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
+                          std::uint64_t distinct_coefs);
+
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain, std::uint32_t lanes = 0);
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape = {});
 
 }  // namespace polyeval::lower

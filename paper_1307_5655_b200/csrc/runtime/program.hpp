@@ -50,9 +50,11 @@ struct Program {
   // int64: largest B such that all |x_v| <= B is provably wrap-free;
   // variables absent from the polynomial get UINT64_MAX.
   std::vector<std::uint64_t> i64_uniform_bound;
+  // same, for the exact-on-FP64 path: every intermediate below 2^53
+  std::vector<std::uint64_t> i53_uniform_bound;
 
   mutable std::mutex mu;
-  mutable std::array<std::unique_ptr<Artifact>, 4> artifacts;
+  mutable std::array<std::unique_ptr<Artifact>, 5> artifacts;
 
   /// Generated (and compiled) artifact for a domain; thread-safe.
   Artifact& artifact(lower::Domain d, bool need_cubin) const;
@@ -63,7 +65,8 @@ struct Program {
 /// Overflow proof for the exact int64 path: every intermediate of the walk
 /// (fused or strict) is a partial sum of terms c_t * prod x_v^(a_tv - s_v),
 /// bounded by M = sum_t |c_t| prod_v max(1, X_v)^a_tv; powers are bounded by
-/// max(1, X_v)^max_e. Wrap-free iff M < 2^63 and every power < 2^63.
-bool i64_proof_holds(const Program& p, const std::uint64_t* bounds);
+/// max(1, X_v)^max_e. Wrap-free iff M < 2^63 and every power < 2^63; with
+/// limit_bits = 53 every intermediate is an exactly representable double.
+bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bits = 63);
 
 }  // namespace polyeval::rt

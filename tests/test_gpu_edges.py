@@ -1,0 +1,125 @@
+"""GPU edge cases: exact-integer tiers and overflow refusal, invalid intervals,
+special values, host/device pointer handling, determinism."""
+import numpy as np
+import pytest
+
+import paper_1307_5655_b200 as pe
+from paper_1307_5655_b200 import workloads as W
+import pyoracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, device):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+
+
+def test_i64_fp64_tier_equals_int_pipe(cuda_device):
+    wl = W.c3()
+    prog = pe.compile(wl.poly, wl.schemes)
+    pts = wl.points(100_003)
+    a = pe.Evaluator(pe.BigIntDomain(), prog).evaluate([_t(p, cuda_device) for p in pts])
+    b = pe.Evaluator(pe.BigIntDomain(int_pipe=True), prog).evaluate([_t(p, cuda_device) for p in pts])
+    ref = pyoracle.Oracle(wl.poly, wl.schemes).eval_i64(pts)
+    assert np.array_equal(a.cpu().numpy(), ref) and np.array_equal(b.cpu().numpy(), ref)
+
+
+def test_i64_large_values_use_int_pipe_exactly(cuda_device):
+    # values far above 2^53 but below 2^63: only the int64 kernel is exact
+    p = pe.Polynomial(np.array([[3], [1], [0]]), np.array([7, -3, 2**40], dtype=np.int64))
+    prog = pe.compile(p, pe.builtin_scheme("horner"))
+    x = np.array([2**17 + 5, -(2**17) - 11, 3, 0, 123456], dtype=np.int64)
+    got = pe.Evaluator(pe.BigIntDomain(), prog).evaluate([x])
+    ref = [7 * int(v) ** 3 - 3 * int(v) + 2**40 for v in x]
+    assert [int(g) for g in got] == ref
+
+
+def test_i64_retry_with_actual_maxima(cuda_device):
+    # uniform bound is limited by y^30; x far above it still provably fits
+    p = pe.Polynomial(np.array([[1, 0], [0, 30]]), np.array([1, 1], dtype=np.int64), ("x", "y"))
+    prog = pe.compile(p, [pe.builtin_scheme("balanced")] * 2)
+    x = np.array([2**40, -(2**40), 5], dtype=np.int64)
+    y = np.array([2, -2, 1], dtype=np.int64)
+    got = pe.Evaluator(pe.BigIntDomain(), prog).evaluate([_t(x, cuda_device), _t(y, cuda_device)])
+    assert [int(v) for v in got.cpu().numpy()] == [int(a) + int(b) ** 30 for a, b in zip(x, y)]
+
+
+def test_i64_overflow_is_refused(cuda_device):
+    p = pe.Polynomial(np.array([[40]]), np.array([3], dtype=np.int64))
+    prog = pe.compile(p, pe.builtin_scheme("estrin"))
+    with pytest.raises(OverflowError):
+        pe.Evaluator(pe.BigIntDomain(), prog).evaluate([np.array([1, 2, 4], dtype=np.int64)])
+    # INT64_MIN coordinate can never satisfy a bound
+    with pytest.raises(OverflowError):
+        pe.Evaluator(pe.BigIntDomain(), prog).evaluate([np.array([np.iinfo(np.int64).min])])
+
+
+def test_i64_caller_bounds(cuda_device):
+    wl = W.c3()
+    prog = pe.compile(wl.poly, wl.schemes)
+    ev = pe.Evaluator(pe.BigIntDomain(), prog)
+    pts = wl.points(1000)
+    ref = pyoracle.Oracle(wl.poly, wl.schemes).eval_i64(pts)
+    assert np.array_equal(ev.evaluate(pts, bounds=[2, 2]), ref)
+    with pytest.raises(OverflowError):  # asserted bound violated by the data
+        ev.evaluate(pts, bounds=[1, 1])
+    with pytest.raises(OverflowError):  # proof impossible for the asserted range
+        ev.evaluate(pts, bounds=[1 << 40, 1 << 40])
+
+
+def test_interval_rejects_invalid_endpoints(cuda_device):
+    wl = W.c5()
+    prog = pe.compile(wl.poly, wl.schemes)
+    ev = pe.Evaluator(pe.IntervalDomain(), prog)
+    with pytest.raises(ValueError):
+        ev.evaluate(([np.array([0.5, 2.0])], [np.array([0.6, 1.0])]))  # lo > hi
+    with pytest.raises(ValueError):
+        ev.evaluate(([np.array([np.nan])], [np.array([1.0])]))
+
+
+def test_interval_special_values_bit_exact(cuda_device):
+    specials = np.array([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1e-300, -1e-300, 1.0,
+                         -1.0, 1e154, -1e154, 1e300, -1e300, 1.7976931348623157e308,
+                         -1.7976931348623157e308, np.inf, -np.inf])
+    lo = np.minimum.outer(specials, specials).ravel()
+    hi = np.maximum.outer(specials, specials).ravel()
+    rng = np.random.default_rng(9)
+    for scheme in ("horner", "estrin", "balanced", "direct"):
+        c = rng.uniform(-1, 1, 13)
+        p = pe.Polynomial(np.arange(12, -1, -1).reshape(-1, 1), c)
+        prog = pe.compile(p, pe.builtin_scheme(scheme))
+        glo, ghi = pe.Evaluator(pe.IntervalDomain(), prog).evaluate(([lo], [hi]))
+        olo, ohi = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
+        assert np.array_equal(glo.view(np.int64), olo.view(np.int64))
+        assert np.array_equal(ghi.view(np.int64), ohi.view(np.int64))
+
+
+def test_f64_special_values_strict_bit_exact(cuda_device):
+    x = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1e308, -1e308, 1e-200])
+    p = pe.Polynomial(np.arange(7, -1, -1).reshape(-1, 1), np.linspace(-1, 1, 8))
+    for scheme in ("horner", "estrin", "balanced"):
+        prog = pe.compile(p, pe.builtin_scheme(scheme))
+        got = pe.Evaluator(pe.DoubleDomain(strict=True), prog).evaluate([x])
+        ref = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_f64([x])
+        same = (got.view(np.int64) == ref.view(np.int64)) | (np.isnan(got) & np.isnan(ref))
+        assert same.all()
+
+
+def test_arity_mismatch(cuda_device):
+    prog = pe.compile(W.c3().poly, W.c3().schemes)
+    with pytest.raises(ValueError):
+        pe.Evaluator(pe.BigIntDomain(), prog).evaluate([np.array([1], dtype=np.int64)])
+
+
+def test_repeatable_and_shard_invariant(cuda_device):
+    # the walk is per point: evaluating halves separately gives identical bits
+    import torch
+    wl = W.c4()
+    prog = pe.compile(wl.poly, wl.schemes)
+    pts = [_t(a, cuda_device) for a in wl.points(20_001)]
+    ev = pe.Evaluator(pe.DoubleDomain(), prog)
+    full = ev.evaluate(pts)
+    again = ev.evaluate(pts)
+    halves = torch.cat([ev.evaluate([a[:7777] for a in pts]), ev.evaluate([a[7777:] for a in pts])])
+    assert torch.equal(full, again) and torch.equal(full, halves)
