@@ -184,6 +184,18 @@ struct LaunchArgs {
   std::vector<std::uint64_t> bounds;
 };
 
+int sm_count(int device) {
+  static std::mutex m;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(m);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  check_cuda(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device), "SM count");
+  cache[device] = n;
+  return n;
+}
+
 void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
   const auto& img = a.image;
   std::uint64_t gcoef = 0;
@@ -201,7 +213,13 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   std::vector<void*> args;
   for (auto& v : vals) args.push_back(&v);
   if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
-  const std::uint64_t block = img.block;
+  // Small batches: shrink the CTA (the kernel reads its tile size from
+  // %ntid; .maxntid is only an upper bound) until every SM has work.
+  std::uint64_t block = img.block;
+  const std::uint64_t want_ctas = 2 * static_cast<std::uint64_t>(sm_count(device));
+  while (block > 64 && block % 64 == 0 && (la.n + block * img.lanes - 1) / (block * img.lanes) < want_ctas) {
+    block /= 2;
+  }
   const std::uint64_t tile = block * img.lanes;
   const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
