@@ -51,17 +51,21 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   // SM (ptxas capped at 128 registers) beats several 128-thread CTAs.
   KernelShape s;
   (void)ops;
+  // Coefficients alternate between constant-bank loads (LDCU, uniform pipe)
+  // and immediates (MOV pairs, ALU/FMA/uniform pipes): ptxas otherwise turns
+  // half the constant loads into per-thread LDC on the MIO queue
+  // (profiles/r1_imm_sweep.txt).
   if (d == Domain::Interval) {
-    s = {1, 512, 32};  // integer-pipe bound; no coefficient pressure
+    s = {1, 512, 32, 0};  // integer-pipe bound; no coefficient pressure
   } else if (powers > 32) {
     // very wide programs (large power tables): registers are the limit
-    s = {1, 512, 32};
+    s = {1, 512, 0, 2};
   } else if (distinct_coefs < 64) {
     // few distinct coefficients: ptxas encodes them as immediates or keeps
     // them in uniform registers; independent sub-chains give enough ILP
-    s = {1, 128, 0};
+    s = {1, 512, 0, 0};
   } else {
-    s = {4, 512, 0};
+    s = {4, 256, 0, 2};
   }
   auto env = [](const char* name, std::uint32_t lo, std::uint32_t hi, std::uint32_t& out) {
     if (const char* e = std::getenv(name)) {
@@ -72,6 +76,7 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   env("PE_LANES", 1, 8, s.lanes);
   env("PE_BLOCK", 32, 1024, s.block);
   env("PE_SYNC", 0, 1u << 20, s.sync_every);
+  env("PE_IMM", 0, 3, s.imm_mode);
   return s;
 }
 
@@ -108,7 +113,8 @@ template <typename C>
 class Emitter {
  public:
   Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
-      : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every) {}
+      : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
+        imm_mode_(shape.imm_mode) {}
 
   KernelImage run() {
     KernelImage img;
@@ -132,6 +138,16 @@ class Emitter {
     img.global_words.assign(words_.begin() + n_const_ + n_param_, words_.end());
 
     emit_prologue();
+    if (iv && interval_fast_path_ok()) {
+      decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n";
+      body_ << "  mov.b64 %facc, 0;\n";
+      fast_ = true;
+      emit_powers();
+      emit_walk();
+      emit_fast_exit();
+      fast_ = false;
+      img.interval_fast_path = true;
+    }
     emit_powers();
     emit_walk();
     emit_epilogue();
@@ -218,6 +234,21 @@ class Emitter {
   }
 
   // coefficient words / arithmetic registers
+  // The fast interval path needs finite, nonzero, non-straddling coefficient
+  // intervals (checked here once) and a walk that ends in a register.
+  bool interval_fast_path_ok() const {
+    if (const char* e = std::getenv("PE_IV_FAST")) {
+      if (std::atoi(e) == 0) return false;
+    }
+    if (!s_.result.is(Operand::Reg)) return false;
+    for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
+      const IvCoef c = inject(s_.coefs[k]);
+      if (!std::isfinite(c.lo) || !std::isfinite(c.hi) || c.lo == 0.0 || c.hi == 0.0) return false;
+      if ((c.lo < 0) != (c.hi < 0)) return false;
+    }
+    return true;
+  }
+
   const char* ldty() const { return d_ == Domain::I64 ? "b64" : "f64"; }
   const char* rty() const { return d_ == Domain::I64 ? "s64" : "f64"; }
   // coordinates and results in memory
@@ -228,6 +259,12 @@ class Emitter {
   // Loads coefficient word w into a fresh register (shared by all lanes).
   std::string load_word(std::uint32_t w) {
     std::string r = "%c" + std::to_string(n_creg_++);
+    if (imm_mode_ == 1 || (imm_mode_ == 2 && (w & 1)) || (imm_mode_ == 3 && w >= n_const_)) {
+      // immediate: ptxas materialises it with two 32-bit moves on the ALU /
+      // FMA / uniform pipes instead of a constant-cache load on the MIO queue
+      body_ << "  mov.b64 " << r << ", " << hex64(words_[w]) << ";\n";
+      return r;
+    }
     if (w < n_const_) {
       body_ << "  ld.const." << ldty() << " " << r << ", [pe_coef+" << 8 * w << "];\n";
     } else if (w < n_const_ + n_param_) {
@@ -241,11 +278,15 @@ class Emitter {
 
   // ---------------- operands ----------------
   std::string reg(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
-    if (d_ == Domain::Interval) return (hi ? "%vh" : "%vl") + std::to_string(id) + ln(lane);
+    if (d_ == Domain::Interval) {
+      return std::string(fast_ ? "%f" : "%") + (hi ? "vh" : "vl") + std::to_string(id) + ln(lane);
+    }
     return "%v" + std::to_string(id) + ln(lane);
   }
   std::string pw(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
-    if (d_ == Domain::Interval) return (hi ? "%ph" : "%pl") + std::to_string(id) + ln(lane);
+    if (d_ == Domain::Interval) {
+      return std::string(fast_ ? "%f" : "%") + (hi ? "ph" : "pl") + std::to_string(id) + ln(lane);
+    }
     return "%q" + std::to_string(id) + ln(lane);
   }
   std::string xr(std::uint32_t v, std::uint32_t lane, bool hi = false) const {
@@ -383,12 +424,23 @@ class Emitter {
           if (d_ == Domain::Interval) {
             body_ << "  mov.f64 " << pw(id, k, false) << ", " << xr(p.var, k, false) << ";\n"
                   << "  mov.f64 " << pw(id, k, true) << ", " << xr(p.var, k, true) << ";\n";
+            if (fast_) {
+              fcheck_straddle({pw(id, k, false), pw(id, k, true)});
+              fcheck_finite(pw(id, k, false));
+              fcheck_finite(pw(id, k, true));
+            }
           } else {
             body_ << "  mov." << ldty() << " " << pw(id, k) << ", " << xr(p.var, k) << ";\n";
           }
           continue;
         }
-        if (d_ == Domain::Interval) {
+        if (d_ == Domain::Interval && fast_) {
+          fast_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
+                   {pw(p.hi, k, false), pw(p.hi, k, true)}, false, false);
+          fcheck_straddle({pw(id, k, false), pw(id, k, true)});
+          fcheck_finite(pw(id, k, false));
+          fcheck_finite(pw(id, k, true));
+        } else if (d_ == Domain::Interval) {
           iv_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
                  {pw(p.hi, k, false), pw(p.hi, k, true)}, k == 0);
         } else if (d_ == Domain::I64) {
@@ -550,16 +602,121 @@ class Emitter {
     next(dhi, mx, true);
   }
 
+  // ---------------- interval fast path ----------------
+  // Same op sequence as the strict replay, cheaper primitives that are exact
+  // under preconditions, plus a per-thread accumulator (%facc, sign bit) that
+  // records every way a precondition can fail. A thread whose accumulator or
+  // result says "special" re-runs the point through the strict replay, so
+  // every result stays bit-identical to the reference.
+  //
+  //  * next_down/next_up of a finite nonzero double is -/+1 on its magnitude
+  //    bits: u -/+ (s|1), s = u >> 63 (arith). This is std::nextafter except
+  //    at +-0, +-inf and NaN; the failing cases flip the sign bit (+0 down,
+  //    -0 up, canonical NaN up) or produce NaN (+inf up, -inf down), which
+  //    the sign-flip accumulator and the final NaN/inf test catch.
+  //  * a product of two intervals that do not straddle zero is, by
+  //    monotonicity of RN, [RN(A1*B1), RN(A2*B2)] with the endpoint choice
+  //    set by the two signs (interval_mul's min/max of four products,
+  //    interval.cpp:43-52). Straddling register operands set the
+  //    accumulator. Zero endpoints either give the same value as the zero
+  //    rule or a zero that the next step flags; NaN/inf always reach one of
+  //    the two products ({A1,A2} and {B1,B2} are both endpoint pairs).
+  void fnext(const std::string& dst, const std::string& src, bool up) {
+    const std::string u = tmp_u(), s = tmp_u(), d = tmp_u(), r = tmp_u(), x = tmp_u();
+    body_ << "  mov.b64 " << u << ", " << src << ";\n"
+          << "  shr.s64 " << s << ", " << u << ", 63;\n"
+          << "  or.b64 " << d << ", " << s << ", 1;\n"
+          << (up ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", " << d << ";\n"
+          << "  xor.b64 " << x << ", " << r << ", " << u << ";\n"
+          << "  or.b64 %facc, %facc, " << x << ";\n"
+          << "  mov.b64 " << dst << ", " << r << ";\n";
+  }
+
+  void fast_add(const std::string& dlo, const std::string& dhi,
+                const std::pair<std::string, std::string>& a,
+                const std::pair<std::string, std::string>& b, bool a_is_zero) {
+    if (a_is_zero) {
+      fnext(dlo, b.first, false);
+      fnext(dhi, b.second, true);
+      return;
+    }
+    const std::string lo = tmp_f(), hi = tmp_f();
+    body_ << "  add.rn.f64 " << lo << ", " << a.first << ", " << b.first << ";\n"
+          << "  add.rn.f64 " << hi << ", " << a.second << ", " << b.second << ";\n";
+    fnext(dlo, lo, false);
+    fnext(dhi, hi, true);
+  }
+
+  // accumulator |= (lo ^ hi): sign bit set iff the interval straddles zero
+  // (or has a sign-mismatched zero endpoint) — only the high words matter
+  void fcheck_straddle(const std::pair<std::string, std::string>& a) {
+    const std::string ul = tmp_u(), uh = tmp_u(), x = tmp_u();
+    body_ << "  mov.b64 " << ul << ", " << a.first << ";\n  mov.b64 " << uh << ", " << a.second
+          << ";\n  xor.b64 " << x << ", " << ul << ", " << uh << ";\n  or.b64 %facc, %facc, " << x
+          << ";\n";
+  }
+
+  // accumulator gets the sign bit if v is inf or NaN (exponent 0x7FF + 1
+  // carries into the sign bit)
+  void fcheck_finite(const std::string& v) {
+    const std::string u = tmp_u(), e = tmp_u(), x = tmp_u();
+    body_ << "  mov.b64 " << u << ", " << v << ";\n  add.s64 " << e << ", " << u
+          << ", 0x0010000000000000;\n  xor.b64 " << x << ", " << e << ", " << u
+          << ";\n  or.b64 %facc, %facc, " << x << ";\n";
+  }
+
+  void fast_mul(const std::string& dlo, const std::string& dhi,
+                const std::pair<std::string, std::string>& a,
+                const std::pair<std::string, std::string>& b, bool check_a, bool check_b) {
+    if (check_a) fcheck_straddle(a);
+    if (check_b) fcheck_straddle(b);
+    const std::string ah = tmp_u(), bh = tmp_u();
+    const std::string an = tmp_p(), bn = tmp_p(), ng = tmp_p();
+    body_ << "  mov.b64 " << ah << ", " << a.second << ";\n  mov.b64 " << bh << ", " << b.second
+          << ";\n  setp.lt.s64 " << an << ", " << ah << ", 0;\n  setp.lt.s64 " << bn << ", " << bh
+          << ", 0;\n  xor.pred " << ng << ", " << an << ", " << bn << ";\n";
+    const std::string A1 = tmp_f(), B1 = tmp_f(), A2 = tmp_f(), B2 = tmp_f();
+    body_ << "  selp.f64 " << A1 << ", " << a.second << ", " << a.first << ", " << bn << ";\n"
+          << "  selp.f64 " << A2 << ", " << a.first << ", " << a.second << ", " << bn << ";\n"
+          << "  selp.f64 " << B1 << ", " << b.second << ", " << b.first << ", " << an << ";\n"
+          << "  selp.f64 " << B2 << ", " << b.first << ", " << b.second << ", " << an << ";\n";
+    const std::string lo = tmp_f(), hi = tmp_f();
+    body_ << "  mul.rn.f64 " << lo << ", " << A1 << ", " << B1 << ";\n"
+          << "  mul.rn.f64 " << hi << ", " << A2 << ", " << B2 << ";\n";
+    // product sign is known: next_down(lo) = lo - d, next_up(hi) = hi + d,
+    // d = -1 for negative products, +1 for positive ones
+    const std::string d = tmp_u(), ul = tmp_u(), uh = tmp_u(), rl = tmp_u(), rh = tmp_u(),
+                      xl = tmp_u(), xh = tmp_u();
+    body_ << "  selp.b64 " << d << ", -1, 1, " << ng << ";\n"
+          << "  mov.b64 " << ul << ", " << lo << ";\n  mov.b64 " << uh << ", " << hi << ";\n"
+          << "  sub.s64 " << rl << ", " << ul << ", " << d << ";\n"
+          << "  add.s64 " << rh << ", " << uh << ", " << d << ";\n"
+          << "  xor.b64 " << xl << ", " << rl << ", " << ul << ";\n"
+          << "  xor.b64 " << xh << ", " << rh << ", " << uh << ";\n"
+          << "  or.b64 %facc, %facc, " << xl << ";\n  or.b64 %facc, %facc, " << xh << ";\n"
+          << "  mov.b64 " << dlo << ", " << rl << ";\n  mov.b64 " << dhi << ", " << rh << ";\n";
+  }
+
   void emit_iv_op(const Op& op) {
     const Loaded la = load(op.a), lb = load(op.b);
     for (std::uint32_t k = 0; k < P_; ++k) {
       const std::string dlo = reg(op.dst, k, false), dhi = reg(op.dst, k, true);
       switch (op.kind) {
         case OpKind::Add:
-          iv_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero), k == 0);
+          if (fast_) {
+            fast_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero));
+          } else {
+            iv_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero), k == 0);
+          }
           break;
         case OpKind::Mul:
-          iv_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), k == 0);
+          if (fast_) {
+            // coefficients are host-checked, powers checked where computed
+            fast_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Reg),
+                     op.b.is(Operand::Reg));
+          } else {
+            iv_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), k == 0);
+          }
           break;
         case OpKind::Fma:
           throw std::logic_error("interval streams are strict (no FMA)");
@@ -567,7 +724,28 @@ class Emitter {
     }
   }
 
+  // Interval fast path: if the accumulator or either result endpoint says
+  // "special", the thread re-evaluates through the strict replay.
+  void emit_fast_exit() {
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      fcheck_finite(reg(s_.result.id, k, false));
+      fcheck_finite(reg(s_.result.id, k, true));
+    }
+    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n  @%pslow bra $Lslow;\n";
+    emit_store();
+    body_ << "  bra $Ldone;\n$Lslow:\n";
+  }
+
   void emit_epilogue() {
+    emit_store();
+    body_ << "$Ldone:\n  ret;\n";
+    if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
+    if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
+    if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
+    if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+  }
+
+  void emit_store() {
     const bool iv = d_ == Domain::Interval;
     const Loaded lr = load(s_.result);
     for (std::uint32_t o = 0; o < (iv ? 2u : 1u); ++o) {
@@ -593,11 +771,6 @@ class Emitter {
               << ioty() << " [%rd10], " << val << ";\n";
       }
     }
-    body_ << "$Ldone:\n  ret;\n";
-    if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
-    if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
-    if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
-    if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
   }
 
   const Stream<C>& s_;
@@ -605,6 +778,8 @@ class Emitter {
   std::uint32_t P_;
   std::uint32_t block_;
   std::uint32_t sync_every_;
+  std::uint32_t imm_mode_;
+  bool fast_ = false;  // emitting the interval fast path
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
@@ -629,6 +804,7 @@ KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape) 
   if (shape.lanes == 0) shape.lanes = def.lanes;
   if (shape.block == 0) shape.block = def.block;
   if (shape.sync_every == 0) shape.sync_every = def.sync_every;
+  if (shape.imm_mode == 0) shape.imm_mode = def.imm_mode;
   Emitter<C> e(stream, domain, shape);
   return e.run();
 }

@@ -48,6 +48,7 @@ struct KernelImage {
   std::uint32_t const_words = 0;
   std::uint32_t block = 128;
   std::uint32_t lanes = 1;         // points per thread (tile = block * lanes)
+  bool interval_fast_path = false; // fast exact path + strict replay fallback
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
   std::uint64_t int_ops = 0;       // int64 add/mul/mad per point
@@ -66,6 +67,9 @@ struct KernelShape {
   std::uint32_t lanes = 0;
   std::uint32_t block = 0;
   std::uint32_t sync_every = 0;
+  // coefficient delivery: 0 constant bank (LDC/LDCU), 1 immediates (MOV
+  // pairs), 2 alternate words, 3 immediates beyond the constant-bank tier
+  std::uint32_t imm_mode = 0;
 };
 
 /// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC

@@ -1,0 +1,9 @@
+# coefficient delivery (PE_IMM) x shape sweep
+run() { cfg=$1; pts=$2; shift 2; for combo in "$@"; do
+  IFS=, read L B S M <<< "$combo"
+  r=$(PE_LANES=$L PE_BLOCK=$B PE_SYNC=$S PE_IMM=$M timeout 300 python scripts/profile_one.py --config $cfg --points $pts --reps 3 2>&1 | tail -1)
+  echo "$cfg L=$L B=$B S=$S IMM=$M :: $r"; done; }
+run c2e1000 10000000 4,512,0,0 4,512,0,1 4,512,0,2 2,512,0,2 2,512,0,1 3,512,0,2 4,256,0,2 6,384,0,2 8,256,0,2 1,256,0,2
+run c2b1000 10000000 4,512,0,0 4,512,0,2 4,512,0,1
+run c4 4000000 1,512,32,0 1,512,32,2 1,512,32,1 1,512,0,2 2,256,0,2 2,256,32,2 1,256,0,2
+run c3 10000000 1,128,0,0 2,256,0,0 1,512,0,0 4,512,0,0

@@ -123,3 +123,36 @@ def test_repeatable_and_shard_invariant(cuda_device):
     again = ev.evaluate(pts)
     halves = torch.cat([ev.evaluate([a[:7777] for a in pts]), ev.evaluate([a[7777:] for a in pts])])
     assert torch.equal(full, again) and torch.equal(full, halves)
+
+
+def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch):
+    # The fast interval path (sign-case products, integer nextafter with
+    # sign-flip detection) must equal the strict replay and the oracle on
+    # intervals that straddle zero, touch zero, underflow and overflow.
+    rng = np.random.default_rng(21)
+    n = 50_000
+    x = rng.uniform(-1, 1, n)
+    w = np.where(rng.uniform(size=n) < 0.1, rng.uniform(0, 0.5, n), 1e-6)
+    lo, hi = x, x + w
+    lo[:50] = 0.0
+    hi[50:100] = 0.0
+    lo[100:150] = -hi[100:150]
+    big = rng.uniform(1e150, 1e160, 200)
+    lo[200:400], hi[200:400] = big, big * 2
+    tiny = rng.uniform(1e-200, 1e-190, 200)
+    lo[400:600], hi[400:600] = tiny, tiny * 2
+    for scheme, deg in (("estrin", 200), ("horner", 30), ("balanced", 64)):
+        wl = W.c5()
+        p = pe.Polynomial(np.arange(deg, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, deg + 1))
+        monkeypatch.setenv("PE_IV_FAST", "0")
+        slow = pe.compile(p, pe.builtin_scheme(scheme))
+        s = pe.Evaluator(pe.IntervalDomain(), slow).evaluate(([lo], [hi]))
+        monkeypatch.delenv("PE_IV_FAST")
+        fast = pe.compile(p, pe.builtin_scheme(scheme))
+        f = pe.Evaluator(pe.IntervalDomain(), fast).evaluate(([lo], [hi]))
+        assert "%facc" not in slow.ptx(pe.DOMAIN_INTERVAL)
+        assert "%facc" in fast.ptx(pe.DOMAIN_INTERVAL)
+        o = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
+        for a, b, c in zip(f, s, o):
+            assert np.array_equal(a.view(np.int64), c.view(np.int64))
+            assert np.array_equal(b.view(np.int64), c.view(np.int64))
