@@ -161,6 +161,10 @@ Artifact& Program::loaded(lower::Domain d, int device) const {
                "cudaLibraryLoadData");
     check_cuda(cudaLibraryGetKernel(&a.kernel, a.library, a.image.entry.c_str()),
                "cudaLibraryGetKernel");
+    if (!a.image.fix_entry.empty()) {
+      check_cuda(cudaLibraryGetKernel(&a.fix_kernel, a.library, a.image.fix_entry.c_str()),
+                 "cudaLibraryGetKernel(fix)");
+    }
   }
   if (!a.image.global_words.empty() && !a.global_coefs.count(device)) {
     void* p = nullptr;
@@ -182,6 +186,8 @@ struct LaunchArgs {
   std::uint64_t n = 0;
   std::uint64_t flag = 0;
   std::vector<std::uint64_t> bounds;
+  // interval fast path: fixup list (u32 point indices), counter, capacity
+  std::uint64_t list = 0, count = 0, cap = 0;
 };
 
 int sm_count(int device) {
@@ -210,6 +216,14 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   if (img.has_bounds) {
     for (std::uint32_t v = 0; v < img.nvars; ++v) vals.push_back(la.bounds.at(v));
   }
+  if (img.interval_fast_path) {
+    if (!la.list || !la.count) throw std::logic_error("interval fast path needs a fixup list");
+    vals.push_back(la.list);
+    vals.push_back(la.count);
+    vals.push_back(la.cap);
+    check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(la.count), 0, sizeof(unsigned), stream),
+               "cudaMemsetAsync(fixup count)");
+  }
   std::vector<void*> args;
   for (auto& v : vals) args.push_back(&v);
   if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
@@ -228,6 +242,17 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
                               args.data(), 0, stream),
              "cudaLaunchKernel(walk)");
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (img.interval_fast_path) {
+    // strict replay of the points the fast path could not prove; it reads
+    // the list length on the device, so no host round trip in between
+    const unsigned fix_grid = static_cast<unsigned>(
+        std::min<std::uint64_t>(2 * static_cast<std::uint64_t>(sm_count(device)),
+                                (la.cap + 127) / 128));
+    check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.fix_kernel), dim3(fix_grid ? fix_grid : 1),
+                                dim3(128), args.data(), 0, stream),
+               "cudaLaunchKernel(fixup)");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
 }
 
 enum class MemKind { Host, Device };
@@ -322,14 +347,50 @@ struct Flag {
 /// through a 3-slot chunked H2D / kernel / D2H pipeline on the device's own
 /// streams (copy engines overlap the walk of the neighbouring chunk).
 /// `flag_dev` (may be null) is the device status word for domain checks.
+// Device scratch for the interval fixup list: one (list, count) per pipeline
+// slot. Capacity 1/16 of the chunk by default (special points are rare); the
+// full chunk after an overflow.
+struct FixupLists {
+  std::vector<void*> lists, counts;
+  std::uint64_t cap = 0;
+  std::vector<cudaStream_t> streams;
+  FixupLists(const Artifact& a, size_t chunk, bool full, const std::vector<cudaStream_t>& ss) {
+    if (!a.image.interval_fast_path) return;
+    cap = full ? chunk : std::min<std::uint64_t>(chunk, chunk / 16 + 4096);
+    streams = ss;
+    for (auto s : ss) {
+      void *l = nullptr, *c = nullptr;
+      check_cuda(cudaMallocAsync(&l, 4 * cap, s), "cudaMallocAsync(fixup list)");
+      check_cuda(cudaMallocAsync(&c, 4, s), "cudaMallocAsync(fixup count)");
+      lists.push_back(l);
+      counts.push_back(c);
+    }
+  }
+  void bind(LaunchArgs& la, size_t slot) const {
+    if (lists.empty()) return;
+    la.list = reinterpret_cast<std::uint64_t>(lists[slot]);
+    la.count = reinterpret_cast<std::uint64_t>(counts[slot]);
+    la.cap = cap;
+  }
+  ~FixupLists() {
+    for (size_t i = 0; i < lists.size(); ++i) {
+      cudaFreeAsync(lists[i], streams[i]);
+      cudaFreeAsync(counts[i], streams[i]);
+    }
+  }
+};
+
 void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
-               const LaunchArgs& proto, cudaStream_t user_stream, bool sync) {
+               const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
+               bool full_fixup = false) {
   const size_t elem = 8;
   if (kind == MemKind::Device) {
     const size_t max_chunk = size_t{1} << 30;
+    FixupLists fix(a, std::min(n, max_chunk), full_fixup, {user_stream});
     for (size_t off = 0; off < n; off += max_chunk) {
       LaunchArgs la = proto;
+      fix.bind(la, 0);
       la.n = std::min(max_chunk, n - off);
       la.ins.clear();
       la.outs.clear();
@@ -351,12 +412,15 @@ void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
     check_cuda(cudaEventRecord(flag_ready, user_stream), "cudaEventRecord");
     for (auto s : c.streams) check_cuda(cudaStreamWaitEvent(s, flag_ready, 0), "cudaStreamWaitEvent");
   }
+  FixupLists fix(a, chunk, full_fixup,
+                 std::vector<cudaStream_t>(c.streams, c.streams + DeviceCtx::kSlots));
   size_t k = 0;
   for (size_t off = 0; off < n; off += chunk, ++k) {
     const int slot = static_cast<int>(k % DeviceCtx::kSlots);
     cudaStream_t s = c.streams[slot];
     const size_t m = std::min(chunk, n - off);
     LaunchArgs la = proto;
+    fix.bind(la, static_cast<size_t>(slot));
     la.n = m;
     la.ins.clear();
     la.outs.clear();
@@ -677,12 +741,18 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
     const Artifact& a = p.loaded(lower::Domain::Interval, dev);
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
-    Flag flag(s);
-    LaunchArgs la;
-    la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
-    run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false);
-    if (flag.read() != 0) return fail(PE_EINVAL, "invalid interval endpoints (NaN or lo > hi)");
-    return PE_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      Flag flag(s);
+      LaunchArgs la;
+      la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
+      run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false, attempt == 1);
+      const unsigned f = flag.read();
+      if (f & 2) return fail(PE_EINVAL, "invalid interval endpoints (NaN or lo > hi)");
+      if (!(f & 4)) return PE_OK;
+      // more points needed the strict replay than the fixup list held:
+      // re-run with a list as large as the batch (cannot overflow)
+    }
+    return fail(PE_ELOGIC, "interval fixup list overflowed at full capacity");
   });
 }
 

@@ -137,8 +137,15 @@ class Emitter {
     img.param_words.assign(words_.begin() + n_const_, words_.begin() + n_const_ + n_param_);
     img.global_words.assign(words_.begin() + n_const_ + n_param_, words_.end());
 
+    const bool fast = iv && interval_fast_path_ok();
+    img.interval_fast_path = fast;
+    img.entry = std::string("pe_walk_") + domain_name(d_);
+
+    // main entry
+    reset_entry();
     emit_prologue();
-    if (iv && interval_fast_path_ok()) {
+    if (fast) {
+      // exact fast path; points it cannot prove go to the fixup list
       decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n";
       body_ << "  mov.b64 %facc, 0;\n";
       fast_ = true;
@@ -146,17 +153,39 @@ class Emitter {
       emit_walk();
       emit_fast_exit();
       fast_ = false;
-      img.interval_fast_path = true;
+      finish_entry();
+    } else {
+      emit_powers();
+      emit_walk();
+      emit_epilogue();
     }
-    emit_powers();
-    emit_walk();
-    emit_epilogue();
+    const std::string main_entry = entry_text(img, img.entry);
+
+    // fixup entry: strict replay of the listed points (grid-stride loop)
+    std::string fix_entry;
+    if (fast) {
+      img.fix_entry = img.entry + "_fix";
+      const std::uint32_t lanes = P_, sync = sync_every_;
+      P_ = 1;
+      sync_every_ = 0;  // threads leave the grid-stride loop at different trips
+      reset_entry();
+      fix_ = true;
+      emit_fix_prologue();
+      emit_powers();
+      emit_walk();
+      emit_store();
+      body_ << "  add.u64 %rd1, %rd1, %rd2;\n  bra $Lfix;\n";
+      finish_entry();
+      fix_ = false;
+      fix_entry = entry_text(img, img.fix_entry);
+      P_ = lanes;
+      sync_every_ = sync;
+    }
 
     std::ostringstream m;
-    img.entry = std::string("pe_walk_") + domain_name(d_);
     m << "//\n// polyeval-b200 generated kernel: domain=" << domain_name(d_)
       << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
-      << " lanes=" << P_ << "\n//\n";
+      << " lanes=" << P_ << (fast ? " interval-fast-path+fixup" : "") << "\n//\n";
     m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
     if (n_const_ > 0) {
       m << ".const .align 8 .b64 pe_coef[" << n_const_ << "] = {";
@@ -166,7 +195,37 @@ class Emitter {
       }
       m << "};\n\n";
     }
-    m << ".visible .entry " << img.entry << "(";
+    m << main_entry << fix_entry;
+    img.ptx = m.str();
+    img.fp_ops = fp_ops_;
+    img.int_ops = int_ops_;
+    img.hash = fnv1a(img.ptx.data(), img.ptx.size());
+    return img;
+  }
+
+ private:
+  // ---------------- entries ----------------
+  void reset_entry() {
+    body_.str("");
+    body_.clear();
+    decls_.str("");
+    decls_.clear();
+    n_creg_ = n_tf_ = n_tu_ = n_tp_ = 0;
+  }
+
+  void finish_entry() {
+    body_ << "$Ldone:\n  ret;\n";
+    if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
+    if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
+    if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
+    if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+  }
+
+  // Both entries of a module take the same parameter list, so one argument
+  // array launches either.
+  std::string entry_text(const KernelImage& img, const std::string& name) const {
+    std::ostringstream m;
+    m << ".visible .entry " << name << "(";
     bool first = true;
     auto param = [&](const std::string& decl) {
       m << (first ? "\n  " : ",\n  ") << decl;
@@ -180,20 +239,18 @@ class Emitter {
     if (img.has_bounds) {
       for (std::uint32_t v = 0; v < s_.nvars; ++v) param(".param .u64 pe_bound" + std::to_string(v));
     }
+    if (img.interval_fast_path) {
+      param(".param .u64 pe_list");
+      param(".param .u64 pe_count");
+      param(".param .u64 pe_cap");
+    }
     if (n_param_ > 0) param(".param .align 8 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
     m << ")\n.maxntid " << img.block << ", 1, 1\n{\n";
     m << "  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n";
-    m << decls_.str();
-    m << body_.str();
-    m << "}\n";
-    img.ptx = m.str();
-    img.fp_ops = fp_ops_;
-    img.int_ops = int_ops_;
-    img.hash = fnv1a(img.ptx.data(), img.ptx.size());
-    return img;
+    m << decls_.str() << body_.str() << "}\n\n";
+    return m.str();
   }
 
- private:
   // ---------------- coefficient words ----------------
   void assign_words() {
     coef_lo_.resize(s_.coefs.size());
@@ -731,18 +788,66 @@ class Emitter {
       fcheck_finite(reg(s_.result.id, k, false));
       fcheck_finite(reg(s_.result.id, k, true));
     }
-    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n  @%pslow bra $Lslow;\n";
+    const char* dbg = std::getenv("PE_IV_DEBUG");
+    if (dbg && std::atoi(dbg) == 1) {
+      // diagnostics: out_hi receives the accumulator bits, no slow path
+      body_ << "  ld.param.u64 %rd9, [pe_out1];\n  cvta.to.global.u64 %rd9, %rd9;\n"
+            << "  add.u64 %rd10, %rd9, %ix0;\n  st.global.b64 [%rd10], %facc;\n  bra $Ldone;\n";
+    }
+    // special: append the thread's valid point indices to the fixup list
+    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n  @!%pslow bra $Lfaststore;\n"
+          << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
+          << "  ld.param.u64 %rd15, [pe_list];\n  cvta.to.global.u64 %rd15, %rd15;\n"
+          << "  ld.param.u64 %rd16, [pe_cap];\n"
+          << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n";
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      // list overflow (more special points than capacity): flag bit 4, the
+      // host re-runs with a full-size list
+      body_ << "  @%pv" << k << " atom.global.add.u32 %r4, [%rd14], 1;\n"
+            << "  cvt.u64.u32 %rd17, %r4;\n  setp.lt.u64 %p3, %rd17, %rd16;\n"
+            << "  not.pred %p4, %p3;\n  and.pred %p4, %p4, %pv" << k << ";\n"
+            << "  @%p4 atom.global.or.b32 %r6, [%rd7], 4;\n"
+            << "  and.pred %p3, %p3, %pv" << k << ";\n"
+            << "  shr.u64 %rd18, %ix" << k << ", 3;\n  cvt.u32.u64 %r5, %rd18;\n"
+            << "  shl.b64 %rd17, %rd17, 2;\n  add.u64 %rd17, %rd15, %rd17;\n"
+            << "  @%p3 st.global.u32 [%rd17], %r5;\n";
+    }
+    body_ << "  bra $Ldone;\n$Lfaststore:\n";
     emit_store();
-    body_ << "  bra $Ldone;\n$Lslow:\n";
+  }
+
+  // Fixup entry: grid-stride over the first min(count, cap) listed points,
+  // each re-evaluated by the strict replay (inputs were validated by the
+  // main entry).
+  void emit_fix_prologue() {
+    body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
+          << "  mul.wide.u32 %rd1, %r1, %r2;\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
+          << "  mov.u32 %r4, %nctaid.x;\n  mul.wide.u32 %rd2, %r4, %r2;\n"
+          << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
+          << "  ld.global.u32 %r5, [%rd14];\n  cvt.u64.u32 %rd3, %r5;\n"
+          << "  ld.param.u64 %rd16, [pe_cap];\n  min.u64 %rd3, %rd3, %rd16;\n"
+          << "  ld.param.u64 %rd15, [pe_list];\n  cvta.to.global.u64 %rd15, %rd15;\n";
+    if (n_global_ > 0) {
+      body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
+    }
+    decls_ << "  .reg .b64 %ix<1>;\n  .reg .pred %pv<1>;\n";
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      decls_ << "  .reg .f64 " << xr(v, 0, false) << ", " << xr(v, 0, true) << ";\n";
+    }
+    body_ << "$Lfix:\n  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n"
+          << "  shl.b64 %rd17, %rd1, 2;\n  add.u64 %rd17, %rd15, %rd17;\n"
+          << "  ld.global.u32 %r6, [%rd17];\n  cvt.u64.u32 %rd13, %r6;\n"
+          << "  shl.b64 %ix0, %rd13, 3;\n  setp.eq.u64 %pv0, %rd13, %rd13;\n";
+    for (std::uint32_t i = 0; i < 2 * s_.nvars; ++i) {
+      body_ << "  ld.param.u64 %rd5, [pe_in" << i << "];\n  cvta.to.global.u64 %rd5, %rd5;\n"
+            << "  add.u64 %rd6, %rd5, %ix0;\n  ld.global.nc.f64 " << xr(i / 2, 0, i % 2 == 1)
+            << ", [%rd6];\n";
+    }
   }
 
   void emit_epilogue() {
     emit_store();
-    body_ << "$Ldone:\n  ret;\n";
-    if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
-    if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
-    if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
-    if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+    finish_entry();
   }
 
   void emit_store() {
@@ -780,6 +885,7 @@ class Emitter {
   std::uint32_t sync_every_;
   std::uint32_t imm_mode_;
   bool fast_ = false;  // emitting the interval fast path
+  bool fix_ = false;   // emitting the fixup entry
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;

@@ -31,6 +31,7 @@ struct Artifact {
   double compile_seconds = 0.0;
   cudaLibrary_t library = nullptr;
   cudaKernel_t kernel = nullptr;
+  cudaKernel_t fix_kernel = nullptr;  // interval fast path: strict replay of listed points
   std::map<int, void*> global_coefs;  // per device: global-tier coefficient words
 };
 

@@ -133,10 +133,13 @@ def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch):
     n = 50_000
     x = rng.uniform(-1, 1, n)
     w = np.where(rng.uniform(size=n) < 0.1, rng.uniform(0, 0.5, n), 1e-6)
-    lo, hi = x, x + w
-    lo[:50] = 0.0
-    hi[50:100] = 0.0
-    lo[100:150] = -hi[100:150]
+    lo, hi = x.copy(), x + w
+    lo[:50] = 0.0                      # touches zero from above
+    hi[:50] = np.abs(hi[:50])
+    hi[50:100] = 0.0                   # touches zero from below
+    lo[50:100] = -np.abs(lo[50:100])
+    lo[100:150] = -np.abs(hi[100:150])  # straddles zero
+    hi[100:150] = np.abs(hi[100:150])
     big = rng.uniform(1e150, 1e160, 200)
     lo[200:400], hi[200:400] = big, big * 2
     tiny = rng.uniform(1e-200, 1e-190, 200)
