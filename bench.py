@@ -246,9 +246,11 @@ def run_native(args, world, rank, local):
     t_setup = time.perf_counter()
     progs = [pe.compile(w.poly, w.schemes) for w in wls]
     if domain == "interval":
-        evs = [pe.Evaluator(pe.IntervalDomain(), p, device=local) for p in progs]
+        evs = [pe.Evaluator(pe.IntervalDomain(), p, device=local, deferred_checks=True)
+               for p in progs]
     elif domain == "i64":
-        evs = [pe.Evaluator(pe.BigIntDomain(), p, device=local) for p in progs]
+        evs = [pe.Evaluator(pe.BigIntDomain(), p, device=local, deferred_checks=True)
+               for p in progs]
     else:
         evs = [pe.Evaluator(pe.DoubleDomain(), p, device=local) for p in progs]
 
@@ -314,6 +316,9 @@ def run_native(args, world, rank, local):
             step(ev)
             torch.cuda.synchronize(dev)
             barrier(world)
+            for e in evs:  # deferred domain checks (int64 bound, interval endpoints)
+                if getattr(e, "deferred_checks", False):
+                    e.synchronize(sptr)
             ms = [a.elapsed_time(b) for a, b in ev]
             for i, m in enumerate(ms):
                 per_launch_ms[i].append(m)

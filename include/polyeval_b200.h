@@ -96,6 +96,14 @@ typedef struct pe_exec {
   /* pe_eval_i64 only: caller-asserted per-variable bounds |x_v| <= bound[v]
    * (nvars entries; NULL = derive from the data with a device max-reduction). */
   const uint64_t* i64_bounds;
+  /* Device-pointer pe_eval_i64 / pe_eval_interval: 1 = return right after
+   * enqueueing (no host round trip per call); domain-check failures (a
+   * coordinate beyond the proven int64 bound, invalid interval endpoints)
+   * accumulate in a per-(device, stream) status word and are reported by the
+   * next pe_synchronize(exec). The int64 retry with data-derived bounds is
+   * not attempted in this mode (re-run synchronously to get it). */
+  int32_t deferred_checks;
+  int32_t reserved;
 } pe_exec;
 
 /* Compiles a polynomial given as raw terms: `exponents` is nterms x nvars

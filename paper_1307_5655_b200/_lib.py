@@ -31,6 +31,8 @@ class pe_exec(C.Structure):
         ("synchronize", C.c_int32),
         ("i64_int_pipe", C.c_int32),
         ("i64_bounds", C.POINTER(C.c_uint64)),
+        ("deferred_checks", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

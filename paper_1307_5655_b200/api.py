@@ -260,10 +260,15 @@ def _is_torch_cuda(x) -> bool:
 class Evaluator:
     """Batch evaluation session (reference Evaluator<D>, eval.hpp:69-90)."""
 
-    def __init__(self, domain, program: CompiledProgram, device: int = -1):
+    def __init__(self, domain, program: CompiledProgram, device: int = -1,
+                 deferred_checks: bool = False):
+        """deferred_checks: device-pointer int64 / interval calls return
+        without a host round trip; domain-check failures surface at
+        `synchronize()` (pe_exec.deferred_checks)."""
         self.domain = domain
         self.program = program
         self.device = device
+        self.deferred_checks = bool(deferred_checks)
         if isinstance(domain, BigIntDomain) and not program.integer:
             raise ValueError("BigIntDomain needs integer coefficients")
 
@@ -274,6 +279,7 @@ class Evaluator:
         ex.stream = stream
         ex.synchronize = 1 if sync else 0
         ex.i64_int_pipe = 1 if isinstance(self.domain, BigIntDomain) and self.domain.int_pipe else 0
+        ex.deferred_checks = 1 if self.deferred_checks else 0
         if bounds is not None:
             arr = (C.c_uint64 * len(bounds))(*[int(b) for b in bounds])
             ex.i64_bounds = arr
@@ -333,6 +339,12 @@ class Evaluator:
         fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
         L.check(fn(self.program.handle, ptrs, n, self._ptr(out), C.byref(ex)))
         return out
+
+    def synchronize(self, stream=None):
+        """Waits for the stream; raises any deferred domain-check failure."""
+        import torch
+        ex = self._exec(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        L.check(L.lib().pe_synchronize(C.byref(ex)))
 
     @staticmethod
     def _stream(stream, dev):

@@ -270,6 +270,15 @@ MemKind classify(const void* p, int* device) {
   return MemKind::Host;
 }
 
+// Deferred-check state of one caller stream: an accumulating status word and
+// a grow-only full-capacity interval fixup list, both stream-ordered.
+struct StreamState {
+  unsigned* status = nullptr;
+  void* list = nullptr;
+  unsigned* count = nullptr;
+  std::uint64_t list_cap = 0;
+};
+
 struct DeviceCtx {
   static constexpr int kSlots = 3;
   cudaStream_t streams[kSlots] = {};
@@ -277,6 +286,28 @@ struct DeviceCtx {
   size_t cap = 0;
   std::mutex mu;  // serialises host-staged calls on a device
   int sms = 0;
+  std::mutex state_mu;
+  std::map<cudaStream_t, StreamState> states;
+
+  StreamState& state(cudaStream_t s, std::uint64_t need_list) {
+    std::lock_guard<std::mutex> lock(state_mu);
+    StreamState& st = states[s];
+    if (!st.status) {
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&st.status), 2 * sizeof(unsigned)),
+                 "cudaMalloc(status)");
+      check_cuda(cudaMemsetAsync(st.status, 0, 2 * sizeof(unsigned), s), "cudaMemsetAsync(status)");
+      st.count = st.status + 1;
+    }
+    if (need_list > st.list_cap) {
+      if (st.list) {
+        check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cudaFree(st.list);
+      }
+      check_cuda(cudaMalloc(&st.list, 4 * need_list), "cudaMalloc(fixup list)");
+      st.list_cap = need_list;
+    }
+    return st;
+  }
 };
 
 DeviceCtx& device_ctx(int device) {
@@ -355,7 +386,7 @@ struct FixupLists {
   std::uint64_t cap = 0;
   std::vector<cudaStream_t> streams;
   FixupLists(const Artifact& a, size_t chunk, bool full, const std::vector<cudaStream_t>& ss) {
-    if (!a.image.interval_fast_path) return;
+    if (!a.image.interval_fast_path || chunk == 0) return;
     cap = full ? chunk : std::min<std::uint64_t>(chunk, chunk / 16 + 4096);
     streams = ss;
     for (auto s : ss) {
@@ -387,10 +418,12 @@ void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
   const size_t elem = 8;
   if (kind == MemKind::Device) {
     const size_t max_chunk = size_t{1} << 30;
-    FixupLists fix(a, std::min(n, max_chunk), full_fixup, {user_stream});
+    // a caller-bound list (deferred checks) is reused; otherwise per call
+    const bool own_list = proto.list == 0;
+    FixupLists fix(a, own_list ? std::min(n, max_chunk) : 0, full_fixup, {user_stream});
     for (size_t off = 0; off < n; off += max_chunk) {
       LaunchArgs la = proto;
-      fix.bind(la, 0);
+      if (own_list) fix.bind(la, 0);
       la.n = std::min(max_chunk, n - off);
       la.ins.clear();
       la.outs.clear();
@@ -693,6 +726,26 @@ pe_status pe_synchronize(const pe_exec* exec) {
     if (exec && exec->device >= 0) check_cuda(cudaSetDevice(exec->device), "cudaSetDevice");
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    DeviceCtx& c = device_ctx(dev);
+    unsigned* status = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(c.state_mu);
+      auto it = c.states.find(s);
+      if (it != c.states.end()) status = it->second.status;
+    }
+    if (!status) return PE_OK;
+    unsigned h = 0;
+    check_cuda(cudaMemcpy(&h, status, sizeof h, cudaMemcpyDeviceToHost), "status D2H");
+    if (h) check_cuda(cudaMemset(status, 0, sizeof h), "status reset");
+    if (h & 2) return fail(PE_EINVAL, "invalid interval endpoints (NaN or lo > hi) in a deferred call");
+    if (h & 1) {
+      return fail(PE_EOVERFLOW,
+                  "a coordinate exceeded the proven int64 bound in a deferred call "
+                  "(re-run with synchronous checks to derive the batch bounds)");
+    }
+    if (h & 4) return fail(PE_ELOGIC, "interval fixup list overflow in a deferred call");
     return PE_OK;
   });
 }
@@ -741,6 +794,20 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
     const Artifact& a = p.loaded(lower::Domain::Interval, dev);
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    if (exec && exec->deferred_checks && kind == MemKind::Device) {
+      // no host round trip: status accumulates on the stream, the fixup
+      // list has full capacity (cannot overflow)
+      StreamState& st = device_ctx(dev).state(s, std::min<size_t>(n, size_t{1} << 30));
+      LaunchArgs la;
+      la.flag = reinterpret_cast<std::uint64_t>(st.status);
+      if (a.image.interval_fast_path) {
+        la.list = reinterpret_cast<std::uint64_t>(st.list);
+        la.count = reinterpret_cast<std::uint64_t>(st.count);
+        la.cap = st.list_cap;
+      }
+      run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false);
+      return PE_OK;
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
       Flag flag(s);
       LaunchArgs la;
@@ -779,6 +846,19 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
                       : p.i64_uniform_bound;
     if (caller_bounds && !i64_proof_holds(p, bounds.data())) {
       return fail(PE_EOVERFLOW, "int64 range proof fails for the asserted coordinate bounds");
+    }
+    if (exec && exec->deferred_checks && kind == MemKind::Device) {
+      // no host round trip: the bound check writes the stream's status word
+      const std::vector<std::uint64_t> b53 = caller_bounds ? bounds : p.i53_uniform_bound;
+      const bool tier53 = !force_int && i64_proof_holds(p, b53.data(), 53);
+      const Artifact& a =
+          p.loaded(tier53 ? lower::Domain::I64F : lower::Domain::I64, dev);
+      StreamState& st = device_ctx(dev).state(s, 0);
+      LaunchArgs la;
+      la.flag = reinterpret_cast<std::uint64_t>(st.status);
+      la.bounds = tier53 ? b53 : bounds;
+      run_batch(a, dev, kind, n, ins, {out}, la, s, false);
+      return PE_OK;
     }
     // Tier 1: every intermediate provably below 2^53 -> exact integer
     // arithmetic on the FP64 FMA pipe (one DFMA per record instead of a

@@ -146,8 +146,9 @@ class Emitter {
     emit_prologue();
     if (fast) {
       // exact fast path; points it cannot prove go to the fixup list
-      decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n";
+      decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n  .reg .pred %pb<4>;\n";
       body_ << "  mov.b64 %facc, 0;\n";
+      for (int i = 0; i < 4; ++i) body_ << "  setp.ne.b32 %pb" << i << ", %r3, %r3;\n";
       fast_ = true;
       emit_powers();
       emit_walk();
@@ -177,7 +178,7 @@ class Emitter {
       body_ << "  add.u64 %rd1, %rd1, %rd2;\n  bra $Lfix;\n";
       finish_entry();
       fix_ = false;
-      fix_entry = entry_text(img, img.fix_entry);
+      fix_entry = entry_text(img, img.fix_entry, 128);  // launched with 128 threads
       P_ = lanes;
       sync_every_ = sync;
     }
@@ -223,7 +224,9 @@ class Emitter {
 
   // Both entries of a module take the same parameter list, so one argument
   // array launches either.
-  std::string entry_text(const KernelImage& img, const std::string& name) const {
+  std::string entry_text(const KernelImage& img, const std::string& name,
+                         std::uint32_t maxntid = 0) const {
+    if (maxntid == 0) maxntid = img.block;
     std::ostringstream m;
     m << ".visible .entry " << name << "(";
     bool first = true;
@@ -245,7 +248,7 @@ class Emitter {
       param(".param .u64 pe_cap");
     }
     if (n_param_ > 0) param(".param .align 8 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
-    m << ")\n.maxntid " << img.block << ", 1, 1\n{\n";
+    m << ")\n.maxntid " << maxntid << ", 1, 1\n{\n";
     m << "  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n";
     m << decls_.str() << body_.str() << "}\n\n";
     return m.str();
@@ -679,6 +682,24 @@ class Emitter {
   //    rule or a zero that the next step flags; NaN/inf always reach one of
   //    the two products ({A1,A2} and {B1,B2} are both endpoint pairs).
   void fnext(const std::string& dst, const std::string& src, bool up) {
+    if (fma_next_) {
+      // FP64-pipe nextafter: RN(v +- |v| * phi), phi = 2^-53 (1 + 2^-52).
+      // For a finite normal v the exact increment is strictly between 1/2
+      // and 3/2 of the spacing on its side, so RN lands on the neighbour
+      // (also across binades and into the subnormal range, and DBL_MAX up
+      // gives +inf). For 0 and subnormals it returns v unchanged — caught by
+      // the equality test, OR-accumulated into 4 rotating predicates so the
+      // checks do not form one serial chain; inf gives NaN, caught at the
+      // end.
+      const std::string a = tmp_f();
+      body_ << "  abs.f64 " << a << ", " << src << ";\n";
+      if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
+      body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n"
+            << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << dst << ", " << src << ", %pb" << (nb_ & 3)
+            << ";\n";
+      ++nb_;
+      return;
+    }
     const std::string u = tmp_u(), s = tmp_u(), d = tmp_u(), r = tmp_u(), x = tmp_u();
     body_ << "  mov.b64 " << u << ", " << src << ";\n"
           << "  shr.s64 " << s << ", " << u << ", 63;\n"
@@ -740,6 +761,11 @@ class Emitter {
     const std::string lo = tmp_f(), hi = tmp_f();
     body_ << "  mul.rn.f64 " << lo << ", " << A1 << ", " << B1 << ";\n"
           << "  mul.rn.f64 " << hi << ", " << A2 << ", " << B2 << ";\n";
+    if (fma_next_) {
+      fnext(dlo, lo, false);
+      fnext(dhi, hi, true);
+      return;
+    }
     // product sign is known: next_down(lo) = lo - d, next_up(hi) = hi + d,
     // d = -1 for negative products, +1 for positive ones
     const std::string d = tmp_u(), ul = tmp_u(), uh = tmp_u(), rl = tmp_u(), rh = tmp_u(),
@@ -795,7 +821,10 @@ class Emitter {
             << "  add.u64 %rd10, %rd9, %ix0;\n  st.global.b64 [%rd10], %facc;\n  bra $Ldone;\n";
     }
     // special: append the thread's valid point indices to the fixup list
-    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n  @!%pslow bra $Lfaststore;\n"
+    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n"
+          << "  or.pred %pslow, %pslow, %pb0;\n  or.pred %pslow, %pslow, %pb1;\n"
+          << "  or.pred %pslow, %pslow, %pb2;\n  or.pred %pslow, %pslow, %pb3;\n"
+          << "  @!%pslow bra $Lfaststore;\n"
           << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
           << "  ld.param.u64 %rd15, [pe_list];\n  cvta.to.global.u64 %rd15, %rd15;\n"
           << "  ld.param.u64 %rd16, [pe_cap];\n"
@@ -886,6 +915,13 @@ class Emitter {
   std::uint32_t imm_mode_;
   bool fast_ = false;  // emitting the interval fast path
   bool fix_ = false;   // emitting the fixup entry
+  // fast-path nextafter on the FP64 pipe (default) or as integer +-1 with
+  // sign-flip detection (PE_IV_NEXT=int)
+  bool fma_next_ = [] {
+    const char* e = std::getenv("PE_IV_NEXT");
+    return !(e && std::string(e) == "int");
+  }();
+  std::uint32_t nb_ = 0;
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;

@@ -1,3 +1,6 @@
 set -x
 timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest.log
-timeout 1200 bash scripts/gpu_sweep5.sh > gpurun_out/sweep5.log 2>&1
+for c in c3 c5; do
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+done
+timeout 1200 bash scripts/gpu_sweep5.sh > gpurun_out/sweep5b.log 2>&1

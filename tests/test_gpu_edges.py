@@ -125,7 +125,9 @@ def test_repeatable_and_shard_invariant(cuda_device):
     assert torch.equal(full, again) and torch.equal(full, halves)
 
 
-def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch):
+@pytest.mark.parametrize("next_mode", ["fma", "int"])
+def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch, next_mode):
+    monkeypatch.setenv("PE_IV_NEXT", next_mode)
     # The fast interval path (sign-case products, integer nextafter with
     # sign-flip detection) must equal the strict replay and the oracle on
     # intervals that straddle zero, touch zero, underflow and overflow.
@@ -159,3 +161,31 @@ def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch):
         for a, b, c in zip(f, s, o):
             assert np.array_equal(a.view(np.int64), c.view(np.int64))
             assert np.array_equal(b.view(np.int64), c.view(np.int64))
+
+
+def test_deferred_checks_same_results_and_late_errors(cuda_device):
+    import torch
+    w3, w5 = W.c3(), W.c5()
+    p3, p5 = pe.compile(w3.poly, w3.schemes), pe.compile(w5.poly, w5.schemes)
+    x3 = [_t(a, cuda_device) for a in w3.points(70_001)]
+    lo, hi = w5.points(70_001)
+    x5 = ([_t(lo[0], cuda_device)], [_t(hi[0], cuda_device)])
+    e3 = pe.Evaluator(pe.BigIntDomain(), p3, deferred_checks=True)
+    e5 = pe.Evaluator(pe.IntervalDomain(), p5, deferred_checks=True)
+    a3, (a5l, a5h) = e3.evaluate(x3), e5.evaluate(x5)
+    e3.synchronize()
+    b3 = pe.Evaluator(pe.BigIntDomain(), p3).evaluate(x3)
+    b5l, b5h = pe.Evaluator(pe.IntervalDomain(), p5).evaluate(x5)
+    assert torch.equal(a3, b3) and torch.equal(a5l, b5l) and torch.equal(a5h, b5h)
+    # a bound violation surfaces at synchronize(), not at the call
+    bad = [x3[0].clone(), x3[1].clone()]
+    bad[0][5] = 1 << 40
+    e3.evaluate(bad)
+    with pytest.raises(OverflowError):
+        e3.synchronize()
+    e3.synchronize()  # status was reset
+    badlo = x5[0][0].clone()
+    badlo[3] = 5.0  # lo > hi
+    e5.evaluate(([badlo], x5[1]))
+    with pytest.raises(ValueError):
+        e5.synchronize()
