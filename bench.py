@@ -284,8 +284,20 @@ def run_native(args, world, rank, local):
     # FP64 / int64-MAD pipe peak on this GPU (roofline denominator)
     import ctypes as C
     from paper_1307_5655_b200 import _lib as L
+    # int64 programs run on the FP64 pipe when the 2^53 exactness proof holds
+    # for the data's range (C3: |x|,|y| <= 2); the denominator is the pipe used
+    int_tier = "fp64-exact"
+    if domain == "i64":
+        _, b53 = progs[0].i64_bounds()
+        coord_max = [int(t.abs().max().item()) for t in inputs]
+        if not all(m <= b for m, b in zip(coord_max, b53)):
+            int_tier = "int64-imad"
     peak, sms = C.c_double(), C.c_int32()
-    L.check(L.lib().pe_measure_peak(local, 1 if domain == "i64" else 0, C.byref(peak), C.byref(sms)))
+    L.check(L.lib().pe_measure_peak(local, 1 if int_tier == "int64-imad" and domain == "i64" else 0,
+                                    C.byref(peak), C.byref(sms)))
+    int_peak = C.c_double()
+    if domain == "i64":
+        L.check(L.lib().pe_measure_peak(local, 1, C.byref(int_peak), C.byref(sms)))
 
     # L2 flush buffer (> 126 MB L2) written between timed steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -339,15 +351,18 @@ def run_native(args, world, rank, local):
         algo_per_pt = info["walk_muls"] + info["power_muls"]
         unit_ops = "DFMA"
     elif domain == "i64":
-        algo_per_pt = info["walk_muls"]  # int64 MADs (adds fused)
-        unit_ops = "int64 MAD"
+        algo_per_pt = info["walk_muls"] + info["power_muls"]  # int64 MADs (adds fused)
+        unit_ops = ("exact DFMA (int64 MAD on the FP64 pipe)" if int_tier == "fp64-exact"
+                    else "int64 MAD")
     else:
         algo_per_pt = 2 * info["walk_adds"] + 4 * (info["walk_muls"] + info["power_muls"])
         unit_ops = "fp64 add/mul (interval endpoints)"
     achieved = algo_per_pt * n / (avg[top] * 1e-3)  # ops/s
     nominal = sms.value * 64 * 1.965e9
     roofline = {
-        "bound": "fp64" if domain != "i64" else "int64_mad",
+        "bound": "fp64" if (domain != "i64" or int_tier == "fp64-exact") else "int64_mad",
+        "int64_tier": int_tier if domain == "i64" else None,
+        "frac_vs_int64_mad_peak": (achieved / int_peak.value) if domain == "i64" else None,
         "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "Tops/s",
         "frac": achieved / peak.value,
         "peak_source": "measured live: pe_measure_peak microbenchmark (8 independent chains/thread, "

@@ -164,6 +164,16 @@ pe_status pe_program_ptx(const pe_program* program, int32_t domain, char* out,
 pe_status pe_program_compile_only(const pe_program* program, int32_t domain,
                                   uint64_t* cubin_bytes);
 
+/* int64 programs: per-variable coordinate bounds (nvars entries each) under
+ * which evaluation is provably wrap-free (bound63) and provably exact on the
+ * FP64 pipe (bound53, the faster tier). UINT64_MAX = unconstrained. */
+pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63,
+                                uint64_t* bound53);
+
+/* Number of kernels a fused pe_eval_f64 launches (wide programs are split
+ * into slices at outer-variable exponent boundaries). */
+pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices);
+
 /* Batch evaluation. coords: nvars pointers, each to n values. */
 pe_status pe_eval_f64(const pe_program* program, const double* const* coords,
                       size_t n, double* out, const pe_exec* exec);

@@ -70,6 +70,9 @@ EXPORTS = [
     ("pe_program_ptx", C.c_int,
      [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("pe_program_compile_only", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]),
+    ("pe_program_i64_bounds", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("pe_program_f64_slices", C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
     ("pe_eval_f64", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
     ("pe_eval_i64", C.c_int,

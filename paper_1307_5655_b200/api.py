@@ -217,6 +217,19 @@ class CompiledProgram:
                                                 C.byref(nb)))
         return {"fp_ops": fp.value, "int_ops": it.value, "ptx_bytes": nb.value}
 
+    def i64_bounds(self):
+        """(bound63, bound53): per-variable coordinate bounds for the exact
+        int64 kernel and the faster exact-on-FP64 tier."""
+        b63 = (C.c_uint64 * self.nvars)()
+        b53 = (C.c_uint64 * self.nvars)()
+        L.check(L.lib().pe_program_i64_bounds(self._h, b63, b53))
+        return list(b63), list(b53)
+
+    def f64_slices(self) -> int:
+        k = C.c_uint32()
+        L.check(L.lib().pe_program_f64_slices(self._h, C.byref(k)))
+        return k.value
+
     def compile_only(self, domain: int) -> int:
         nb = C.c_uint64()
         L.check(L.lib().pe_program_compile_only(self._h, domain, C.byref(nb)))

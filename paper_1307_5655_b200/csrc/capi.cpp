@@ -152,9 +152,78 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
   return *slot;
 }
 
+namespace {
+// Loads an artifact's cubin (context-independent library) and uploads its
+// global-tier coefficients to `device`. Caller holds the program mutex.
+void ensure_loaded(Artifact& a, int device);
+}  // namespace
+
 Artifact& Program::loaded(lower::Domain d, int device) const {
   Artifact& a = artifact(d, true);
   std::lock_guard<std::mutex> lock(mu);
+  ensure_loaded(a, device);
+  return a;
+}
+
+std::size_t Program::slice_count() const {
+  if (integer || nvars < 2) return 1;
+  std::size_t k = 0;
+  if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
+  if (k == 0) {
+    // measured on C4 (profiles/r1_slice_experiment.txt): straight-line
+    // kernels beyond ~3k records pay for instruction fetch; ~3k per slice
+    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 3000, 2, 16) : 1;
+  }
+  return std::max<std::size_t>(1, k);
+}
+
+std::vector<const Artifact*> Program::f64_kernels(int device) const {
+  const std::size_t k = slice_count();
+  if (k <= 1) return {&loaded(lower::Domain::F64, device)};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!slices_planned) {
+    // terms are in decreasing lexicographic order: equal outer exponents are
+    // contiguous; cut at outer-exponent boundaries near multiples of T/k
+    const auto& terms = poly_f->terms();
+    const std::size_t T = terms.size();
+    std::vector<std::size_t> cuts{0};
+    for (std::size_t i = 1; i < T && cuts.size() < k; ++i) {
+      if (terms[i].exponents[0] != terms[i - 1].exponents[0] && i * k >= cuts.size() * T) {
+        cuts.push_back(i);
+      }
+    }
+    cuts.push_back(T);
+    std::vector<FunctionScheme> fs;
+    for (const auto& d : scheme_descs) fs.push_back(scheme_from_desc(d));
+    for (std::size_t s = 0; s + 1 < cuts.size(); ++s) {
+      std::vector<Term<double>> part(terms.begin() + static_cast<std::ptrdiff_t>(cuts[s]),
+                                     terms.begin() + static_cast<std::ptrdiff_t>(cuts[s + 1]));
+      Polynomial<double> sp = Polynomial<double>::canonicalize(std::move(part), variables);
+      EvaluationTree<double> t = build_multivariate(sp, std::span<const FunctionScheme>(fs));
+      compute_lazy_heights(t);
+      slice_progs.push_back(std::make_unique<CompiledProgram<double>>(compile(t)));
+      auto a = std::make_unique<Artifact>();
+      lower::KernelShape shape;
+      shape.accumulate = s > 0;
+      a->image = lower::emit_ptx(lower::lower_fused(*slice_progs.back()), lower::Domain::F64, shape);
+      CompileResult r = compile_ptx(a->image.ptx, a->image.entry);
+      if (!r.ok) throw std::logic_error(r.log);
+      a->cubin = std::move(r.cubin);
+      a->compile_seconds = r.seconds;
+      slice_arts.push_back(std::move(a));
+    }
+    slices_planned = true;
+  }
+  std::vector<const Artifact*> out;
+  for (auto& a : slice_arts) {
+    ensure_loaded(*a, device);
+    out.push_back(a.get());
+  }
+  return out;
+}
+
+namespace {
+void ensure_loaded(Artifact& a, int device) {
   if (!a.library) {
     check_cuda(cudaLibraryLoadData(&a.library, a.cubin.data(), nullptr, nullptr, 0, nullptr,
                                    nullptr, 0),
@@ -174,10 +243,7 @@ Artifact& Program::loaded(lower::Domain d, int device) const {
                "cudaMemcpy(global coefficients)");
     a.global_coefs[device] = p;
   }
-  return a;
 }
-
-namespace {
 
 // ------------------------------------------------------------------ launch
 
@@ -411,11 +477,14 @@ struct FixupLists {
   }
 };
 
-void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
+// `arts` run in order on each chunk (wide fp64 programs: slice 0 stores,
+// later slices accumulate); inputs are staged once per chunk for all of them.
+void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
                bool full_fixup = false) {
   const size_t elem = 8;
+  const Artifact& a = *arts.front();  // interval programs have exactly one
   if (kind == MemKind::Device) {
     const size_t max_chunk = size_t{1} << 30;
     // a caller-bound list (deferred checks) is reused; otherwise per call
@@ -429,7 +498,7 @@ void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
       la.outs.clear();
       for (auto p : ins) la.ins.push_back(reinterpret_cast<std::uint64_t>(static_cast<const char*>(p) + off * elem));
       for (auto p : outs) la.outs.push_back(reinterpret_cast<std::uint64_t>(static_cast<char*>(p) + off * elem));
-      launch(a, device, la, user_stream);
+      for (const Artifact* art : arts) launch(*art, device, la, user_stream);
     }
     if (sync) check_cuda(cudaStreamSynchronize(user_stream), "cudaStreamSynchronize");
     return;
@@ -467,7 +536,7 @@ void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
     for (size_t o = 0; o < outs.size(); ++o) {
       la.outs.push_back(reinterpret_cast<std::uint64_t>(c.buffers[slot][ins.size() + o]));
     }
-    launch(a, device, la, s);
+    for (const Artifact* art : arts) launch(*art, device, la, s);
     for (size_t o = 0; o < outs.size(); ++o) {
       check_cuda(cudaMemcpyAsync(static_cast<char*>(outs[o]) + off * elem,
                                  c.buffers[slot][ins.size() + o], m * elem, cudaMemcpyDeviceToHost, s),
@@ -476,6 +545,14 @@ void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
   }
   for (auto s : c.streams) check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   if (flag_ready) cudaEventDestroy(flag_ready);
+}
+
+void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
+               const std::vector<const void*>& ins, const std::vector<void*>& outs,
+               const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
+               bool full_fixup = false) {
+  run_batch(std::vector<const Artifact*>{&a}, device, kind, n, ins, outs, proto, user_stream, sync,
+            full_fixup);
 }
 
 // ------------------------------------------------------------------ errors
@@ -532,7 +609,14 @@ void build_program(Program& p, const std::uint32_t* exps, const C* coeffs, size_
   p.nterms = poly.terms().size();
   p.variables = vars;
   p.stats = program_stats(*prog);
-  if constexpr (std::is_same_v<C, std::int64_t>) p.terms_i = poly.terms();
+  if constexpr (std::is_same_v<C, std::int64_t>) {
+    p.terms_i = poly.terms();
+  } else {
+    p.poly_f = std::make_unique<Polynomial<double>>(poly);
+  }
+  for (std::uint32_t v = 0; v < nvars; ++v) {
+    p.scheme_descs.push_back(SchemeDesc{schemes[v].upper, schemes[v].lower, schemes[v].cutoff});
+  }
 }
 
 }  // namespace
@@ -698,6 +782,27 @@ pe_status pe_program_ptx(const pe_program* program, int32_t domain, char* out, s
   });
 }
 
+pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63, uint64_t* bound53) {
+  return guarded([&]() -> pe_status {
+    if (!program) return fail(PE_EINVAL, "null argument");
+    const Program& p = program->impl;
+    if (!p.integer) return fail(PE_EINVAL, "program has fp64 coefficients");
+    for (uint32_t v = 0; v < p.nvars; ++v) {
+      if (bound63) bound63[v] = p.i64_uniform_bound[v];
+      if (bound53) bound53[v] = p.i53_uniform_bound[v];
+    }
+    return PE_OK;
+  });
+}
+
+pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices) {
+  return guarded([&]() -> pe_status {
+    if (!program || !slices) return fail(PE_EINVAL, "null argument");
+    *slices = static_cast<uint32_t>(program->impl.slice_count());
+    return PE_OK;
+  });
+}
+
 pe_status pe_program_compile_only(const pe_program* program, int32_t domain, uint64_t* cubin_bytes) {
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "null argument");
@@ -764,13 +869,14 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     MemKind kind;
     const int dev = resolve_device(exec, out, &kind);
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
-    const lower::Domain d = strict ? lower::Domain::F64Strict : lower::Domain::F64;
-    const Artifact& a = p.loaded(d, dev);
+    const std::vector<const Artifact*> arts =
+        strict ? std::vector<const Artifact*>{&p.loaded(lower::Domain::F64Strict, dev)}
+               : p.f64_kernels(dev);
     std::vector<const void*> ins(coords, coords + p.nvars);
     std::vector<void*> outs{out};
     LaunchArgs la;
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
-    run_batch(a, dev, kind, n, ins, outs, la, s, exec && exec->synchronize);
+    run_batch(arts, dev, kind, n, ins, outs, la, s, exec && exec->synchronize);
     return PE_OK;
   });
 }

@@ -114,7 +114,9 @@ class Emitter {
  public:
   Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
-        imm_mode_(shape.imm_mode) {}
+        imm_mode_(shape.imm_mode), accumulate_(shape.accumulate) {
+    if (accumulate_ && d_ != Domain::F64) throw std::logic_error("accumulate is fp64-only");
+  }
 
   KernelImage run() {
     KernelImage img;
@@ -901,8 +903,15 @@ class Emitter {
           body_ << "  cvt.rni.s64.f64 " << t << ", " << val << ";\n";
           val = t;
         }
-        body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  @%pv" << k << " st.global."
-              << ioty() << " [%rd10], " << val << ";\n";
+        if (accumulate_) {
+          const std::string old = tmp_f(), sum = tmp_f();
+          body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  ld.global.f64 " << old
+                << ", [%rd10];\n  add.rn.f64 " << sum << ", " << old << ", " << val << ";\n";
+          val = sum;
+        } else {
+          body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n";
+        }
+        body_ << "  @%pv" << k << " st.global." << ioty() << " [%rd10], " << val << ";\n";
       }
     }
   }
@@ -913,6 +922,7 @@ class Emitter {
   std::uint32_t block_;
   std::uint32_t sync_every_;
   std::uint32_t imm_mode_;
+  bool accumulate_ = false;
   bool fast_ = false;  // emitting the interval fast path
   bool fix_ = false;   // emitting the fixup entry
   // fast-path nextafter on the FP64 pipe (default) or as integer +-1 with

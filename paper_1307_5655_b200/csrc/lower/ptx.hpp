@@ -71,6 +71,9 @@ struct KernelShape {
   // coefficient delivery: 0 constant bank (LDC/LDCU), 1 immediates (MOV
   // pairs), 2 alternate words, 3 immediates beyond the constant-bank tier
   std::uint32_t imm_mode = 0;
+  // fp64 slices of a wide program: add the slice value into the result
+  // instead of storing it (out[i] += v)
+  bool accumulate = false;
 };
 
 /// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC

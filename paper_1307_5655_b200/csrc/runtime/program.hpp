@@ -43,6 +43,14 @@ struct Program {
 
   std::unique_ptr<EvaluationTree<double>> tree_f;
   std::unique_ptr<CompiledProgram<double>> prog_f;
+  // fp64 slicing of wide multivariate programs: terms split at outer-variable
+  // exponent boundaries into K sub-polynomials, each compiled with the same
+  // schemes; slice 0 stores, slices 1..K-1 accumulate (fused fp64 only).
+  std::unique_ptr<Polynomial<double>> poly_f;
+  std::vector<SchemeDesc> scheme_descs;
+  mutable std::vector<std::unique_ptr<CompiledProgram<double>>> slice_progs;
+  mutable std::vector<std::unique_ptr<Artifact>> slice_arts;
+  mutable bool slices_planned = false;
   std::unique_ptr<EvaluationTree<std::int64_t>> tree_i;
   std::unique_ptr<CompiledProgram<std::int64_t>> prog_i;
   std::vector<Term<std::int64_t>> terms_i;  // canonical terms (int64 proof)
@@ -61,6 +69,10 @@ struct Program {
   Artifact& artifact(lower::Domain d, bool need_cubin) const;
   /// Loaded kernel handle + global-tier coefficients on `device`.
   Artifact& loaded(lower::Domain d, int device) const;
+  /// Kernels pe_eval_f64 (fused) launches in order: the whole program, or
+  /// its slices for wide programs.
+  std::vector<const Artifact*> f64_kernels(int device) const;
+  std::size_t slice_count() const;
 };
 
 /// Overflow proof for the exact int64 path: every intermediate of the walk

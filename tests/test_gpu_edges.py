@@ -189,3 +189,23 @@ def test_deferred_checks_same_results_and_late_errors(cuda_device):
     e5.evaluate(([badlo], x5[1]))
     with pytest.raises(ValueError):
         e5.synchronize()
+
+
+@pytest.mark.parametrize("slices", ["1", "3", "7"])
+def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
+    # wide fp64 programs run as K slice kernels (store, then accumulate);
+    # any K must stay inside the fused-fp64 tolerance, host or device buffers
+    monkeypatch.setenv("PE_SLICES", slices)
+    rng = np.random.default_rng(4)
+    ex = np.unique(rng.integers(0, 20, size=(3000, 3)), axis=0).astype(np.uint32)
+    p = pe.Polynomial(ex, rng.normal(size=len(ex)), ("x", "y", "z"))
+    sch = [pe.builtin_scheme("balanced")] * 3
+    prog = pe.compile(p, sch)
+    pts = [rng.uniform(-1, 1, 10_007) for _ in range(3)]
+    ref = pyoracle.Oracle(p, sch).eval_f64(pts)
+    scale = pyoracle.abs_term_sum(p, pts)
+    ev = pe.Evaluator(pe.DoubleDomain(), prog)
+    dev = ev.evaluate([_t(a, cuda_device) for a in pts]).cpu().numpy()
+    host = ev.evaluate(pts)
+    assert np.all(np.abs(dev - ref) <= 1e-12 * scale)
+    assert np.array_equal(dev.view(np.int64), host.view(np.int64))
