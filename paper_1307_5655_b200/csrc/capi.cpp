@@ -170,9 +170,10 @@ std::size_t Program::slice_count() const {
   std::size_t k = 0;
   if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
   if (k == 0) {
-    // measured on C4 (profiles/r1_slice_experiment.txt): straight-line
-    // kernels beyond ~3k records pay for instruction fetch; ~3k per slice
-    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 3000, 2, 16) : 1;
+    // measured on C4 (profiles/r1_slices_c4.txt): straight-line kernels
+    // beyond a few thousand records pay for instruction fetch and register
+    // pressure (power tables); ~2k records per slice
+    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 2100, 2, 16) : 1;
   }
   return std::max<std::size_t>(1, k);
 }
