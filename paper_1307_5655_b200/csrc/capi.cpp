@@ -144,7 +144,7 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
     slot = std::move(a);
   }
   if (need_cubin && slot->cubin.empty()) {
-    CompileResult r = compile_ptx(slot->image.ptx, slot->image.entry);
+    CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);
     if (!r.ok) throw std::logic_error(r.log);
     slot->cubin = std::move(r.cubin);
     slot->compile_seconds = r.seconds;
@@ -207,7 +207,7 @@ std::vector<const Artifact*> Program::f64_kernels(int device) const {
       lower::KernelShape shape;
       shape.accumulate = s > 0;
       a->image = lower::emit_ptx(lower::lower_fused(*slice_progs.back()), lower::Domain::F64, shape);
-      CompileResult r = compile_ptx(a->image.ptx, a->image.entry);
+      CompileResult r = compile_ptx_cached(a->image.ptx, a->image.entry);
       if (!r.ok) throw std::logic_error(r.log);
       a->cubin = std::move(r.cubin);
       a->compile_seconds = r.seconds;

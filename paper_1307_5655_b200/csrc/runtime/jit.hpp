@@ -19,4 +19,10 @@ struct CompileResult {
 /// ptxas for sm_100a with -O3 and line info; never touches a GPU.
 CompileResult compile_ptx(const std::string& ptx, const std::string& tag);
 
+/// compile_ptx behind an on-disk cubin cache keyed by the PTX text
+/// (PE_CACHE_DIR, else $XDG_CACHE_HOME or ~/.cache /polyeval-b200;
+/// PE_CACHE_DIR=off disables). `cached` reports a hit.
+CompileResult compile_ptx_cached(const std::string& ptx, const std::string& tag,
+                                 bool* cached = nullptr);
+
 }  // namespace polyeval::rt
