@@ -178,6 +178,14 @@ pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices);
 pe_status pe_eval_f64(const pe_program* program, const double* const* coords,
                       size_t n, double* out, const pe_exec* exec);
 
+/* Several fused-fp64 programs (same variable count) over one point batch:
+ * results outs[j][i] = programs[j](point i). With host buffers the points
+ * cross PCIe once for all k programs (the reference analogue: k Evaluator
+ * sessions fed the same points). */
+pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
+                            const double* const* coords, size_t n,
+                            double* const* outs, const pe_exec* exec);
+
 pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords,
                       size_t n, int64_t* out, const pe_exec* exec);
 

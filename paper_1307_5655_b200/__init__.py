@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     builtin_scheme,
     compile,
     evaluate,
+    evaluate_many,
     launch_count,
     scheme_from_name,
     threshold_combine,

@@ -75,6 +75,9 @@ EXPORTS = [
     ("pe_program_f64_slices", C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
     ("pe_eval_f64", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_eval_f64_multi", C.c_int,
+     [C.POINTER(C.c_void_p), C.c_size_t, C.POINTER(C.c_void_p), C.c_size_t,
+      C.POINTER(C.c_void_p), C.POINTER(pe_exec)]),
     ("pe_eval_i64", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
     ("pe_eval_interval", C.c_int,

@@ -377,6 +377,22 @@ class Evaluator:
         return np.empty(n, dtype=np.int64 if kind == "i64" else np.float64)
 
 
+def evaluate_many(programs, points, outs=None, device: int = -1, stream=None):
+    """Fused-fp64 evaluation of several programs over one batch
+    (pe_eval_f64_multi): host points are staged to the GPU once."""
+    ev = Evaluator(DoubleDomain(), programs[0], device=device)
+    cols, n = ev._soa(points, np.float64)
+    dev = _is_torch_cuda(cols[0])
+    if outs is None:
+        outs = [Evaluator._alloc(n, "f64", dev, cols[0]) for _ in programs]
+    handles = (C.c_void_p * len(programs))(*[p.handle.value for p in programs])
+    ptrs = (C.c_void_p * len(cols))(*[Evaluator._ptr(a) for a in cols])
+    optrs = (C.c_void_p * len(outs))(*[Evaluator._ptr(o) for o in outs])
+    ex = ev._exec(Evaluator._stream(stream, dev))
+    L.check(L.lib().pe_eval_f64_multi(handles, len(programs), ptrs, n, optrs, C.byref(ex)))
+    return outs
+
+
 def evaluate(program: CompiledProgram, points, domain):
     """One-shot convenience wrapper (reference eval.hpp:262-268)."""
     return Evaluator(domain, program).evaluate(points)

@@ -483,9 +483,19 @@ struct FixupLists {
 void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
-               bool full_fixup = false) {
+               bool full_fixup = false, const std::vector<size_t>& out_base = {}) {
   const size_t elem = 8;
   const Artifact& a = *arts.front();  // interval programs have exactly one
+  // art i writes outs[out_base[i] .. out_base[i] + n_out) (default: from 0)
+  auto launch_all = [&](const LaunchArgs& la, cudaStream_t st) {
+    for (size_t i = 0; i < arts.size(); ++i) {
+      LaunchArgs l = la;
+      const size_t b = out_base.empty() ? 0 : out_base[i];
+      l.outs.assign(la.outs.begin() + static_cast<std::ptrdiff_t>(b),
+                    la.outs.begin() + static_cast<std::ptrdiff_t>(b + arts[i]->image.n_out));
+      launch(*arts[i], device, l, st);
+    }
+  };
   if (kind == MemKind::Device) {
     const size_t max_chunk = size_t{1} << 30;
     // a caller-bound list (deferred checks) is reused; otherwise per call
@@ -499,7 +509,7 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
       la.outs.clear();
       for (auto p : ins) la.ins.push_back(reinterpret_cast<std::uint64_t>(static_cast<const char*>(p) + off * elem));
       for (auto p : outs) la.outs.push_back(reinterpret_cast<std::uint64_t>(static_cast<char*>(p) + off * elem));
-      for (const Artifact* art : arts) launch(*art, device, la, user_stream);
+      launch_all(la, user_stream);
     }
     if (sync) check_cuda(cudaStreamSynchronize(user_stream), "cudaStreamSynchronize");
     return;
@@ -537,7 +547,7 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     for (size_t o = 0; o < outs.size(); ++o) {
       la.outs.push_back(reinterpret_cast<std::uint64_t>(c.buffers[slot][ins.size() + o]));
     }
-    for (const Artifact* art : arts) launch(*art, device, la, s);
+    launch_all(la, s);
     for (size_t o = 0; o < outs.size(); ++o) {
       check_cuda(cudaMemcpyAsync(static_cast<char*>(outs[o]) + off * elem,
                                  c.buffers[slot][ins.size() + o], m * elem, cudaMemcpyDeviceToHost, s),
@@ -878,6 +888,41 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     LaunchArgs la;
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     run_batch(arts, dev, kind, n, ins, outs, la, s, exec && exec->synchronize);
+    return PE_OK;
+  });
+}
+
+pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
+                            const double* const* coords, size_t n, double* const* outs,
+                            const pe_exec* exec) {
+  return guarded([&]() -> pe_status {
+    if (!programs || k == 0) return fail(PE_EINVAL, "no programs");
+    if (n == 0) return PE_OK;
+    if (!coords || !outs) return fail(PE_EINVAL, "null buffer");
+    const std::uint32_t nv = programs[0] ? programs[0]->impl.nvars : 0;
+    for (size_t j = 0; j < k; ++j) {
+      if (!programs[j] || !outs[j]) return fail(PE_EINVAL, "null program or output");
+      if (programs[j]->impl.nvars != nv) return fail(PE_EINVAL, "programs differ in variable count");
+    }
+    for (uint32_t v = 0; v < nv; ++v) {
+      if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
+    }
+    MemKind kind;
+    const int dev = resolve_device(exec, outs[0], &kind);
+    check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    std::vector<const Artifact*> arts;
+    std::vector<size_t> base;
+    for (size_t j = 0; j < k; ++j) {
+      for (const Artifact* a : programs[j]->impl.f64_kernels(dev)) {
+        arts.push_back(a);
+        base.push_back(j);
+      }
+    }
+    std::vector<const void*> ins(coords, coords + nv);
+    std::vector<void*> o(outs, outs + k);
+    LaunchArgs la;
+    cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    run_batch(arts, dev, kind, n, ins, o, la, s, exec && exec->synchronize, false, base);
     return PE_OK;
   });
 }

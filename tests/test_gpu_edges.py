@@ -191,6 +191,17 @@ def test_deferred_checks_same_results_and_late_errors(cuda_device):
         e5.synchronize()
 
 
+def test_evaluate_many_matches_single_calls(cuda_device):
+    progs = [pe.compile(w.poly, w.schemes) for w in W.c2_all()]
+    pts = W.c2(1000, "estrin").points(250_001)
+    many_host = pe.evaluate_many(progs, pts)
+    many_dev = pe.evaluate_many(progs, [_t(a, cuda_device) for a in pts])
+    for p, h, d in zip(progs, many_host, many_dev):
+        single = pe.Evaluator(pe.DoubleDomain(), p).evaluate(pts)
+        assert np.array_equal(h.view(np.int64), single.view(np.int64))
+        assert np.array_equal(d.cpu().numpy().view(np.int64), single.view(np.int64))
+
+
 @pytest.mark.parametrize("slices", ["1", "3", "7"])
 def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
     # wide fp64 programs run as K slice kernels (store, then accumulate);
