@@ -338,7 +338,7 @@ class Evaluator:
                 out = (self._alloc(n, "f64", dev, lo_c[0]), self._alloc(n, "f64", dev, lo_c[0]))
             lo_p = (C.c_void_p * len(lo_c))(*[self._ptr(a) for a in lo_c])
             hi_p = (C.c_void_p * len(hi_c))(*[self._ptr(a) for a in hi_c])
-            ex = self._exec(self._stream(stream, dev))
+            ex = self._exec(self._stream(stream, lo_c[0]))
             L.check(lib.pe_eval_interval(self.program.handle, lo_p, hi_p, n, self._ptr(out[0]),
                                          self._ptr(out[1]), C.byref(ex)))
             return out
@@ -348,7 +348,7 @@ class Evaluator:
         if out is None:
             out = self._alloc(n, "i64" if integer else "f64", dev, cols[0])
         ptrs = (C.c_void_p * len(cols))(*[self._ptr(a) for a in cols])
-        ex = self._exec(self._stream(stream, dev), bounds=bounds)
+        ex = self._exec(self._stream(stream, cols[0]), bounds=bounds)
         fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
         L.check(fn(self.program.handle, ptrs, n, self._ptr(out), C.byref(ex)))
         return out
@@ -356,16 +356,20 @@ class Evaluator:
     def synchronize(self, stream=None):
         """Waits for the stream; raises any deferred domain-check failure."""
         import torch
-        ex = self._exec(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        if stream is None:
+            dev = torch.device("cuda", self.device) if self.device >= 0 else None
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        ex = self._exec(stream)
         L.check(L.lib().pe_synchronize(C.byref(ex)))
 
     @staticmethod
-    def _stream(stream, dev):
+    def _stream(stream, like):
+        """Explicit stream, else torch's current stream on the data's device."""
         if stream is not None:
             return stream
-        if dev:
+        if like is not None and _is_torch_cuda(like):
             import torch
-            return torch.cuda.current_stream().cuda_stream
+            return torch.cuda.current_stream(like.device).cuda_stream
         return None
 
     @staticmethod
@@ -388,7 +392,7 @@ def evaluate_many(programs, points, outs=None, device: int = -1, stream=None):
     handles = (C.c_void_p * len(programs))(*[p.handle.value for p in programs])
     ptrs = (C.c_void_p * len(cols))(*[Evaluator._ptr(a) for a in cols])
     optrs = (C.c_void_p * len(outs))(*[Evaluator._ptr(o) for o in outs])
-    ex = ev._exec(Evaluator._stream(stream, dev))
+    ex = ev._exec(Evaluator._stream(stream, cols[0]))
     L.check(L.lib().pe_eval_f64_multi(handles, len(programs), ptrs, n, optrs, C.byref(ex)))
     return outs
 
