@@ -152,14 +152,35 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ----------------------------------------------------------------- CPU legs
 
-def cpu_reference_rate(wls, sample_points: int, threads: int, pts_cache=None):
-    """points/s of the unmodified reference (oracle/_ref) on `threads` host
-    threads, one Evaluator session per thread over contiguous shards."""
+def cpu_kind():
+    """("reference", host threads) when the unmodified reference library was
+    built into oracle/_ref, else ("port", 1): the single-threaded C oracle."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
+    if pyoracle.ref_available():
+        return "reference", host_threads()
+    return "port", 1
+
+
+def cpu_reference_rate(wls, sample_points: int, threads: int, pts_cache=None):
+    """points/s of the unmodified reference (oracle/_ref) on `threads` host
+    threads, one Evaluator session per thread over contiguous shards (or of
+    the C oracle port when the reference library is absent)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    use_ref = pyoracle.ref_available()
     total_pts, total_s = 0, 0.0
     for wl in wls:
-        ref = pyoracle.Reference(wl.poly, wl.schemes)
+        if use_ref:
+            ref = pyoracle.Reference(wl.poly, wl.schemes)
+        else:
+            orc = pyoracle.Oracle(wl.poly, wl.schemes)
+
+            class _Port:  # same call shape as Reference, threads ignored
+                eval_f64 = staticmethod(lambda pts, t: orc.eval_f64(pts))
+                eval_i64 = staticmethod(lambda pts, t: orc.eval_i64(pts))
+                eval_interval = staticmethod(lambda lo, hi, t: orc.eval_interval(lo, hi))
+            ref = _Port()
         if wl.domain == "interval":
             lo, hi = wl.points(sample_points)
             t = time.perf_counter()
@@ -197,7 +218,7 @@ def run_reference_arm(args, world, rank):
     wls = workloads(args.config)
     if rank != 0:
         return
-    threads = host_threads()
+    kind, threads = cpu_kind()
     per_step = calibrate_sample(wls, threads, budget_s=max(1.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_reference_rate(wls, per_step, threads)
@@ -221,9 +242,10 @@ def run_reference_arm(args, world, rank):
                    "points_per_step": per_step * len(wls)},
         "term_evals_per_s": value * terms,
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads,
-                         "kind": "reference",
+                         "kind": kind,
                          "sample": f"{per_step} points per program per step, {len(wls)} programs, "
-                                   "unmodified reference Evaluator<D>, one session per thread"},
+                                   + ("unmodified reference Evaluator<D>, one session per thread"
+                                      if kind == "reference" else "C oracle port, 1 thread")},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -421,12 +443,14 @@ def run_native(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            threads = host_threads()
+            kind, threads = cpu_kind()
             per = calibrate_sample(wls, threads, args.cpu_seconds)
             rate, secs = cpu_reference_rate(wls, per, threads)
-            cpu = {"value": rate, "unit": "points/s", "cores": threads, "kind": "reference",
+            cpu = {"value": rate, "unit": "points/s", "cores": threads, "kind": kind,
                    "sample": f"{per} points per program x {len(wls)} programs "
-                             f"({secs:.1f} s), unmodified reference Evaluator<D> per thread"}
+                             f"({secs:.1f} s), "
+                             + ("unmodified reference Evaluator<D> per thread"
+                                if kind == "reference" else "C oracle port, 1 thread")}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "points/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}

@@ -193,3 +193,41 @@ def test_survey_table_counts():
     assert np.array_equal(d1.records(), d2.records()) and d1.info()["walk_adds"] == 1535
     c5 = pe.compile(W.c5().poly, W.c5().schemes).info()
     assert (c5["walk_adds"], c5["walk_muls"], c5["register_count"]) == (300, 200, 5)
+
+
+def test_c_abi_error_contract():
+    lib = L.lib()
+    exps = (C.c_uint32 * 2)(1, 0)
+    coefs = (C.c_double * 2)(1.0, 2.0)
+    h = C.c_void_p()
+    bad_scheme = (L.pe_scheme_desc * 1)(L.pe_scheme_desc(7, 0, 0))
+    assert lib.pe_program_create(exps, coefs, 2, 1, bad_scheme, 0, C.byref(h)) == L.PE_EINVAL
+    assert b"scheme" in lib.pe_last_error()
+    ok = (L.pe_scheme_desc * 1)(L.pe_scheme_desc(3, 3, 0))
+    assert lib.pe_program_create(exps, coefs, 2, 0, ok, 0, C.byref(h)) == L.PE_EINVAL  # nvars 0
+    assert lib.pe_program_create(None, coefs, 2, 1, ok, 0, C.byref(h)) == L.PE_EINVAL
+    assert lib.pe_program_create(exps, coefs, 2, 1, ok, 9, C.byref(h)) == L.PE_EINVAL  # coeff type
+    assert lib.pe_program_create(exps, coefs, 2, 1, None, 0, C.byref(h)) == L.PE_EINVAL
+    # zero terms is the zero polynomial, not an error
+    assert lib.pe_program_create(None, None, 0, 1, ok, 0, C.byref(h)) == L.PE_OK
+    lib.pe_program_destroy(h)
+    # eval with n == 0 is a no-op; null program is EINVAL (no GPU needed)
+    assert lib.pe_eval_f64(None, None, 0, None, None) == L.PE_EINVAL
+    with pytest.raises(ValueError):
+        pe.compile(pe.Polynomial(np.array([[1]]), np.array([1.0])), pe.FunctionScheme(
+            pe.BuiltinScheme.estrin, pe.BuiltinScheme.horner, 0)).kernel_stats(9)
+
+
+def test_scheme_range_violation_is_invalid_argument():
+    # reference tree.cpp:41-44: a split outside (0, k] throws invalid_argument;
+    # the builtins never do, so threshold on an out-of-range cutoff is the
+    # only way through the ABI — every builtin combination must stay valid
+    rng = np.random.default_rng(5)
+    for up in range(4):
+        for lo in range(4):
+            for cut in (1, 2, 3, 7, 100):
+                s = pe.FunctionScheme(pe.BuiltinScheme(up), pe.BuiltinScheme(lo), cut)
+                p = _random_poly(rng, max_degree=40)
+                rec, rc = pyoracle.Oracle(p, [s]).records()
+                prog = pe.compile(p, [s])
+                assert np.array_equal(prog.records(), rec) and prog.info()["register_count"] == rc

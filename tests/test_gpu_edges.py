@@ -220,3 +220,39 @@ def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
     host = ev.evaluate(pts)
     assert np.all(np.abs(dev - ref) <= 1e-12 * scale)
     assert np.array_equal(dev.view(np.int64), host.view(np.int64))
+
+
+def test_program_shared_across_host_threads(cuda_device):
+    # reference contract (eval.hpp:59-68): a compiled program is immutable and
+    # shareable; sessions may run concurrently. Here 6 host threads share one
+    # program (kernels JIT-compiled once), each on its own stream or host path.
+    import threading
+    import torch
+    wl = W.c2(1000, "balanced")
+    prog = pe.compile(wl.poly, wl.schemes)
+    pts = wl.points(200_003)
+    want = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(pts)
+    results, errors = {}, []
+
+    def work(i):
+        try:
+            if i % 2:
+                results[i] = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(pts)
+            else:
+                s = torch.cuda.Stream(device=cuda_device)
+                with torch.cuda.stream(s):
+                    cols = [torch.from_numpy(a).to(cuda_device) for a in pts]
+                    out = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(cols, stream=s.cuda_stream)
+                    s.synchronize()
+                results[i] = out.cpu().numpy()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for r in results.values():
+        assert np.array_equal(r.view(np.int64), want.view(np.int64))
