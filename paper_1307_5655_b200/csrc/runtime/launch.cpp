@@ -1,0 +1,272 @@
+// Launch runtime: kernel launches, host-staged pipelines, per-device and
+// per-stream state. See runtime/launch.hpp.
+#include "runtime/launch.hpp"
+
+#include <algorithm>
+#include <memory>
+#include <stdexcept>
+
+namespace polyeval::rt {
+
+std::atomic<std::uint64_t>& launch_counter() {
+  static std::atomic<std::uint64_t> n{0};
+  return n;
+}
+
+
+int sm_count(int device) {
+  static std::mutex m;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(m);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  check_cuda(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device), "SM count");
+  cache[device] = n;
+  return n;
+}
+
+void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
+  const auto& img = a.image;
+  std::uint64_t gcoef = 0;
+  if (!img.global_words.empty()) gcoef = reinterpret_cast<std::uint64_t>(a.global_coefs.at(device));
+  std::vector<std::uint64_t> vals;
+  vals.reserve(img.n_in + img.n_out + 4 + img.nvars);
+  for (auto v : la.ins) vals.push_back(v);
+  for (auto v : la.outs) vals.push_back(v);
+  vals.push_back(la.n);
+  vals.push_back(gcoef);
+  if (img.has_flag) vals.push_back(la.flag);
+  if (img.has_bounds) {
+    for (std::uint32_t v = 0; v < img.nvars; ++v) vals.push_back(la.bounds.at(v));
+  }
+  if (img.interval_fast_path) {
+    if (!la.list || !la.count) throw std::logic_error("interval fast path needs a fixup list");
+    vals.push_back(la.list);
+    vals.push_back(la.count);
+    vals.push_back(la.cap);
+    check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(la.count), 0, sizeof(unsigned), stream),
+               "cudaMemsetAsync(fixup count)");
+  }
+  std::vector<void*> args;
+  for (auto& v : vals) args.push_back(&v);
+  if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
+  // Small batches: shrink the CTA (the kernel reads its tile size from
+  // %ntid; .maxntid is only an upper bound) until every SM has work.
+  std::uint64_t block = img.block;
+  const std::uint64_t want_ctas = 2 * static_cast<std::uint64_t>(sm_count(device));
+  while (block > 64 && block % 64 == 0 && (la.n + block * img.lanes - 1) / (block * img.lanes) < want_ctas) {
+    block /= 2;
+  }
+  const std::uint64_t tile = block * img.lanes;
+  const std::uint64_t grid = (la.n + tile - 1) / tile;
+  if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
+  check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.kernel),
+                              dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
+                              args.data(), 0, stream),
+             "cudaLaunchKernel(walk)");
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  if (img.interval_fast_path) {
+    // strict replay of the points the fast path could not prove; it reads
+    // the list length on the device, so no host round trip in between
+    const unsigned fix_grid = static_cast<unsigned>(
+        std::min<std::uint64_t>(2 * static_cast<std::uint64_t>(sm_count(device)),
+                                (la.cap + 127) / 128));
+    check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.fix_kernel), dim3(fix_grid ? fix_grid : 1),
+                                dim3(128), args.data(), 0, stream),
+               "cudaLaunchKernel(fixup)");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+  }
+}
+
+
+MemKind classify(const void* p, int* device) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return MemKind::Host;
+  }
+  if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+    if (device) *device = attr.device;
+    return MemKind::Device;
+  }
+  return MemKind::Host;
+}
+
+
+
+DeviceCtx& device_ctx(int device) {
+  static std::mutex g;
+  static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;
+  std::lock_guard<std::mutex> lock(g);
+  auto& c = ctxs[device];
+  if (!c) {
+    c = std::make_unique<DeviceCtx>();
+    for (auto& s : c->streams) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device),
+               "cudaDeviceGetAttribute");
+  }
+  return *c;
+}
+
+static void ensure_buffers(DeviceCtx& c, size_t arrays, size_t bytes) {
+  if (c.cap >= bytes && c.buffers[0].size() >= arrays) return;
+  for (auto& slot : c.buffers) {
+    for (void* p : slot) cudaFree(p);
+    slot.clear();
+  }
+  c.cap = std::max(bytes, c.cap);
+  for (auto& slot : c.buffers) {
+    for (size_t i = 0; i < arrays; ++i) {
+      void* p = nullptr;
+      check_cuda(cudaMalloc(&p, c.cap), "cudaMalloc(staging)");
+      slot.push_back(p);
+    }
+  }
+}
+
+int resolve_device(const pe_exec* ex, const void* probe, MemKind* kind) {
+  int ptr_dev = -1;
+  *kind = classify(probe, &ptr_dev);
+  if (ex && ex->device >= 0) {
+    if (*kind == MemKind::Device && ptr_dev >= 0 && ptr_dev != ex->device) {
+      throw std::invalid_argument("device pointer does not belong to exec->device");
+    }
+    return ex->device;
+  }
+  if (*kind == MemKind::Device && ptr_dev >= 0) return ptr_dev;
+  int cur = 0;
+  check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+  return cur;
+}
+
+
+/// Runs `la` over [0, n): device pointers in place on `stream`; host pointers
+/// through a 3-slot chunked H2D / kernel / D2H pipeline on the device's own
+/// streams (copy engines overlap the walk of the neighbouring chunk).
+/// `flag_dev` (may be null) is the device status word for domain checks.
+// Device scratch for the interval fixup list: one (list, count) per pipeline
+// slot. Capacity 1/16 of the chunk by default (special points are rare); the
+// full chunk after an overflow.
+namespace {
+struct FixupLists {
+  std::vector<void*> lists, counts;
+  std::uint64_t cap = 0;
+  std::vector<cudaStream_t> streams;
+  FixupLists(const Artifact& a, size_t chunk, bool full, const std::vector<cudaStream_t>& ss) {
+    if (!a.image.interval_fast_path || chunk == 0) return;
+    cap = full ? chunk : std::min<std::uint64_t>(chunk, chunk / 16 + 4096);
+    streams = ss;
+    for (auto s : ss) {
+      void *l = nullptr, *c = nullptr;
+      check_cuda(cudaMallocAsync(&l, 4 * cap, s), "cudaMallocAsync(fixup list)");
+      check_cuda(cudaMallocAsync(&c, 4, s), "cudaMallocAsync(fixup count)");
+      lists.push_back(l);
+      counts.push_back(c);
+    }
+  }
+  void bind(LaunchArgs& la, size_t slot) const {
+    if (lists.empty()) return;
+    la.list = reinterpret_cast<std::uint64_t>(lists[slot]);
+    la.count = reinterpret_cast<std::uint64_t>(counts[slot]);
+    la.cap = cap;
+  }
+  ~FixupLists() {
+    for (size_t i = 0; i < lists.size(); ++i) {
+      cudaFreeAsync(lists[i], streams[i]);
+      cudaFreeAsync(counts[i], streams[i]);
+    }
+  }
+};
+
+}  // namespace
+
+// `arts` run in order on each chunk (wide fp64 programs: slice 0 stores,
+// later slices accumulate); inputs are staged once per chunk for all of them.
+void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kind, size_t n,
+               const std::vector<const void*>& ins, const std::vector<void*>& outs,
+               const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
+               bool full_fixup, const std::vector<size_t>& out_base) {
+  const size_t elem = 8;
+  const Artifact& a = *arts.front();  // interval programs have exactly one
+  // art i writes outs[out_base[i] .. out_base[i] + n_out) (default: from 0)
+  auto launch_all = [&](const LaunchArgs& la, cudaStream_t st) {
+    for (size_t i = 0; i < arts.size(); ++i) {
+      LaunchArgs l = la;
+      const size_t b = out_base.empty() ? 0 : out_base[i];
+      l.outs.assign(la.outs.begin() + static_cast<std::ptrdiff_t>(b),
+                    la.outs.begin() + static_cast<std::ptrdiff_t>(b + arts[i]->image.n_out));
+      launch(*arts[i], device, l, st);
+    }
+  };
+  if (kind == MemKind::Device) {
+    const size_t max_chunk = size_t{1} << 30;
+    // a caller-bound list (deferred checks) is reused; otherwise per call
+    const bool own_list = proto.list == 0;
+    FixupLists fix(a, own_list ? std::min(n, max_chunk) : 0, full_fixup, {user_stream});
+    for (size_t off = 0; off < n; off += max_chunk) {
+      LaunchArgs la = proto;
+      if (own_list) fix.bind(la, 0);
+      la.n = std::min(max_chunk, n - off);
+      la.ins.clear();
+      la.outs.clear();
+      for (auto p : ins) la.ins.push_back(reinterpret_cast<std::uint64_t>(static_cast<const char*>(p) + off * elem));
+      for (auto p : outs) la.outs.push_back(reinterpret_cast<std::uint64_t>(static_cast<char*>(p) + off * elem));
+      launch_all(la, user_stream);
+    }
+    if (sync) check_cuda(cudaStreamSynchronize(user_stream), "cudaStreamSynchronize");
+    return;
+  }
+  DeviceCtx& c = device_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  const size_t chunk = std::clamp<size_t>(n / 8, size_t{1} << 18, size_t{1} << 23);
+  ensure_buffers(c, ins.size() + outs.size(), chunk * elem);
+  cudaEvent_t flag_ready = nullptr;
+  if (proto.flag) {
+    // the flag was initialised on user_stream: order the slots after it
+    check_cuda(cudaEventCreateWithFlags(&flag_ready, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(flag_ready, user_stream), "cudaEventRecord");
+    for (auto s : c.streams) check_cuda(cudaStreamWaitEvent(s, flag_ready, 0), "cudaStreamWaitEvent");
+  }
+  FixupLists fix(a, chunk, full_fixup,
+                 std::vector<cudaStream_t>(c.streams, c.streams + DeviceCtx::kSlots));
+  size_t k = 0;
+  for (size_t off = 0; off < n; off += chunk, ++k) {
+    const int slot = static_cast<int>(k % DeviceCtx::kSlots);
+    cudaStream_t s = c.streams[slot];
+    const size_t m = std::min(chunk, n - off);
+    LaunchArgs la = proto;
+    fix.bind(la, static_cast<size_t>(slot));
+    la.n = m;
+    la.ins.clear();
+    la.outs.clear();
+    for (size_t i = 0; i < ins.size(); ++i) {
+      void* d = c.buffers[slot][i];
+      check_cuda(cudaMemcpyAsync(d, static_cast<const char*>(ins[i]) + off * elem, m * elem,
+                                 cudaMemcpyHostToDevice, s),
+                 "cudaMemcpyAsync(H2D)");
+      la.ins.push_back(reinterpret_cast<std::uint64_t>(d));
+    }
+    for (size_t o = 0; o < outs.size(); ++o) {
+      la.outs.push_back(reinterpret_cast<std::uint64_t>(c.buffers[slot][ins.size() + o]));
+    }
+    launch_all(la, s);
+    for (size_t o = 0; o < outs.size(); ++o) {
+      check_cuda(cudaMemcpyAsync(static_cast<char*>(outs[o]) + off * elem,
+                                 c.buffers[slot][ins.size() + o], m * elem, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(D2H)");
+    }
+  }
+  for (auto s : c.streams) check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  if (flag_ready) cudaEventDestroy(flag_ready);
+}
+
+void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
+               const std::vector<const void*>& ins, const std::vector<void*>& outs,
+               const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
+               bool full_fixup) {
+  run_batch(std::vector<const Artifact*>{&a}, device, kind, n, ins, outs, proto, user_stream, sync,
+            full_fixup);
+}
+
+}  // namespace polyeval::rt

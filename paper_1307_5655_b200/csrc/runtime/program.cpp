@@ -1,0 +1,225 @@
+// Program: the front-end result plus lazily generated per-domain kernels
+// (lowering -> PTX -> cubin -> loaded library), the int64 overflow proof and
+// the fp64 slicing of wide programs. See runtime/program.hpp.
+#include "runtime/program.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lower/ptx.hpp"
+#include "lower/stream.hpp"
+#include "runtime/jit.hpp"
+
+namespace polyeval::rt {
+
+namespace {
+using u128 = unsigned __int128;
+constexpr u128 kSat = (static_cast<u128>(1) << 100);
+
+u128 sat_mul(u128 a, u128 b) {
+  if (a == 0 || b == 0) return 0;
+  if (a >= kSat || b >= kSat) return kSat;
+  if (a > kSat / b) return kSat;
+  return std::min<u128>(a * b, kSat);
+}
+u128 sat_pow(u128 base, std::uint32_t e) {
+  u128 r = 1;
+  while (e) {
+    if (e & 1) r = sat_mul(r, base);
+    e >>= 1;
+    if (e) base = sat_mul(base, base);
+  }
+  return r;
+}
+}  // namespace
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                    cudaGetErrorString(e) + ")");
+  }
+}
+
+bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bits) {
+  const u128 limit = static_cast<u128>(1) << limit_bits;
+  std::vector<u128> base(p.nvars);
+  for (std::uint32_t v = 0; v < p.nvars; ++v) base[v] = std::max<u128>(1, bounds[v]);
+  u128 m = 0;
+  std::vector<std::uint32_t> max_e(p.nvars, 0);
+  for (const auto& t : p.terms_i) {
+    const u128 c = t.coefficient < 0 ? static_cast<u128>(-(t.coefficient + 1)) + 1
+                                     : static_cast<u128>(t.coefficient);
+    u128 term = c;
+    for (std::uint32_t v = 0; v < p.nvars; ++v) {
+      term = sat_mul(term, sat_pow(base[v], t.exponents[v]));
+      max_e[v] = std::max(max_e[v], t.exponents[v]);
+    }
+    m = std::min<u128>(m + term, kSat);
+  }
+  if (m >= limit) return false;
+  for (std::uint32_t v = 0; v < p.nvars; ++v) {
+    // coordinates themselves must be exact in the working type
+    if (limit_bits < 63 && static_cast<u128>(bounds[v]) > limit) return false;
+    if (sat_pow(base[v], max_e[v]) >= limit) return false;
+  }
+  return true;
+}
+
+std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits) {
+  std::vector<std::uint64_t> out(p.nvars, UINT64_MAX);
+  std::vector<bool> present(p.nvars, false);
+  for (const auto& t : p.terms_i) {
+    for (std::uint32_t v = 0; v < p.nvars; ++v) present[v] = present[v] || t.exponents[v] > 0;
+  }
+  // the exact-FP64 path converts coordinates to double: they must be < 2^53
+  // even for variables absent from the polynomial
+  const std::uint64_t absent = limit_bits == 53 ? (1ull << 53) : UINT64_MAX;
+  for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = absent;
+  std::uint64_t lo = 0, hi = limit_bits == 53 ? (1ull << 53) : (1ull << 62);
+  std::vector<std::uint64_t> probe(p.nvars);
+  auto ok = [&](std::uint64_t b) {
+    for (std::uint32_t v = 0; v < p.nvars; ++v) probe[v] = present[v] ? b : 0;
+    return i64_proof_holds(p, probe.data(), limit_bits);
+  };
+  if (!ok(0)) {
+    lo = 0;
+    for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? 0 : absent;
+    // even X = 1 overflows: every evaluation is refused
+    return out;
+  }
+  while (lo < hi) {  // largest b with ok(b)
+    const std::uint64_t mid = lo + (hi - lo + 1) / 2;
+    if (ok(mid)) lo = mid; else hi = mid - 1;
+  }
+  for (std::uint32_t v = 0; v < p.nvars; ++v) out[v] = present[v] ? lo : absent;
+  return out;
+}
+
+Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = artifacts[static_cast<int>(d)];
+  if (!slot) {
+    auto a = std::make_unique<Artifact>();
+    const bool strict = d == lower::Domain::F64Strict || d == lower::Domain::Interval;
+    if (integer) {
+      auto s = strict ? lower::lower_strict(*prog_i) : lower::lower_fused(*prog_i);
+      a->image = lower::emit_ptx(s, d);
+    } else {
+      if (d == lower::Domain::I64 || d == lower::Domain::I64F) {
+        throw std::invalid_argument("pe_eval_i64 needs a program with int64 coefficients");
+      }
+      auto s = strict ? lower::lower_strict(*prog_f) : lower::lower_fused(*prog_f);
+      a->image = lower::emit_ptx(s, d);
+    }
+    slot = std::move(a);
+  }
+  if (need_cubin && slot->cubin.empty()) {
+    CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);
+    if (!r.ok) throw std::logic_error(r.log);
+    slot->cubin = std::move(r.cubin);
+    slot->compile_seconds = r.seconds;
+  }
+  return *slot;
+}
+
+namespace {
+// Loads an artifact's cubin (context-independent library) and uploads its
+// global-tier coefficients to `device`. Caller holds the program mutex.
+void ensure_loaded(Artifact& a, int device);
+}  // namespace
+
+Artifact& Program::loaded(lower::Domain d, int device) const {
+  Artifact& a = artifact(d, true);
+  std::lock_guard<std::mutex> lock(mu);
+  ensure_loaded(a, device);
+  return a;
+}
+
+std::size_t Program::slice_count() const {
+  if (integer || nvars < 2) return 1;
+  std::size_t k = 0;
+  if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
+  if (k == 0) {
+    // measured on C4 (profiles/r1_slices_c4.txt): straight-line kernels
+    // beyond a few thousand records pay for instruction fetch and register
+    // pressure (power tables); ~2k records per slice
+    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 2100, 2, 16) : 1;
+  }
+  return std::max<std::size_t>(1, k);
+}
+
+std::vector<const Artifact*> Program::f64_kernels(int device) const {
+  const std::size_t k = slice_count();
+  if (k <= 1) return {&loaded(lower::Domain::F64, device)};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!slices_planned) {
+    // terms are in decreasing lexicographic order: equal outer exponents are
+    // contiguous; cut at outer-exponent boundaries near multiples of T/k
+    const auto& terms = poly_f->terms();
+    const std::size_t T = terms.size();
+    std::vector<std::size_t> cuts{0};
+    for (std::size_t i = 1; i < T && cuts.size() < k; ++i) {
+      if (terms[i].exponents[0] != terms[i - 1].exponents[0] && i * k >= cuts.size() * T) {
+        cuts.push_back(i);
+      }
+    }
+    cuts.push_back(T);
+    std::vector<FunctionScheme> fs;
+    for (const auto& d : scheme_descs) fs.push_back(scheme_from_desc(d));
+    for (std::size_t s = 0; s + 1 < cuts.size(); ++s) {
+      std::vector<Term<double>> part(terms.begin() + static_cast<std::ptrdiff_t>(cuts[s]),
+                                     terms.begin() + static_cast<std::ptrdiff_t>(cuts[s + 1]));
+      Polynomial<double> sp = Polynomial<double>::canonicalize(std::move(part), variables);
+      EvaluationTree<double> t = build_multivariate(sp, std::span<const FunctionScheme>(fs));
+      compute_lazy_heights(t);
+      slice_progs.push_back(std::make_unique<CompiledProgram<double>>(compile(t)));
+      auto a = std::make_unique<Artifact>();
+      lower::KernelShape shape;
+      shape.accumulate = s > 0;
+      a->image = lower::emit_ptx(lower::lower_fused(*slice_progs.back()), lower::Domain::F64, shape);
+      CompileResult r = compile_ptx_cached(a->image.ptx, a->image.entry);
+      if (!r.ok) throw std::logic_error(r.log);
+      a->cubin = std::move(r.cubin);
+      a->compile_seconds = r.seconds;
+      slice_arts.push_back(std::move(a));
+    }
+    slices_planned = true;
+  }
+  std::vector<const Artifact*> out;
+  for (auto& a : slice_arts) {
+    ensure_loaded(*a, device);
+    out.push_back(a.get());
+  }
+  return out;
+}
+
+namespace {
+void ensure_loaded(Artifact& a, int device) {
+  if (!a.library) {
+    check_cuda(cudaLibraryLoadData(&a.library, a.cubin.data(), nullptr, nullptr, 0, nullptr,
+                                   nullptr, 0),
+               "cudaLibraryLoadData");
+    check_cuda(cudaLibraryGetKernel(&a.kernel, a.library, a.image.entry.c_str()),
+               "cudaLibraryGetKernel");
+    if (!a.image.fix_entry.empty()) {
+      check_cuda(cudaLibraryGetKernel(&a.fix_kernel, a.library, a.image.fix_entry.c_str()),
+                 "cudaLibraryGetKernel(fix)");
+    }
+  }
+  if (!a.image.global_words.empty() && !a.global_coefs.count(device)) {
+    void* p = nullptr;
+    const size_t bytes = a.image.global_words.size() * 8;
+    check_cuda(cudaMalloc(&p, bytes), "cudaMalloc(global coefficients)");
+    check_cuda(cudaMemcpy(p, a.image.global_words.data(), bytes, cudaMemcpyHostToDevice),
+               "cudaMemcpy(global coefficients)");
+    a.global_coefs[device] = p;
+  }
+}
+}  // namespace
+
+}  // namespace polyeval::rt

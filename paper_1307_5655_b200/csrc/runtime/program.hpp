@@ -82,4 +82,9 @@ struct Program {
 /// limit_bits = 53 every intermediate is an exactly representable double.
 bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bits = 63);
 
+/// Largest B with the proof holding for |x_v| <= B on every variable present
+/// in the polynomial (absent variables: unconstrained, or 2^53 for the FP64
+/// tier, whose coordinates must be exact doubles).
+std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits);
+
 }  // namespace polyeval::rt
