@@ -120,6 +120,33 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ----------------------------------------------------------------- ncu
+
+NCU_CAPTURES = {  # committed `ncu --set full` captures of the dominant kernels
+    ("c2", "C2_estrin_d1000"): "profiles/r1_ncu_c2_estrin_d1000_raw.csv",
+    ("c2", "C2_balanced_d1000"): "profiles/r1_ncu_c2_balanced_d1000_raw.csv",
+    ("c2", "C2_estrin_d1023"): "profiles/r1_ncu_c2_estrin_d1023_raw.csv",
+    ("c2", "C2_balanced_d1023"): "profiles/r1_ncu_c2_balanced_d1023_raw.csv",
+}
+
+
+def ncu_traffic(cfg, program):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed ncu capture of this kernel (None when not captured)."""
+    import csv
+    path = NCU_CAPTURES.get((cfg, program))
+    if not path or not os.path.exists(os.path.join(ROOT, path)):
+        return None
+    rows = list(csv.reader(open(os.path.join(ROOT, path))))
+    head, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = head.index(name)
+        total += float(vals[i]) * scale.get(units[i], 1)
+    return {"bytes_per_launch": total, "source": path}
+
+
 # ----------------------------------------------------------------- dist
 
 def dist_setup(ngpus):
@@ -395,7 +422,8 @@ def run_native(args, world, rank, local):
         "issued_fp64_per_point": st["fp_ops"], "issued_int64_per_point": st["int_ops"],
         "hbm_frac": (bytes_in + bytes_out) / (avg[top] * 1e-3) / 1e9 /
                     json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else None,
-        "traffic": None,
+        "traffic": ncu_traffic(args.config, wls[top].name),
+        "algorithmic_bytes_per_launch": bytes_in + bytes_out,
         "per_program_ms": {w.name: round(a, 4) for w, a in zip(wls, avg)},
     }
 
