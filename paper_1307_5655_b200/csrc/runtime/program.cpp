@@ -5,7 +5,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <future>
 #include <memory>
+#include <thread>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -141,16 +143,16 @@ Artifact& Program::loaded(lower::Domain d, int device) const {
 }
 
 std::size_t Program::slice_count() const {
-  if (integer || nvars < 2) return 1;
+  if (integer) return 1;
   std::size_t k = 0;
   if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
   if (k == 0) {
     // measured on C4 (profiles/r1_slices_c4.txt): straight-line kernels
     // beyond a few thousand records pay for instruction fetch and register
     // pressure (power tables); ~2k records per slice
-    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 2100, 2, 16) : 1;
+    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 2100, 2, 256) : 1;
   }
-  return std::max<std::size_t>(1, k);
+  return std::min<std::size_t>(std::max<std::size_t>(1, k), std::max<std::size_t>(1, nterms));
 }
 
 std::vector<const Artifact*> Program::f64_kernels(int device) const {
@@ -175,18 +177,41 @@ std::vector<const Artifact*> Program::f64_kernels(int device) const {
       std::vector<Term<double>> part(terms.begin() + static_cast<std::ptrdiff_t>(cuts[s]),
                                      terms.begin() + static_cast<std::ptrdiff_t>(cuts[s + 1]));
       Polynomial<double> sp = Polynomial<double>::canonicalize(std::move(part), variables);
-      EvaluationTree<double> t = build_multivariate(sp, std::span<const FunctionScheme>(fs));
+      EvaluationTree<double> t = nvars == 1 ? build(sp, fs[0], 0)
+                                            : build_multivariate(sp, std::span<const FunctionScheme>(fs));
       compute_lazy_heights(t);
       slice_progs.push_back(std::make_unique<CompiledProgram<double>>(compile(t)));
       auto a = std::make_unique<Artifact>();
       lower::KernelShape shape;
       shape.accumulate = s > 0;
       a->image = lower::emit_ptx(lower::lower_fused(*slice_progs.back()), lower::Domain::F64, shape);
-      CompileResult r = compile_ptx_cached(a->image.ptx, a->image.entry);
-      if (!r.ok) throw std::logic_error(r.log);
-      a->cubin = std::move(r.cubin);
-      a->compile_seconds = r.seconds;
       slice_arts.push_back(std::move(a));
+    }
+    // ptxas the slices concurrently (independent modules; nvPTXCompiler
+    // handles are independent)
+    std::vector<std::future<CompileResult>> jobs;
+    const std::size_t width = std::max(1u, std::thread::hardware_concurrency());
+    for (std::size_t s = 0; s < slice_arts.size(); ++s) {
+      if (jobs.size() == width) {
+        // bounded fan-out: finish the oldest before starting another
+        CompileResult r = jobs.front().get();
+        jobs.erase(jobs.begin());
+        if (!r.ok) throw std::logic_error(r.log);
+        auto& done = slice_arts[s - width];
+        done->cubin = std::move(r.cubin);
+        done->compile_seconds = r.seconds;
+      }
+      const Artifact* a = slice_arts[s].get();
+      jobs.push_back(std::async(std::launch::async, [a] {
+        return compile_ptx_cached(a->image.ptx, a->image.entry);
+      }));
+    }
+    for (std::size_t i = 0; i < jobs.size(); ++i) {
+      CompileResult r = jobs[i].get();
+      if (!r.ok) throw std::logic_error(r.log);
+      auto& done = slice_arts[slice_arts.size() - jobs.size() + i];
+      done->cubin = std::move(r.cubin);
+      done->compile_seconds = r.seconds;
     }
     slices_planned = true;
   }

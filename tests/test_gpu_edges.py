@@ -222,6 +222,22 @@ def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
     assert np.array_equal(dev.view(np.int64), host.view(np.int64))
 
 
+def test_wide_univariate_program_is_sliced(cuda_device):
+    # dense degree 20000: sliced into ~2k-record kernels (slice k holds the
+    # terms of one exponent range; its tree has a large root partial degree)
+    rng = np.random.default_rng(12)
+    d = 20_000
+    p = pe.Polynomial(np.arange(d, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, d + 1))
+    sch = [pe.builtin_scheme("estrin")]
+    prog = pe.compile(p, sch)
+    assert prog.f64_slices() > 1
+    x = [rng.uniform(-1, 1, 3001)]
+    got = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(x)
+    ref = pyoracle.Oracle(p, sch).eval_f64(x)
+    scale = pyoracle.abs_term_sum(p, x)
+    assert np.all(np.abs(got - ref) <= 1e-12 * scale)
+
+
 def test_program_shared_across_host_threads(cuda_device):
     # reference contract (eval.hpp:59-68): a compiled program is immutable and
     # shareable; sessions may run concurrently. Here 6 host threads share one
