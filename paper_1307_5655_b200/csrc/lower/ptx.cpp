@@ -763,8 +763,22 @@ class Emitter {
     const std::string lo = tmp_f(), hi = tmp_f();
     body_ << "  mul.rn.f64 " << lo << ", " << A1 << ", " << B1 << ";\n"
           << "  mul.rn.f64 " << hi << ", " << A2 << ", " << B2 << ";\n";
-    if (fma_next_) {
+    if (fma_next_ && !hybrid_next_) {
       fnext(dlo, lo, false);
+      fnext(dhi, hi, true);
+      return;
+    }
+    if (fma_next_ && hybrid_next_) {
+      // pipe balance: the lower endpoint steps on the integer pipe (sign is
+      // known, so -/+1 on the bits; a sign flip marks +-0/NaN as special),
+      // the upper one on the FP64 pipe
+      const std::string d = tmp_u(), ul = tmp_u(), rl = tmp_u(), xl = tmp_u();
+      body_ << "  selp.b64 " << d << ", -1, 1, " << ng << ";\n"
+            << "  mov.b64 " << ul << ", " << lo << ";\n"
+            << "  sub.s64 " << rl << ", " << ul << ", " << d << ";\n"
+            << "  xor.b64 " << xl << ", " << rl << ", " << ul << ";\n"
+            << "  or.b64 %facc, %facc, " << xl << ";\n"
+            << "  mov.b64 " << dlo << ", " << rl << ";\n";
       fnext(dhi, hi, true);
       return;
     }
@@ -930,6 +944,13 @@ class Emitter {
   bool fma_next_ = [] {
     const char* e = std::getenv("PE_IV_NEXT");
     return !(e && std::string(e) == "int");
+  }();
+  // PE_IV_NEXT=hybrid: product lower endpoints step on the integer pipe,
+  // upper ones on FP64 — measured slower than all-FP64 on C5 (2.66 vs
+  // 2.42 ms per 1e7, profiles/r1_c5_next_modes.txt), so opt-in only
+  bool hybrid_next_ = [] {
+    const char* e = std::getenv("PE_IV_NEXT");
+    return e && std::string(e) == "hybrid";
   }();
   std::uint32_t nb_ = 0;
   std::vector<std::uint64_t> words_;
