@@ -29,6 +29,7 @@ extern "C" cudaError_t pe_launch_max_abs_i64(const long long* x, size_t n,
                                              unsigned long long* out, int sms,
                                              cudaStream_t stream);
 extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s);
+extern "C" cudaError_t pe_measure_dfma_latency(double* cycles_per_op);
 
 struct pe_program {
   polyeval::rt::Program impl;
@@ -297,12 +298,16 @@ pe_status pe_program_compile_only(const pe_program* program, int32_t domain, uin
 
 pe_status pe_measure_peak(int32_t device, int32_t kind, double* ops_per_s, int32_t* sms) {
   return guarded([&]() -> pe_status {
-    if (!ops_per_s || (kind != 0 && kind != 1)) return fail(PE_EINVAL, "bad argument");
+    if (!ops_per_s || kind < 0 || kind > 2) return fail(PE_EINVAL, "bad argument");
     if (device >= 0) check_cuda(cudaSetDevice(device), "cudaSetDevice");
     int dev = 0, n_sm = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     check_cuda(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev), "attr");
-    check_cuda(pe_measure_pipe_peak(kind, n_sm, ops_per_s), "pipe peak microbenchmark");
+    if (kind == 2) {
+      check_cuda(pe_measure_dfma_latency(ops_per_s), "DFMA latency microbenchmark");
+    } else {
+      check_cuda(pe_measure_pipe_peak(kind, n_sm, ops_per_s), "pipe peak microbenchmark");
+    }
     launch_counter().fetch_add(5, std::memory_order_relaxed);
     if (sms) *sms = n_sm;
     return PE_OK;

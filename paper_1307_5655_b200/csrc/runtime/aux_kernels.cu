@@ -91,7 +91,33 @@ __global__ void __launch_bounds__(256) imad64_peak_kernel(long long* out, int it
   if (s == 0x123456789LL) out[0] = s;
 }
 
+// one warp, one dependent DFMA chain: SM cycles per DFMA (latency)
+__global__ void dfma_latency_kernel(double* out, long long* cycles, int iters, double a, double b) {
+  double r = threadIdx.x * 1e-3;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) r = fma(r, a, b);
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) *cycles = t1 - t0;
+  if (r == 1234.5) out[0] = r;
+}
+
 }  // namespace
+
+// Dependent-DFMA latency in SM cycles (single warp, 4096-deep chain).
+extern "C" cudaError_t pe_measure_dfma_latency(double* cycles_per_op) {
+  void* buf = nullptr;
+  cudaError_t e = cudaMalloc(&buf, 64);
+  if (e != cudaSuccess) return e;
+  long long* cyc = reinterpret_cast<long long*>(static_cast<char*>(buf) + 32);
+  long long h = 0;
+  for (int rep = 0; rep < 2; ++rep) {
+    dfma_latency_kernel<<<1, 32>>>(static_cast<double*>(buf), cyc, 4096, 0.999999, 1e-7);
+  }
+  e = cudaMemcpy(&h, cyc, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  *cycles_per_op = static_cast<double>(h) / 4096.0;
+  return e;
+}
 
 // ops/s for one (warm) launch; 1 op = one DFMA / one 64-bit multiply-add
 extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s) {

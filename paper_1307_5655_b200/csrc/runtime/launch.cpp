@@ -219,7 +219,13 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
   }
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
-  const size_t chunk = std::clamp<size_t>(n / 8, size_t{1} << 18, size_t{1} << 23);
+  // 16+ chunks keep the un-overlapped first H2D / last D2H short; >= 256K
+  // points keep each walk launch large enough to fill the GPU
+  size_t chunk = std::clamp<size_t>(n / 16, size_t{1} << 18, size_t{1} << 22);
+  if (const char* e = std::getenv("PE_STAGE_CHUNK")) {
+    const long v = std::atol(e);
+    if (v >= 4096) chunk = static_cast<size_t>(v);
+  }
   ensure_buffers(c, ins.size() + outs.size(), chunk * elem);
   cudaEvent_t flag_ready = nullptr;
   if (proto.flag) {
