@@ -222,6 +222,43 @@ def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
     assert np.array_equal(dev.view(np.int64), host.view(np.int64))
 
 
+@pytest.mark.parametrize("domain", ["f64", "i64", "interval"])
+def test_no_out_of_bounds_writes(cuda_device, domain):
+    # compute-sanitizer is closed on this pool: check the tail handling
+    # directly — results for n points land in [0, n) and the canary words
+    # after them (and before them) stay untouched, for ragged n and every
+    # kernel shape (lanes x block) the runtime may pick
+    import torch
+    rng = np.random.default_rng(3)
+    if domain == "i64":
+        p = W.c3().poly
+        sch = W.c3().schemes
+    else:
+        p = pe.Polynomial(np.arange(300, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, 301))
+        sch = [pe.builtin_scheme("estrin")]
+    prog = pe.compile(p, sch)
+    for n in (1, 31, 33, 127, 1025, 4097, 70_001):
+        pad = 64
+        dt = torch.int64 if domain == "i64" else torch.float64
+        canary = 1 << 62 if domain == "i64" else 1e300  # no result can equal it
+        outs = [torch.full((n + 2 * pad,), canary, dtype=dt, device=cuda_device)
+                for _ in range(2 if domain == "interval" else 1)]
+        if domain == "i64":
+            cols = [torch.from_numpy(rng.integers(-2, 3, n)).to(cuda_device) for _ in range(p.nvars)]
+            pe.Evaluator(pe.BigIntDomain(), prog).evaluate(cols, out=outs[0][pad:pad + n])
+        elif domain == "f64":
+            cols = [torch.from_numpy(rng.uniform(-1, 1, n)).to(cuda_device)]
+            pe.Evaluator(pe.DoubleDomain(), prog).evaluate(cols, out=outs[0][pad:pad + n])
+        else:
+            lo = torch.from_numpy(rng.uniform(-1, 1, n)).to(cuda_device)
+            pe.Evaluator(pe.IntervalDomain(), prog).evaluate(
+                ([lo], [lo + 1e-6]), out=(outs[0][pad:pad + n], outs[1][pad:pad + n]))
+        for o in outs:
+            o = o.cpu()
+            assert bool((o[:pad] == canary).all()) and bool((o[pad + n:] == canary).all()), n
+            assert not bool((o[pad:pad + n] == canary).any()), n
+
+
 def test_wide_univariate_program_is_sliced(cuda_device):
     # dense degree 20000: sliced into ~2k-record kernels (slice k holds the
     # terms of one exponent range; its tree has a large root partial degree)
