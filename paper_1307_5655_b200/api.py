@@ -274,23 +274,30 @@ class Evaluator:
     """Batch evaluation session (reference Evaluator<D>, eval.hpp:69-90)."""
 
     def __init__(self, domain, program: CompiledProgram, device: int = -1,
-                 deferred_checks: bool = False):
-        """deferred_checks: device-pointer int64 / interval calls return
+                 deferred_checks: bool = False, synchronize: bool = False):
+        """CUDA-tensor calls are asynchronous on the stream they are enqueued
+        on (torch's current stream of the data's device unless `stream=` is
+        given), like any torch CUDA op; `synchronize=True` waits for the
+        result before returning. Host (numpy) calls always return finished
+        results.
+
+        deferred_checks: device-pointer int64 / interval calls return
         without a host round trip; domain-check failures surface at
         `synchronize()` (pe_exec.deferred_checks)."""
         self.domain = domain
         self.program = program
         self.device = device
         self.deferred_checks = bool(deferred_checks)
+        self.sync = bool(synchronize)
         if isinstance(domain, BigIntDomain) and not program.integer:
             raise ValueError("BigIntDomain needs integer coefficients")
 
-    def _exec(self, stream=None, sync=True, bounds=None) -> L.pe_exec:
+    def _exec(self, stream=None, sync=None, bounds=None) -> L.pe_exec:
         ex = L.pe_exec()
         ex.device = self.device
         ex.strict_f64 = 1 if isinstance(self.domain, DoubleDomain) and self.domain.strict else 0
         ex.stream = stream
-        ex.synchronize = 1 if sync else 0
+        ex.synchronize = 1 if (self.sync if sync is None else sync) else 0
         ex.i64_int_pipe = 1 if isinstance(self.domain, BigIntDomain) and self.domain.int_pipe else 0
         ex.deferred_checks = 1 if self.deferred_checks else 0
         if bounds is not None:

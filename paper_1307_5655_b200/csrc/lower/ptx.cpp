@@ -109,6 +109,80 @@ IvCoef inject(std::int64_t c) {
           std::nextafter(d, std::numeric_limits<double>::infinity())};
 }
 
+// A Hörner-shaped run acc = fma(acc, B, c_j), j = 1..L, with one multiplier
+// B and scalar coefficients is emitted as a counted loop over a constant
+// array instead of L straight-line FMAs. The arithmetic is the same FMA
+// sequence (bit-identical results); the kernel shrinks from ~16 B x L x P
+// of code to one cached loop body, which removes the instruction-fetch
+// bound of small batches (C1: 1e5 points, 26 us per straight-line launch,
+// profiles/r1_launches_c1.csv).
+struct ChainRun {
+  std::size_t head = 0, last = 0;  // ops head+1..last form the loop
+  Operand mult;
+};
+
+template <typename C>
+std::vector<ChainRun> chain_runs(const Stream<C>& s, Domain d, std::uint32_t sync_every,
+                                 std::uint64_t budget) {
+  std::vector<ChainRun> runs;
+  if (s.strict || sync_every != 0) return runs;
+  if (d != Domain::F64 && d != Domain::I64F && d != Domain::I64) return runs;
+  std::size_t min_run = 64;
+  if (const char* e = std::getenv("PE_LOOP")) min_run = static_cast<std::size_t>(std::atol(e));
+  if (min_run == 0) return runs;
+  // uses of the value each op defines (registers may be redefined)
+  const std::size_t n = s.ops.size();
+  std::vector<std::uint32_t> uses(n, 0);
+  std::unordered_map<std::uint32_t, std::size_t> last_def;
+  auto read = [&](const Operand& o) {
+    if (!o.is(Operand::Reg)) return;
+    auto it = last_def.find(o.id);
+    if (it != last_def.end()) ++uses[it->second];
+  };
+  for (std::size_t i = 0; i < n; ++i) {
+    read(s.ops[i].a);
+    read(s.ops[i].b);
+    read(s.ops[i].c);
+    last_def[s.ops[i].dst] = i;
+  }
+  read(s.result);
+  // op j continues the chain of op j-1: acc operand is the previous value
+  // (used once), same multiplier, scalar coefficient addend
+  auto same = [](const Operand& x, const Operand& y) { return x.kind == y.kind && x.id == y.id; };
+  auto link = [&](std::size_t j, Operand* mult) -> bool {
+    const Op& p = s.ops[j - 1];
+    const Op& o = s.ops[j];
+    if (o.kind != OpKind::Fma || !o.c.is(Operand::Coef) || uses[j - 1] != 1) return false;
+    Operand m;
+    if (o.a.is(Operand::Reg) && o.a.id == p.dst) {
+      m = o.b;
+    } else if (o.b.is(Operand::Reg) && o.b.id == p.dst) {
+      m = o.a;
+    } else {
+      return false;
+    }
+    if (!m.is(Operand::Pow) && !(m.is(Operand::Reg) && m.id != p.dst)) return false;
+    if (mult->kind != Operand::None && !same(*mult, m)) return false;
+    // the multiplier must not be redefined inside the run
+    if (m.is(Operand::Reg) && o.dst == m.id) return false;
+    *mult = m;
+    return true;
+  };
+  for (std::size_t i = 1; i < n;) {
+    Operand mult;
+    std::size_t j = i;
+    while (j < n && link(j, &mult)) ++j;
+    const std::size_t len = j - i;  // ops i..j-1 continue the chain of op i-1
+    const std::uint64_t words = len + 8;  // + prefetch padding
+    if (len >= min_run && words <= budget) {
+      runs.push_back({i - 1, j - 1, mult});
+      budget -= words;
+    }
+    i = len ? j : i + 1;
+  }
+  return runs;
+}
+
 template <typename C>
 class Emitter {
  public:
@@ -135,6 +209,8 @@ class Emitter {
     }
 
     assign_words();
+    find_chain_runs();
+    img.chain_loops = static_cast<std::uint32_t>(runs_.size());
     img.const_words = n_const_;
     img.param_words.assign(words_.begin() + n_const_, words_.begin() + n_const_ + n_param_);
     img.global_words.assign(words_.begin() + n_const_ + n_param_, words_.end());
@@ -198,7 +274,7 @@ class Emitter {
       }
       m << "};\n\n";
     }
-    m << main_entry << fix_entry;
+    m << run_arrays_ << main_entry << fix_entry;
     img.ptx = m.str();
     img.fp_ops = fp_ops_;
     img.int_ops = int_ops_;
@@ -214,6 +290,7 @@ class Emitter {
     decls_.str("");
     decls_.clear();
     n_creg_ = n_tf_ = n_tu_ = n_tp_ = 0;
+    loop_decls_ = false;
   }
 
   void finish_entry() {
@@ -533,7 +610,9 @@ class Emitter {
       decls_ << line.str();
     }
     std::uint64_t since_sync = 0;
-    for (const Op& op : s_.ops) {
+    std::size_t next_run = 0;
+    for (std::size_t i = 0; i < s_.ops.size(); ++i) {
+      const Op& op = s_.ops[i];
       if (sync_every_ && ++since_sync == sync_every_) {
         body_ << "  bar.sync 0;\n";
         since_sync = 0;
@@ -542,8 +621,87 @@ class Emitter {
         emit_iv_op(op);
       } else {
         emit_scalar_op(op);
+        if (next_run < runs_.size() && runs_[next_run].head == i) {
+          emit_chain_loop(runs_[next_run], next_run);
+          i = runs_[next_run].last;
+          ++next_run;
+        }
       }
     }
+  }
+
+  // ---------------- chain loops ----------------
+  // (see chain_runs above)
+  void find_chain_runs() {
+    const std::uint64_t budget =
+        n_const_ < CoefTiers::kConstCap ? CoefTiers::kConstCap - n_const_ : 0;
+    runs_ = chain_runs(s_, d_, sync_every_, budget);
+  }
+
+  // Loop body: U steps; coefficients arrive as warp-uniform constant-bank
+  // loads (LDCU) one iteration ahead of their use, so the load latency
+  // overlaps the previous iteration's FMA chain. The array is padded with U
+  // zero words so the last prefetch stays inside it. (Staging the words in
+  // shared memory instead measured slower: 0.70 vs 0.59 ms per 1e7 C1 points,
+  // per-thread LDS and +18 registers.)
+  void emit_chain_loop(const ChainRun& run, std::size_t idx) {
+    const std::uint32_t U = kLoopU;
+    const std::size_t L = run.last - run.head;
+    const std::string arr = "pe_run" + std::to_string(idx);
+    std::ostringstream a;
+    a << ".const .align 16 .b64 " << arr << "[" << L + U << "] = {";
+    for (std::size_t j = 0; j < L + U; ++j) {
+      if (j) a << (j % 8 == 0 ? ",\n  " : ", ");
+      a << (j < L ? hex64(words_[coef_lo_[s_.ops[run.head + 1 + j].c.id]]) : "0");
+    }
+    a << "};\n\n";
+    run_arrays_ += a.str();
+    if (!loop_decls_) {
+      decls_ << "  .reg .b64 %lp;\n  .reg .b32 %lc;\n  .reg .pred %lq;\n  .reg ." << ldty()
+             << " %lw<" << U << ">;\n  .reg ." << ldty() << " %lx<" << U << ">;\n";
+      loop_decls_ = true;
+    }
+    const std::uint32_t acc = s_.ops[run.head].dst;
+    const Loaded none;
+    auto step = [&](std::uint32_t u) {
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        const std::string r = reg(acc, k), m = opnd(run.mult, none, k);
+        if (d_ == Domain::I64) {
+          body_ << "  mad.lo.s64 " << r << ", " << r << ", " << m << ", %lw" << u << ";\n";
+        } else {
+          body_ << "  fma.rn.f64 " << r << ", " << r << ", " << m << ", %lw" << u << ";\n";
+        }
+      }
+    };
+    auto load8 = [&](const char* set, std::uint32_t off) {
+      for (std::uint32_t u = 0; u < U; u += 2) {
+        body_ << "  ld.const.v2." << ldty() << " {" << set << u << ", " << set << u + 1 << "}, [%lp+"
+              << off + 8 * u << "];\n";
+      }
+    };
+    const std::size_t iters = L / U, rem = L % U;
+    const std::string lbl = "$Lrun" + std::to_string(idx);
+    body_ << "  mov.u64 %lp, " << arr << ";\n";
+    load8("%lw", 0);
+    if (iters > 0) {
+      body_ << "  mov.u32 %lc, " << iters << ";\n" << lbl << ":\n";
+      load8("%lx", 8 * U);  // next iteration's words (padding after the last)
+      for (std::uint32_t u = 0; u < U; ++u) step(u);
+      for (std::uint32_t u = 0; u < U; ++u) {
+        body_ << "  mov.b64 %lw" << u << ", %lx" << u << ";\n";
+      }
+      body_ << "  add.u64 %lp, %lp, " << 8 * U << ";\n  sub.u32 %lc, %lc, 1;\n"
+            << "  setp.ne.u32 %lq, %lc, 0;\n  @%lq bra.uni " << lbl << ";\n";
+    }
+    for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in %lw
+    const std::uint32_t dst = s_.ops[run.last].dst;
+    if (dst != acc) {
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        body_ << "  mov." << (d_ == Domain::I64 ? "b64" : "f64") << " " << reg(dst, k) << ", "
+              << reg(acc, k) << ";\n";
+      }
+    }
+    (d_ == Domain::I64 ? int_ops_ : fp_ops_) += L;
   }
 
   void emit_scalar_op(const Op& op) {
@@ -953,6 +1111,10 @@ class Emitter {
     return e && std::string(e) == "hybrid";
   }();
   std::uint32_t nb_ = 0;
+  static constexpr std::uint32_t kLoopU = 8;  // loop unroll (steps per trip)
+  std::vector<ChainRun> runs_;
+  std::string run_arrays_;
+  bool loop_decls_ = false;
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;

@@ -49,6 +49,7 @@ struct KernelImage {
   std::uint32_t block = 128;
   std::uint32_t lanes = 1;         // points per thread (tile = block * lanes)
   bool interval_fast_path = false; // fast exact path + fixup entry (strict replay)
+  std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point

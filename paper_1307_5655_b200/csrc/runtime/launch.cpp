@@ -52,9 +52,11 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   for (auto& v : vals) args.push_back(&v);
   if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
   // Small batches: shrink the CTA (the kernel reads its tile size from
-  // %ntid; .maxntid is only an upper bound) until every SM has work.
+  // %ntid; .maxntid is only an upper bound) until every SM has work. Looped
+  // kernels (tiny code, no instruction-fetch sharing to lose) split finer,
+  // which evens out the per-SM load of a batch of a few CTAs per SM.
   std::uint64_t block = img.block;
-  const std::uint64_t want_ctas = 2 * static_cast<std::uint64_t>(sm_count(device));
+  const std::uint64_t want_ctas = (img.chain_loops ? 8 : 2) * static_cast<std::uint64_t>(sm_count(device));
   while (block > 64 && block % 64 == 0 && (la.n + block * img.lanes - 1) / (block * img.lanes) < want_ctas) {
     block /= 2;
   }

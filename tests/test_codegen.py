@@ -76,3 +76,42 @@ def test_coefficient_tiers_large_program(monkeypatch):
     ptx = prog.ptx(pe.DOMAIN_F64)
     assert "pe_pcoef" in ptx and "ld.global.nc.f64" in ptx
     assert prog.compile_only(pe.DOMAIN_F64) > 0
+
+
+def test_horner_chain_becomes_counted_loop(monkeypatch):
+    # C1: one 999-step fma(acc, x, c) chain -> a loop over a constant-bank
+    # array (same FMA sequence, so results are bit-identical; see
+    # test_gpu_edges)
+    wl = W.c1()
+    prog = pe.compile(wl.poly, wl.schemes)
+    ptx = prog.ptx(pe.DOMAIN_F64)
+    assert ptx.count("bra.uni $Lrun") == 1
+    assert ".const .align 16 .b64 pe_run0[1007]" in ptx  # 999 words + 8 padding
+    assert prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
+    assert prog.compile_only(pe.DOMAIN_F64) > 0
+    monkeypatch.setenv("PE_LOOP", "0")
+    prog2 = pe.compile(wl.poly, wl.schemes)
+    assert "$Lrun" not in prog2.ptx(pe.DOMAIN_F64)
+    assert prog2.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
+
+
+def test_chain_loops_int64_domains():
+    rng = np.random.default_rng(5)
+    d = 150
+    p = pe.Polynomial(np.arange(d, -1, -1).reshape(-1, 1),
+                      rng.integers(1, 9, d + 1).astype(np.int64))
+    prog = pe.compile(p, pe.builtin_scheme("horner"))
+    for dom in (pe.DOMAIN_I64, pe.DOMAIN_I64F):
+        ptx = prog.ptx(dom)
+        assert "$Lrun0:" in ptx
+        assert prog.compile_only(dom) > 0
+
+
+def test_sparse_horner_splits_runs_at_gaps():
+    # a gap changes the multiplier (x -> x^k): runs stop there
+    e = np.array([300, 299, 298] + list(range(200, -1, -1))).reshape(-1, 1)
+    c = np.linspace(0.5, 1.5, len(e))
+    prog = pe.compile(pe.Polynomial(e, c), pe.builtin_scheme("horner"))
+    ptx = prog.ptx(pe.DOMAIN_F64)
+    assert ptx.count("bra.uni $Lrun") == 1  # the 200-long dense tail
+    assert prog.compile_only(pe.DOMAIN_F64) > 0

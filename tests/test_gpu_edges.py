@@ -309,3 +309,50 @@ def test_program_shared_across_host_threads(cuda_device):
     assert not errors, errors
     for r in results.values():
         assert np.array_equal(r.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("n", [1, 31, 100_000, 100_003])
+def test_chain_loop_bit_identical_to_straight_line(n, cuda_device, monkeypatch):
+    # the looped Hörner chain issues the same FMA sequence as the straight-line
+    # kernel: results must agree bit for bit (and stay within TOL of the oracle)
+    wl = W.c1()
+    pts = wl.points(n)
+    looped = pe.compile(wl.poly, wl.schemes)
+    assert "$Lrun0" in looped.ptx(pe.DOMAIN_F64)
+    a = pe.Evaluator(pe.DoubleDomain(), looped).evaluate([_t(pts[0], cuda_device)]).cpu().numpy()
+    monkeypatch.setenv("PE_LOOP", "0")
+    flat = pe.compile(wl.poly, wl.schemes)
+    assert "$Lrun0" not in flat.ptx(pe.DOMAIN_F64)
+    b = pe.Evaluator(pe.DoubleDomain(), flat).evaluate([_t(pts[0], cuda_device)]).cpu().numpy()
+    assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    ref = pyoracle.Oracle(wl.poly, wl.schemes).eval_f64(pts)
+    assert np.all(np.abs(a - ref) <= 1e-12 * pyoracle.abs_term_sum(wl.poly, pts))
+
+
+def test_chain_loop_int64_exact(cuda_device):
+    rng = np.random.default_rng(5)
+    d = 150
+    p = pe.Polynomial(np.arange(d, -1, -1).reshape(-1, 1),
+                      rng.choice([-8, -3, -1, 1, 2, 7], d + 1).astype(np.int64))
+    schemes = [pe.builtin_scheme("horner")]
+    prog = pe.compile(p, schemes)
+    assert "$Lrun0" in prog.ptx(pe.DOMAIN_I64)
+    x = rng.integers(-1, 2, 20_011).astype(np.int64)
+    ref = pyoracle.Oracle(p, schemes).eval_i64([x])
+    for int_pipe in (False, True):  # exact-on-FP64 tier and int64 IMAD kernel
+        got = pe.Evaluator(pe.BigIntDomain(int_pipe=int_pipe), prog).evaluate(
+            [_t(x, cuda_device)]).cpu().numpy()
+        assert np.array_equal(got, ref)
+
+
+def test_sparse_horner_with_loop_tail(cuda_device):
+    e = np.array([300, 299, 298] + list(range(200, -1, -1))).reshape(-1, 1)
+    rng = np.random.default_rng(9)
+    c = rng.uniform(-1, 1, len(e))
+    schemes = [pe.builtin_scheme("horner")]
+    poly = pe.Polynomial(e, c)
+    prog = pe.compile(poly, schemes)
+    x = [rng.uniform(-1.1, 1.1, 5000)]
+    got = pe.Evaluator(pe.DoubleDomain(), prog).evaluate([_t(x[0], cuda_device)]).cpu().numpy()
+    ref = pyoracle.Oracle(poly, schemes).eval_f64(x)
+    assert np.all(np.abs(got - ref) <= 1e-12 * pyoracle.abs_term_sum(poly, x))
