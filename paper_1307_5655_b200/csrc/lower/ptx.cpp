@@ -256,7 +256,9 @@ class Emitter {
       body_ << "  add.u64 %rd1, %rd1, %rd2;\n  bra $Lfix;\n";
       finish_entry();
       fix_ = false;
-      fix_entry = entry_text(img, img.fix_entry, 128);  // launched with 128 threads
+      // launched with 128 threads, 4 CTAs per SM (<= 128 registers): the
+      // replay is latency-bound, so every listed point gets its own thread
+      fix_entry = entry_text(img, img.fix_entry, 128, 4);
       P_ = lanes;
       sync_every_ = sync;
     }
@@ -289,7 +291,7 @@ class Emitter {
     body_.clear();
     decls_.str("");
     decls_.clear();
-    n_creg_ = n_tf_ = n_tu_ = n_tp_ = 0;
+    n_creg_ = n_tf_ = n_tu_ = n_tp_ = n_tr_ = 0;
     loop_decls_ = false;
   }
 
@@ -299,12 +301,13 @@ class Emitter {
     if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
     if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
     if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+    if (n_tr_ > 0) decls_ << "  .reg .b32 %tr<" << n_tr_ << ">;\n";
   }
 
   // Both entries of a module take the same parameter list, so one argument
   // array launches either.
   std::string entry_text(const KernelImage& img, const std::string& name,
-                         std::uint32_t maxntid = 0) const {
+                         std::uint32_t maxntid = 0, std::uint32_t min_ctas = 0) const {
     if (maxntid == 0) maxntid = img.block;
     std::ostringstream m;
     m << ".visible .entry " << name << "(";
@@ -327,7 +330,9 @@ class Emitter {
       param(".param .u64 pe_cap");
     }
     if (n_param_ > 0) param(".param .align 8 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
-    m << ")\n.maxntid " << maxntid << ", 1, 1\n{\n";
+    m << ")\n.maxntid " << maxntid << ", 1, 1\n";
+    if (min_ctas) m << ".minnctapersm " << min_ctas << "\n";
+    m << "{\n";
     m << "  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n";
     m << decls_.str() << body_.str() << "}\n\n";
     return m.str();
@@ -555,6 +560,7 @@ class Emitter {
         }
       }
     }
+    psign_.assign(np, 0);
     for (std::size_t i = 0; i < np; ++i) {
       const Power& p = s_.powers[i];
       const auto id = static_cast<std::uint32_t>(i);
@@ -574,9 +580,12 @@ class Emitter {
           continue;
         }
         if (d_ == Domain::Interval && fast_) {
+          // a product of non-straddling intervals cannot straddle (a zero
+          // endpoint is caught by the nextafter "no move" test), so only the
+          // coordinates need the straddle check; signs are tracked statically
           fast_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
-                   {pw(p.hi, k, false), pw(p.hi, k, true)}, false, false);
-          fcheck_straddle({pw(id, k, false), pw(id, k, true)});
+                   {pw(p.hi, k, false), pw(p.hi, k, true)}, false, false, psign_[p.lo],
+                   psign_[p.hi]);
           fcheck_finite(pw(id, k, false));
           fcheck_finite(pw(id, k, true));
         } else if (d_ == Domain::Interval) {
@@ -589,6 +598,10 @@ class Emitter {
           body_ << "  mul.rn.f64 " << pw(id, k) << ", " << pw(p.lo, k) << ", " << pw(p.hi, k) << ";\n";
           if (k == 0) ++fp_ops_;
         }
+      }
+      // static sign: squares are positive, products of known signs known
+      if (p.exponent > 1 && static_signs_) {
+        psign_[i] = p.lo == p.hi ? 1 : psign_[p.lo] * psign_[p.hi];
       }
     }
   }
@@ -750,6 +763,7 @@ class Emitter {
   std::string tmp_f() { return "%tf" + std::to_string(n_tf_++); }
   std::string tmp_u() { return "%tu" + std::to_string(n_tu_++); }
   std::string tmp_p() { return "%tp" + std::to_string(n_tp_++); }
+  std::string tmp_r() { return "%tr" + std::to_string(n_tr_++); }
 
   // dst = nextafter(src, +inf) (up) or nextafter(src, -inf) (down), exactly as
   // std::nextafter: +-0 -> +-denorm_min, NaN kept, +inf kept (up) / -inf kept
@@ -854,9 +868,22 @@ class Emitter {
       const std::string a = tmp_f();
       body_ << "  abs.f64 " << a << ", " << src << ";\n";
       if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
-      body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n"
-            << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << dst << ", " << src << ", %pb" << (nb_ & 3)
-            << ";\n";
+      body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
+      // "Did not move" test: either an FP64 compare, or (same answer) a
+      // 32-bit integer compare of the low words on the ALU pipe — a step of
+      // one ulp changes the bit pattern by +-1, so the low words differ iff
+      // the value moved. Mixing the two balances the FP64 and ALU pipes.
+      const bool int_check = iv_check_ == 1 || (iv_check_ == 2 && (nb_ & 1));
+      if (int_check) {
+        const std::string l0 = tmp_r(), h0 = tmp_r(), l1 = tmp_r(), h1 = tmp_r();
+        body_ << "  mov.b64 {" << l0 << ", " << h0 << "}, " << dst << ";\n"
+              << "  mov.b64 {" << l1 << ", " << h1 << "}, " << src << ";\n"
+              << "  setp.eq.or.b32 %pb" << (nb_ & 3) << ", " << l0 << ", " << l1 << ", %pb"
+              << (nb_ & 3) << ";\n";
+      } else {
+        body_ << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << dst << ", " << src << ", %pb"
+              << (nb_ & 3) << ";\n";
+      }
       ++nb_;
       return;
     }
@@ -870,19 +897,39 @@ class Emitter {
           << "  mov.b64 " << dst << ", " << r << ";\n";
   }
 
+  // nextafter of a value whose sign is known statically (sign != 0): the
+  // neighbour is the bit pattern +-1 (magnitude up for the outward step of
+  // that sign, down for the inward one) — two 32-bit ALU adds, no check. It
+  // is std::nextafter for every finite value of that sign including
+  // subnormals; the cases where it is not (+0 down, -0 up, +-inf outward)
+  // give NaN, and NaN/inf never turn finite again on the fast path, so the
+  // final finiteness test sends such points to the strict replay. Unknown
+  // sign: the FP64-pipe step with its "no move" test (fnext).
+  void snext(const std::string& dst, const std::string& src, bool up, int sign) {
+    if (sign == 0 || !int_known_) {
+      fnext(dst, src, up);
+      return;
+    }
+    const std::string u = tmp_u(), r = tmp_u();
+    body_ << "  mov.b64 " << u << ", " << src << ";\n"
+          << ((up == (sign > 0)) ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", 1;\n"
+          << "  mov.b64 " << dst << ", " << r << ";\n";
+  }
+
+  // sign: statically known sign of the sum (0 = unknown)
   void fast_add(const std::string& dlo, const std::string& dhi,
                 const std::pair<std::string, std::string>& a,
-                const std::pair<std::string, std::string>& b, bool a_is_zero) {
+                const std::pair<std::string, std::string>& b, bool a_is_zero, int sign = 0) {
     if (a_is_zero) {
-      fnext(dlo, b.first, false);
-      fnext(dhi, b.second, true);
+      snext(dlo, b.first, false, sign);
+      snext(dhi, b.second, true, sign);
       return;
     }
     const std::string lo = tmp_f(), hi = tmp_f();
     body_ << "  add.rn.f64 " << lo << ", " << a.first << ", " << b.first << ";\n"
           << "  add.rn.f64 " << hi << ", " << a.second << ", " << b.second << ";\n";
-    fnext(dlo, lo, false);
-    fnext(dhi, hi, true);
+    snext(dlo, lo, false, sign);
+    snext(dhi, hi, true, sign);
   }
 
   // accumulator |= (lo ^ hi): sign bit set iff the interval straddles zero
@@ -903,27 +950,47 @@ class Emitter {
           << ";\n  or.b64 %facc, %facc, " << x << ";\n";
   }
 
+  // sa / sb: statically known sign of an operand (+1 / -1; 0 = decided at
+  // run time from its upper endpoint). A known sign fixes which endpoints
+  // pair up, so the corresponding selects (2 FSEL each) disappear.
   void fast_mul(const std::string& dlo, const std::string& dhi,
                 const std::pair<std::string, std::string>& a,
-                const std::pair<std::string, std::string>& b, bool check_a, bool check_b) {
-    if (check_a) fcheck_straddle(a);
-    if (check_b) fcheck_straddle(b);
-    const std::string ah = tmp_u(), bh = tmp_u();
+                const std::pair<std::string, std::string>& b, bool check_a, bool check_b,
+                int sa = 0, int sb = 0) {
+    if (!fma_next_ || hybrid_next_) sa = sb = 0;  // integer steps need the runtime sign
+    if (check_a && sa == 0) fcheck_straddle(a);
+    if (check_b && sb == 0) fcheck_straddle(b);
     const std::string an = tmp_p(), bn = tmp_p(), ng = tmp_p();
-    body_ << "  mov.b64 " << ah << ", " << a.second << ";\n  mov.b64 " << bh << ", " << b.second
-          << ";\n  setp.lt.s64 " << an << ", " << ah << ", 0;\n  setp.lt.s64 " << bn << ", " << bh
-          << ", 0;\n  xor.pred " << ng << ", " << an << ", " << bn << ";\n";
-    const std::string A1 = tmp_f(), B1 = tmp_f(), A2 = tmp_f(), B2 = tmp_f();
-    body_ << "  selp.f64 " << A1 << ", " << a.second << ", " << a.first << ", " << bn << ";\n"
-          << "  selp.f64 " << A2 << ", " << a.first << ", " << a.second << ", " << bn << ";\n"
-          << "  selp.f64 " << B1 << ", " << b.second << ", " << b.first << ", " << an << ";\n"
-          << "  selp.f64 " << B2 << ", " << b.first << ", " << b.second << ", " << an << ";\n";
+    if (sa == 0) {
+      const std::string ah = tmp_u();
+      body_ << "  mov.b64 " << ah << ", " << a.second << ";\n  setp.lt.s64 " << an << ", " << ah
+            << ", 0;\n";
+    }
+    if (sb == 0) {
+      const std::string bh = tmp_u();
+      body_ << "  mov.b64 " << bh << ", " << b.second << ";\n  setp.lt.s64 " << bn << ", " << bh
+            << ", 0;\n";
+    }
+    if (sa == 0 && sb == 0) body_ << "  xor.pred " << ng << ", " << an << ", " << bn << ";\n";
+    // pick(x_if_neg, x_if_pos, sign, pred)
+    auto pick = [&](const std::string& if_neg, const std::string& if_pos, int sign,
+                    const std::string& pred) {
+      if (sign > 0) return if_pos;
+      if (sign < 0) return if_neg;
+      const std::string r = tmp_f();
+      body_ << "  selp.f64 " << r << ", " << if_neg << ", " << if_pos << ", " << pred << ";\n";
+      return r;
+    };
+    const std::string A1 = pick(a.second, a.first, sb, bn);
+    const std::string A2 = pick(a.first, a.second, sb, bn);
+    const std::string B1 = pick(b.second, b.first, sa, an);
+    const std::string B2 = pick(b.first, b.second, sa, an);
     const std::string lo = tmp_f(), hi = tmp_f();
     body_ << "  mul.rn.f64 " << lo << ", " << A1 << ", " << B1 << ";\n"
           << "  mul.rn.f64 " << hi << ", " << A2 << ", " << B2 << ";\n";
     if (fma_next_ && !hybrid_next_) {
-      fnext(dlo, lo, false);
-      fnext(dhi, hi, true);
+      snext(dlo, lo, false, sa * sb);
+      snext(dhi, hi, true, sa * sb);
       return;
     }
     if (fma_next_ && hybrid_next_) {
@@ -954,14 +1021,31 @@ class Emitter {
           << "  mov.b64 " << dlo << ", " << rl << ";\n  mov.b64 " << dhi << ", " << rh << ";\n";
   }
 
+  // Static sign of an operand in the fast path: +1 / -1 when every
+  // unflagged evaluation has that sign on both endpoints, 0 when unknown.
+  // Coefficients are nonzero non-straddling (host-checked); squares are
+  // positive; products and same-sign sums keep known signs (a zero endpoint
+  // is caught by the nextafter "no move" test, so "known" never hides one).
+  int sgn(const Operand& o) const {
+    switch (o.kind) {
+      case Operand::Coef: return inject(s_.coefs[o.id]).lo > 0 ? 1 : -1;
+      case Operand::Reg: return o.id < rsign_.size() ? rsign_[o.id] : 0;
+      case Operand::Pow: return psign_[o.id];
+      default: return 0;
+    }
+  }
+
   void emit_iv_op(const Op& op) {
     const Loaded la = load(op.a), lb = load(op.b);
+    const int sa = fast_ ? sgn(op.a) : 0, sb = fast_ ? sgn(op.b) : 0;
     for (std::uint32_t k = 0; k < P_; ++k) {
       const std::string dlo = reg(op.dst, k, false), dhi = reg(op.dst, k, true);
       switch (op.kind) {
         case OpKind::Add:
           if (fast_) {
-            fast_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero));
+            const int sum_sign = op.a.is(Operand::Zero) ? sb : (sa == sb ? sa : 0);
+            fast_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero),
+                     sum_sign);
           } else {
             iv_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero), k == 0);
           }
@@ -970,7 +1054,7 @@ class Emitter {
           if (fast_) {
             // coefficients are host-checked, powers checked where computed
             fast_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Reg),
-                     op.b.is(Operand::Reg));
+                     op.b.is(Operand::Reg), sa, sb);
           } else {
             iv_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), k == 0);
           }
@@ -978,6 +1062,18 @@ class Emitter {
         case OpKind::Fma:
           throw std::logic_error("interval streams are strict (no FMA)");
       }
+    }
+    if (fast_) {
+      if (rsign_.size() <= op.dst) rsign_.resize(op.dst + 1, 0);
+      int r = 0;
+      if (op.kind == OpKind::Mul) {
+        r = sa * sb;
+      } else if (op.a.is(Operand::Zero)) {
+        r = sb;
+      } else if (sa == sb) {
+        r = sa;
+      }
+      rsign_[op.dst] = static_signs_ ? r : 0;
     }
   }
 
@@ -1111,6 +1207,25 @@ class Emitter {
     return e && std::string(e) == "hybrid";
   }();
   std::uint32_t nb_ = 0;
+  std::vector<int> rsign_, psign_;  // fast path: static signs of registers / powers
+  bool static_signs_ = [] {         // PE_IV_SIGNS=0 disables (A/B measurement)
+    const char* e = std::getenv("PE_IV_SIGNS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  bool int_known_ = [] {            // integer nextafter for known signs (PE_IV_INTSTEP=0 off)
+    const char* e = std::getenv("PE_IV_INTSTEP");
+    return !(e && std::atoi(e) == 0);
+  }();
+  // fast-path "no move" test: 0 FP64 compare, 1 integer low-word compare
+  // (default), 2 alternate (PE_IV_CHECK=fp|int|mix). With static signs, C5
+  // per 1e7 intervals: fp 1.88 ms, mix 1.69, int 1.56
+  // (profiles/r1_c5_check_modes.txt)
+  int iv_check_ = [] {
+    const char* e = std::getenv("PE_IV_CHECK");
+    if (e && std::string(e) == "mix") return 2;
+    if (e && std::string(e) == "fp") return 0;
+    return 1;
+  }();
   static constexpr std::uint32_t kLoopU = 8;  // loop unroll (steps per trip)
   std::vector<ChainRun> runs_;
   std::string run_arrays_;
@@ -1118,7 +1233,7 @@ class Emitter {
   std::vector<std::uint64_t> words_;
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
-  std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0;
+  std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0, n_tr_ = 0;
   std::uint64_t fp_ops_ = 0, int_ops_ = 0;
   std::ostringstream body_, decls_;
 };

@@ -72,7 +72,7 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     // strict replay of the points the fast path could not prove; it reads
     // the list length on the device, so no host round trip in between
     const unsigned fix_grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(2 * static_cast<std::uint64_t>(sm_count(device)),
+        std::min<std::uint64_t>(4 * static_cast<std::uint64_t>(sm_count(device)),
                                 (la.cap + 127) / 128));
     check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.fix_kernel), dim3(fix_grid ? fix_grid : 1),
                                 dim3(128), args.data(), 0, stream),

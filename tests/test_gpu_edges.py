@@ -356,3 +356,37 @@ def test_sparse_horner_with_loop_tail(cuda_device):
     got = pe.Evaluator(pe.DoubleDomain(), prog).evaluate([_t(x[0], cuda_device)]).cpu().numpy()
     ref = pyoracle.Oracle(poly, schemes).eval_f64(x)
     assert np.all(np.abs(got - ref) <= 1e-12 * pyoracle.abs_term_sum(poly, x))
+
+
+@pytest.mark.parametrize("scheme", ["horner", "estrin", "balanced", "direct"])
+def test_interval_fast_path_extreme_magnitudes(scheme, cuda_device):
+    # The fast interval path tracks operand signs statically (coefficients,
+    # even powers, same-sign sums) and steps known-sign endpoints on the
+    # integer pipe; coefficients from 1e-300 to 1e300 and points from
+    # subnormal to 1e150 drive products through underflow to 0 / subnormals
+    # and overflow to inf, where those shortcuts must hand over to the strict
+    # replay. Bit-exact against the oracle.
+    rng = np.random.default_rng(21)
+    exps = np.array([[a, b] for a in range(0, 9) for b in range(0, 9 - a)
+                     if rng.random() < 0.7], dtype=np.uint32)
+    mags = 10.0 ** rng.uniform(-300, 300, len(exps))
+    coefs = mags * rng.choice([-1.0, 1.0], len(exps))
+    poly = pe.Polynomial(exps, coefs, ("x", "y"))
+    schemes = [pe.builtin_scheme(scheme)] * 2
+    prog = pe.compile(poly, schemes)
+    n = 20_000
+    cols_lo, cols_hi = [], []
+    for _ in range(2):
+        centre = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-320, 150, n)
+        width = np.abs(centre) * 10.0 ** rng.uniform(-17, 0, n)
+        lo, hi = centre, centre + width
+        straddle = rng.random(n) < 0.05
+        lo = np.where(straddle, -np.abs(hi), lo)
+        cols_lo.append(np.minimum(lo, hi))
+        cols_hi.append(np.maximum(lo, hi))
+    glo, ghi = pe.Evaluator(pe.IntervalDomain(), prog).evaluate(
+        ([_t(c, cuda_device) for c in cols_lo], [_t(c, cuda_device) for c in cols_hi]))
+    olo, ohi = pyoracle.Oracle(poly, schemes).eval_interval(cols_lo, cols_hi)
+    glo, ghi = glo.cpu().numpy(), ghi.cpu().numpy()
+    assert np.array_equal(glo.view(np.int64), olo.view(np.int64))
+    assert np.array_equal(ghi.view(np.int64), ohi.view(np.int64))
