@@ -10,6 +10,8 @@
  *                          + compile()            tree.hpp:58-77, eval.hpp:57
  *                          (polynomial from raw terms: Polynomial::canonicalize,
  *                          polynomial.hpp:34-36; schemes: scheme.hpp:15-57)
+ *   pe_program_from_compiled  an existing CompiledProgram (compile() output,
+ *                          eval.hpp:32-57), flattened; same evaluation semantics
  *   pe_program_destroy     CompiledProgram lifetime (move-only, eval.hpp:32-54)
  *   pe_eval_f64            Evaluator<DoubleDomain>(domain, program) +
  *                          evaluate(point) per point   eval.hpp:74-90, ring.hpp:40-48
@@ -104,6 +106,15 @@ typedef struct pe_exec {
    * not attempted in this mode (re-run synchronously to get it). */
   int32_t deferred_checks;
   int32_t reserved;
+  /* Host-buffer calls: shard the batch over devices[0..ndevices) — contiguous
+   * slices of ceil(n / ndevices) points, one staged pipeline per device,
+   * running concurrently; every device writes its slice of the results
+   * straight into the caller's host output (the gather). The program is
+   * replicated to each device on first use. NULL / 0 = exec->device only.
+   * Device-buffer calls reject ndevices > 1 (their data lives on one device). */
+  const int32_t* devices;
+  int32_t ndevices;
+  int32_t reserved2;
 } pe_exec;
 
 /* Compiles a polynomial given as raw terms: `exponents` is nterms x nvars
@@ -114,6 +125,48 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs,
                             size_t nterms, uint32_t nvars,
                             const pe_scheme_desc* schemes,
                             pe_coeff_type coeff_type, pe_program** out);
+
+/* One record of a flattened reference CompiledProgram (eval.hpp:32-41:
+ * CompiledProgram::Record). Exactly one of the coefficient fields is read,
+ * per the coeff_type of pe_program_from_compiled; it is ignored when `sub`
+ * names a nested program (the record's coefficient is that program). */
+typedef struct pe_record {
+  double coeff_f64;
+  int64_t coeff_i64;
+  int32_t sub;            /* index of the nested program in `programs`, or -1 */
+  int32_t power_slot;     /* index into exponent_sets[variable], or -1 (absent) */
+  uint32_t lazy_slot;
+  int32_t parent_slot;    /* -1 only for the last (root) record */
+  int32_t reads_register; /* 0 / 1 */
+  int32_t reserved;       /* 0 */
+} pe_record;
+
+/* One (root or nested) program: CompiledProgram::{records, register_count,
+ * variable, root_child_ends} (eval.hpp:43-51). */
+typedef struct pe_compiled_program {
+  const pe_record* records;
+  size_t nrecords;
+  uint32_t register_count;
+  uint32_t variable;
+  const uint32_t* root_child_ends;
+  size_t nroot_child_ends;
+} pe_compiled_program;
+
+/* Lowers an already compiled program — the reference's
+ * CompiledProgram compile(const EvaluationTree&) output (eval.hpp:57),
+ * flattened: programs[0] is the root, nested programs are referenced from
+ * records by index, each exactly once. exponent_sets[v] (sorted, distinct,
+ * >= 1; exponent_set_sizes[v] entries) are the root's per-variable sets
+ * (eval.hpp:53-54). Evaluation follows the given records verbatim: strict
+ * fp64 and intervals replay their op sequence bit for bit. Malformed programs
+ * (slot out of range, a record whose parent register is never read, a nested
+ * program referenced twice, ...) are rejected with PE_EINVAL. Such a program
+ * has no tree: pe_program_dot returns PE_EINVAL, and wide fp64 programs are
+ * not sliced. */
+pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t nprograms,
+                                   uint32_t nvars, const uint32_t* const* exponent_sets,
+                                   const size_t* exponent_set_sizes, pe_coeff_type coeff_type,
+                                   pe_program** out);
 
 void pe_program_destroy(pe_program* program);
 

@@ -89,6 +89,9 @@ def ref_lib():
         lib.ref_eval_i64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int]
         lib.ref_eval_parallel_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                               C.c_uint]
+        lib.ref_export.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                   C.POINTER(C.c_size_t)]
         lib.ref_last_error.restype = C.c_char_p
         _ref = lib
     return _ref
@@ -175,6 +178,7 @@ class Reference:
     def __init__(self, poly, schemes):
         lib = ref_lib()
         self.integer = poly.coefficients.dtype == np.int64
+        self.nvars = poly.nvars
         up, lo, cut = _scheme_arrays(schemes)
         h = C.c_void_p()
         self._keep = (poly.exponents, poly.coefficients)
@@ -196,6 +200,45 @@ class Reference:
             if "int64" in msg:
                 raise OverflowError(msg)
             raise ValueError(msg)
+
+    def export(self):
+        """The reference's own CompiledProgram, flattened (root first, nested
+        programs pre-order) in the shape CompiledProgram.from_compiled takes,
+        plus the per-variable exponent sets."""
+        lib = ref_lib()
+        nr, npg, ne = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._check(lib.ref_export(self._h, None, None, None, None, None, C.byref(nr),
+                                   C.byref(npg), C.byref(ne)))
+        f64 = np.zeros(nr.value, np.float64)
+        i64 = np.zeros(nr.value, np.int64)
+        ints = np.zeros((nr.value, 5), np.int32)
+        info = np.zeros((npg.value, 6), np.uint32)
+        ends = np.zeros(max(1, ne.value), np.uint32)
+        self._check(lib.ref_export(self._h, f64.ctypes.data, i64.ctypes.data, ints.ctypes.data,
+                                   info.ctypes.data, ends.ctypes.data, C.byref(nr), C.byref(npg),
+                                   C.byref(ne)))
+        programs = []
+        for first, n, regs, var, e0, ne_k in info.tolist():
+            recs = []
+            for i in range(first, first + n):
+                sub, ps, lazy, parent, reads = ints[i].tolist()
+                recs.append({"coeff": int(i64[i]) if self.integer else float(f64[i]), "sub": sub,
+                             "power_slot": ps, "lazy_slot": lazy, "parent_slot": parent,
+                             "reads_register": bool(reads)})
+            programs.append({"records": recs, "register_count": regs, "variable": var,
+                             "root_child_ends": ends[e0:e0 + ne_k].tolist()})
+        sets = [self.exponents(v) for v in range(self.nvars)]
+        return programs, sets
+
+    def exponents(self, v):
+        lib = ref_lib()
+        n = C.c_size_t()
+        buf = (C.c_uint32 * 4096)()
+        self._check(lib.ref_exponents(self._h, v, buf, 4096, C.byref(n)))
+        if n.value > 4096:
+            buf = (C.c_uint32 * n.value)()
+            self._check(lib.ref_exponents(self._h, v, buf, n.value, C.byref(n)))
+        return list(buf[:n.value])
 
     def eval_f64(self, coords, threads=1):
         cols = [np.ascontiguousarray(c, dtype=np.float64) for c in coords]

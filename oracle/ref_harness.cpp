@@ -198,6 +198,59 @@ int ref_records(void* h, std::int32_t* out, std::size_t cap, std::size_t* count,
   });
 }
 
+// Flattens the reference CompiledProgram (root + nested, pre-order) for
+// pe_program_from_compiled: per record (coeff as fp64 — exact, k * 2^-S — and
+// as int64 for integer programs; sub program index | -1, power_slot | -1,
+// lazy_slot, parent_slot | -1, reads_register), per program (first record,
+// record count, register_count, variable, first root_child_end, count).
+// Call once with null buffers for the sizes.
+int ref_export(void* h, double* rec_f64, std::int64_t* rec_i64, std::int32_t* rec_int,
+               std::uint32_t* prog_info, std::uint32_t* ends, std::size_t* nrec,
+               std::size_t* nprog, std::size_t* nends) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    std::size_t r = 0, pcount = 0, e = 0;
+    auto visit = [&](auto&& self, const CompiledProgram& p) -> std::size_t {
+      const std::size_t me = pcount++;
+      const std::size_t first = r;
+      r += p.records.size();
+      const std::size_t first_end = e;
+      e += p.root_child_ends.size();
+      if (prog_info) {
+        std::uint32_t* pi = prog_info + 6 * me;
+        pi[0] = static_cast<std::uint32_t>(first);
+        pi[1] = static_cast<std::uint32_t>(p.records.size());
+        pi[2] = p.register_count;
+        pi[3] = static_cast<std::uint32_t>(p.variable);
+        pi[4] = static_cast<std::uint32_t>(first_end);
+        pi[5] = static_cast<std::uint32_t>(p.root_child_ends.size());
+        for (std::size_t k = 0; k < p.root_child_ends.size(); ++k) ends[first_end + k] = p.root_child_ends[k];
+      }
+      for (std::size_t i = 0; i < p.records.size(); ++i) {
+        const auto& rec = p.records[i];
+        std::int32_t sub = -1;
+        if (rec.sub) sub = static_cast<std::int32_t>(self(self, *rec.sub));
+        if (rec_int) {
+          std::int32_t* ri = rec_int + 5 * (first + i);
+          ri[0] = sub;
+          ri[1] = rec.power_slot ? static_cast<std::int32_t>(*rec.power_slot) : -1;
+          ri[2] = static_cast<std::int32_t>(rec.lazy_slot);
+          ri[3] = rec.parent_slot ? static_cast<std::int32_t>(*rec.parent_slot) : -1;
+          ri[4] = rec.reads_register ? 1 : 0;
+          rec_f64[first + i] = rec.sub ? 0.0 : std::ldexp(rec.coeff.to_double(), -rp.shift);
+          rec_i64[first + i] = rec.sub || !rp.integer ? 0 : std::stoll(rec.coeff.to_decimal());
+        }
+      }
+      return me;
+    };
+    visit(visit, *rp.program);
+    *nrec = r;
+    *nprog = pcount;
+    *nends = e;
+    return 0;
+  });
+}
+
 int ref_exponents(void* h, std::uint32_t v, std::uint32_t* out, std::size_t cap, std::size_t* count) {
   return guarded([&] {
     const CompiledProgram& p = *static_cast<RefProgram*>(h)->program;

@@ -33,6 +33,33 @@ class pe_exec(C.Structure):
         ("i64_bounds", C.POINTER(C.c_uint64)),
         ("deferred_checks", C.c_int32),
         ("reserved", C.c_int32),
+        ("devices", C.POINTER(C.c_int32)),
+        ("ndevices", C.c_int32),
+        ("reserved2", C.c_int32),
+    ]
+
+
+class pe_record(C.Structure):
+    _fields_ = [
+        ("coeff_f64", C.c_double),
+        ("coeff_i64", C.c_int64),
+        ("sub", C.c_int32),
+        ("power_slot", C.c_int32),
+        ("lazy_slot", C.c_uint32),
+        ("parent_slot", C.c_int32),
+        ("reads_register", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class pe_compiled_program(C.Structure):
+    _fields_ = [
+        ("records", C.POINTER(pe_record)),
+        ("nrecords", C.c_size_t),
+        ("register_count", C.c_uint32),
+        ("variable", C.c_uint32),
+        ("root_child_ends", C.POINTER(C.c_uint32)),
+        ("nroot_child_ends", C.c_size_t),
     ]
 
 
@@ -57,6 +84,10 @@ EXPORTS = [
     ("pe_program_create", C.c_int,
      [C.POINTER(C.c_uint32), C.c_void_p, C.c_size_t, C.c_uint32,
       C.POINTER(pe_scheme_desc), C.c_int, C.POINTER(C.c_void_p)]),
+    ("pe_program_from_compiled", C.c_int,
+     [C.POINTER(pe_compiled_program), C.c_size_t, C.c_uint32,
+      C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_size_t), C.c_int,
+      C.POINTER(C.c_void_p)]),
     ("pe_program_destroy", None, [C.c_void_p]),
     ("pe_program_info", C.c_int, [C.c_void_p, C.POINTER(pe_program_info_t)]),
     ("pe_program_exponents", C.c_int,

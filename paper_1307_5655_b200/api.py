@@ -142,6 +142,7 @@ class CompiledProgram:
             raise ValueError("need exactly one scheme per variable")
         self.poly = poly
         self.schemes = tuple(schemes)
+        self._nvars = poly.nvars
         self.integer = poly.coefficients.dtype == np.int64
         descs = (L.pe_scheme_desc * poly.nvars)(*[s.desc() for s in schemes])
         h = C.c_void_p()
@@ -167,7 +168,55 @@ class CompiledProgram:
 
     @property
     def nvars(self) -> int:
-        return self.poly.nvars
+        return self._nvars
+
+    @classmethod
+    def from_compiled(cls, programs, exponent_sets, integer: bool = False) -> "CompiledProgram":
+        """Lowers an already compiled program (pe_program_from_compiled).
+
+        programs: list of dicts, [0] the root, each {"records": [dict(coeff,
+        sub, power_slot, lazy_slot, parent_slot, reads_register)],
+        "register_count", "variable", "root_child_ends"}; `sub` / `power_slot`
+        / `parent_slot` are -1 when absent (reference CompiledProgram,
+        eval.hpp:32-54). exponent_sets: one ascending list per variable."""
+        nvars = len(exponent_sets)
+        keep = []
+        progs = (L.pe_compiled_program * len(programs))()
+        for k, pr in enumerate(programs):
+            recs = (L.pe_record * len(pr["records"]))()
+            for i, r in enumerate(pr["records"]):
+                if integer:
+                    recs[i].coeff_i64 = int(r.get("coeff", 0))
+                else:
+                    recs[i].coeff_f64 = float(r.get("coeff", 0.0))
+                recs[i].sub = int(r.get("sub", -1))
+                recs[i].power_slot = int(r.get("power_slot", -1))
+                recs[i].lazy_slot = int(r["lazy_slot"])
+                recs[i].parent_slot = int(r.get("parent_slot", -1))
+                recs[i].reads_register = 1 if r.get("reads_register") else 0
+            ends = (C.c_uint32 * max(1, len(pr.get("root_child_ends", []))))(
+                *pr.get("root_child_ends", []))
+            keep += [recs, ends]
+            progs[k].records = recs
+            progs[k].nrecords = len(pr["records"])
+            progs[k].register_count = int(pr["register_count"])
+            progs[k].variable = int(pr.get("variable", 0))
+            progs[k].root_child_ends = ends
+            progs[k].nroot_child_ends = len(pr.get("root_child_ends", []))
+        sets = [(C.c_uint32 * max(1, len(e)))(*e) for e in exponent_sets]
+        set_ptrs = (C.POINTER(C.c_uint32) * nvars)(*[C.cast(a, C.POINTER(C.c_uint32)) for a in sets])
+        sizes = (C.c_size_t * nvars)(*[len(e) for e in exponent_sets])
+        h = C.c_void_p()
+        L.check(L.lib().pe_program_from_compiled(progs, len(programs), nvars, set_ptrs, sizes,
+                                                 L.COEFF_I64 if integer else L.COEFF_F64,
+                                                 C.byref(h)))
+        self = cls.__new__(cls)
+        self.poly = None
+        self.schemes = ()
+        self._nvars = nvars
+        self.integer = bool(integer)
+        self._h = h
+        return self
 
     def info(self) -> dict:
         inf = L.pe_program_info_t()
@@ -274,7 +323,8 @@ class Evaluator:
     """Batch evaluation session (reference Evaluator<D>, eval.hpp:69-90)."""
 
     def __init__(self, domain, program: CompiledProgram, device: int = -1,
-                 deferred_checks: bool = False, synchronize: bool = False):
+                 deferred_checks: bool = False, synchronize: bool = False,
+                 devices: Sequence[int] | None = None):
         """CUDA-tensor calls are asynchronous on the stream they are enqueued
         on (torch's current stream of the data's device unless `stream=` is
         given), like any torch CUDA op; `synchronize=True` waits for the
@@ -283,12 +333,18 @@ class Evaluator:
 
         deferred_checks: device-pointer int64 / interval calls return
         without a host round trip; domain-check failures surface at
-        `synchronize()` (pe_exec.deferred_checks)."""
+        `synchronize()` (pe_exec.deferred_checks).
+
+        devices: host (numpy) batches are split into contiguous slices, one
+        per listed GPU, evaluated concurrently and written straight into the
+        host result (pe_exec.devices)."""
         self.domain = domain
         self.program = program
         self.device = device
         self.deferred_checks = bool(deferred_checks)
         self.sync = bool(synchronize)
+        self.devices = [int(d) for d in devices] if devices else []
+        self._dev_arr = (C.c_int32 * max(1, len(self.devices)))(*self.devices)
         if isinstance(domain, BigIntDomain) and not program.integer:
             raise ValueError("BigIntDomain needs integer coefficients")
 
@@ -300,6 +356,9 @@ class Evaluator:
         ex.synchronize = 1 if (self.sync if sync is None else sync) else 0
         ex.i64_int_pipe = 1 if isinstance(self.domain, BigIntDomain) and self.domain.int_pipe else 0
         ex.deferred_checks = 1 if self.deferred_checks else 0
+        if self.devices:
+            ex.devices = C.cast(self._dev_arr, C.POINTER(C.c_int32))
+            ex.ndevices = len(self.devices)
         if bounds is not None:
             arr = (C.c_uint64 * len(bounds))(*[int(b) for b in bounds])
             ex.i64_bounds = arr
@@ -388,10 +447,10 @@ class Evaluator:
         return np.empty(n, dtype=np.int64 if kind == "i64" else np.float64)
 
 
-def evaluate_many(programs, points, outs=None, device: int = -1, stream=None):
+def evaluate_many(programs, points, outs=None, device: int = -1, stream=None, devices=None):
     """Fused-fp64 evaluation of several programs over one batch
     (pe_eval_f64_multi): host points are staged to the GPU once."""
-    ev = Evaluator(DoubleDomain(), programs[0], device=device)
+    ev = Evaluator(DoubleDomain(), programs[0], device=device, devices=devices)
     cols, n = ev._soa(points, np.float64)
     dev = _is_torch_cuda(cols[0])
     if outs is None:

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "front/compile.hpp"
@@ -101,6 +102,194 @@ void build_program(Program& p, const std::uint32_t* exps, const C* coeffs, size_
   }
 }
 
+// ---- pe_program_from_compiled: flat reference CompiledProgram -> Program ----
+
+// Converts programs[idx] (and, recursively, its nested programs) after
+// checking every index the walk will use; `used` marks programs already
+// referenced, so the nesting is a tree.
+template <typename C>
+std::unique_ptr<CompiledProgram<C>> convert_program(const pe_compiled_program* progs, size_t np,
+                                                    size_t idx, std::vector<char>& used,
+                                                    std::uint32_t nvars,
+                                                    const std::vector<ExponentSet>& sets) {
+  if (idx >= np) throw std::invalid_argument("nested program index out of range");
+  if (used[idx]) throw std::invalid_argument("program referenced more than once");
+  used[idx] = 1;
+  const pe_compiled_program& src = progs[idx];
+  if (src.nrecords == 0 || !src.records) throw std::invalid_argument("program without records");
+  if (src.register_count == 0) throw std::invalid_argument("register_count must be >= 1");
+  if (src.variable >= nvars) throw std::invalid_argument("program variable out of range");
+  auto out = std::make_unique<CompiledProgram<C>>();
+  out->register_count = src.register_count;
+  out->variable = src.variable;
+  const size_t n = src.nrecords;
+  // register discipline of compiled programs (tree.hpp:68-77): every
+  // non-root record accumulates into a register that a later record reads
+  std::vector<char> read_later(src.register_count, 0);
+  for (size_t i = n; i-- > 0;) {
+    const pe_record& r = src.records[i];
+    if (r.lazy_slot >= src.register_count) throw std::invalid_argument("lazy_slot out of range");
+    if (r.reads_register != 0 && r.reads_register != 1) {
+      throw std::invalid_argument("reads_register must be 0 or 1");
+    }
+    if (i + 1 == n) {
+      if (r.parent_slot != -1) throw std::invalid_argument("root record has a parent_slot");
+    } else {
+      if (r.parent_slot < 0 || static_cast<std::uint32_t>(r.parent_slot) >= src.register_count) {
+        throw std::invalid_argument("parent_slot out of range");
+      }
+      if (!read_later[static_cast<std::uint32_t>(r.parent_slot)]) {
+        throw std::invalid_argument("record accumulates into a register no later record reads");
+      }
+    }
+    if (r.reads_register) read_later[r.lazy_slot] = 1;
+    if (r.power_slot < -1 ||
+        (r.power_slot >= 0 && static_cast<size_t>(r.power_slot) >= sets[src.variable].size())) {
+      throw std::invalid_argument("power_slot out of range");
+    }
+  }
+  // and every register a record reads was accumulated into before
+  std::vector<char> written(src.register_count, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const pe_record& r = src.records[i];
+    if (r.reads_register) {
+      if (!written[r.lazy_slot]) throw std::invalid_argument("record reads a register nothing wrote");
+      written[r.lazy_slot] = 0;
+    }
+    if (i + 1 < n) written[static_cast<std::uint32_t>(r.parent_slot)] = 1;
+  }
+  out->records.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    const pe_record& r = src.records[i];
+    auto& d = out->records[i];
+    if (r.sub >= 0) {
+      if (r.sub == 0) throw std::invalid_argument("the root program cannot be nested");
+      d.sub = convert_program<C>(progs, np, static_cast<size_t>(r.sub), used, nvars, sets);
+    } else if (r.sub != -1) {
+      throw std::invalid_argument("sub must be -1 or a program index");
+    } else if constexpr (std::is_same_v<C, double>) {
+      if (!std::isfinite(r.coeff_f64)) throw std::invalid_argument("coefficient is not finite");
+      d.coeff = r.coeff_f64;
+    } else {
+      d.coeff = r.coeff_i64;
+    }
+    if (r.power_slot >= 0) d.power_slot = static_cast<std::uint32_t>(r.power_slot);
+    d.lazy_slot = r.lazy_slot;
+    if (r.parent_slot >= 0) d.parent_slot = static_cast<std::uint32_t>(r.parent_slot);
+    d.reads_register = r.reads_register != 0;
+  }
+  if (src.nroot_child_ends > 0 && !src.root_child_ends) {
+    throw std::invalid_argument("root_child_ends is null");
+  }
+  for (size_t k = 0; k < src.nroot_child_ends; ++k) {
+    const std::uint32_t e = src.root_child_ends[k];
+    if (e >= n || (k > 0 && e <= src.root_child_ends[k - 1])) {
+      throw std::invalid_argument("root_child_ends must be ascending record indices");
+    }
+    out->root_child_ends.push_back(e);
+  }
+  return out;
+}
+
+// The polynomial a compiled program evaluates, as one term per scalar
+// record ("path terms", like terms not merged): record i of a program over
+// variable v contributes coeff * v^(sum of the power exponents on its way to
+// the program root), times the exponents of the enclosing programs. Every
+// intermediate of the walk is a partial sum of these terms times a sub-product
+// of their powers, so the int64 overflow proof over them is sound.
+template <typename C>
+void expand_terms(const CompiledProgram<C>& p, const std::vector<ExponentSet>& sets,
+                  std::vector<std::uint32_t>& prefix, std::vector<Term<C>>& out) {
+  const size_t n = p.records.size();
+  std::vector<std::uint32_t> parent(n, UINT32_MAX), next_reader(p.register_count, UINT32_MAX);
+  for (size_t i = n; i-- > 0;) {
+    const auto& r = p.records[i];
+    if (r.parent_slot) parent[i] = next_reader[*r.parent_slot];
+    if (r.reads_register) next_reader[r.lazy_slot] = static_cast<std::uint32_t>(i);
+  }
+  std::vector<std::uint64_t> total(n, 0);
+  for (size_t i = n; i-- > 0;) {
+    const auto& r = p.records[i];
+    const std::uint64_t own = r.power_slot ? sets[p.variable].exponents[*r.power_slot] : 0;
+    total[i] = own + (parent[i] == UINT32_MAX ? 0 : total[parent[i]]);
+    if (total[i] > UINT32_MAX) throw std::invalid_argument("exponent overflow in compiled program");
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const auto& r = p.records[i];
+    const std::uint32_t saved = prefix[p.variable];
+    const std::uint64_t e = static_cast<std::uint64_t>(saved) + total[i];
+    if (e > UINT32_MAX) throw std::invalid_argument("exponent overflow in compiled program");
+    prefix[p.variable] = static_cast<std::uint32_t>(e);
+    if (r.sub) {
+      expand_terms(*r.sub, sets, prefix, out);
+    } else if (r.coeff != C{}) {
+      out.push_back(Term<C>{r.coeff, prefix});
+    }
+    prefix[p.variable] = saved;
+  }
+}
+
+template <typename C>
+void program_from_compiled(Program& p, const pe_compiled_program* progs, size_t np,
+                           std::uint32_t nvars, const std::vector<ExponentSet>& sets,
+                           std::unique_ptr<CompiledProgram<C>>& prog) {
+  std::vector<char> used(np, 0);
+  prog = convert_program<C>(progs, np, 0, used, nvars, sets);
+  for (size_t k = 0; k < np; ++k) {
+    if (!used[k]) throw std::invalid_argument("program not reachable from the root");
+  }
+  prog->variable_count = nvars;
+  prog->exponent_sets = sets;
+  std::vector<std::uint32_t> prefix(nvars, 0);
+  std::vector<Term<C>> terms;
+  expand_terms(*prog, sets, prefix, terms);
+  std::vector<std::vector<std::uint32_t>> keys;
+  for (const auto& t : terms) keys.push_back(t.exponents);
+  std::sort(keys.begin(), keys.end());
+  p.nterms = static_cast<std::uint64_t>(std::unique(keys.begin(), keys.end()) - keys.begin());
+  for (std::uint32_t v = 0; v < nvars; ++v) {
+    p.variables.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
+  }
+  p.stats = program_stats(*prog);
+  if constexpr (std::is_same_v<C, std::int64_t>) p.terms_i = std::move(terms);
+}
+
+// exec->devices: one host thread per device, each running the single-device
+// call on its contiguous slice (host buffers only; each slice's results go
+// straight to the caller's output, so the gather is the pipelines' D2H).
+template <typename Fn>
+pe_status across_devices(const pe_exec& ex, size_t n, const void* probe, Fn&& fn) {
+  if (!ex.devices) return fail(PE_EINVAL, "devices is null");
+  int ignored = -1;
+  if (classify(probe, &ignored) == MemKind::Device) {
+    return fail(PE_EINVAL, "multi-device calls take host buffers");
+  }
+  const size_t nd = static_cast<size_t>(ex.ndevices);
+  const size_t per = (n + nd - 1) / nd;
+  std::vector<pe_status> st(nd, PE_OK);
+  std::vector<std::string> msg(nd);
+  std::vector<std::thread> pool;
+  for (size_t k = 0; k < nd; ++k) {
+    const size_t lo = std::min(n, k * per), cnt = std::min(n, lo + per) - lo;
+    if (cnt == 0) continue;
+    pool.emplace_back([&, k, lo, cnt] {
+      pe_exec e = ex;
+      e.device = ex.devices[k];
+      e.devices = nullptr;
+      e.ndevices = 0;
+      st[k] = fn(e, lo, cnt);
+      if (st[k] != PE_OK) msg[k] = g_last_error;
+    });
+  }
+  for (auto& t : pool) t.join();
+  for (size_t k = 0; k < nd; ++k) {
+    if (st[k] != PE_OK) return fail(st[k], "device " + std::to_string(ex.devices[k]) + ": " + msg[k]);
+  }
+  return PE_OK;
+}
+
+bool multi_device(const pe_exec* exec) { return exec && exec->ndevices > 0; }
+
 }  // namespace
 }  // namespace polyeval::rt
 
@@ -140,6 +329,47 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
         if (!std::isfinite(c[t])) return fail(PE_EINVAL, "coefficient is not finite");
       }
       build_program(p, exponents, c, nterms, nvars, schemes, p.tree_f, p.prog_f);
+    }
+    *out = h.release();
+    return PE_OK;
+  });
+}
+
+pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t nprograms,
+                                   uint32_t nvars, const uint32_t* const* exponent_sets,
+                                   const size_t* exponent_set_sizes, pe_coeff_type coeff_type,
+                                   pe_program** out) {
+  return guarded([&]() -> pe_status {
+    if (!out) return fail(PE_EINVAL, "out is null");
+    *out = nullptr;
+    if (!programs || nprograms == 0) return fail(PE_EINVAL, "no programs");
+    if (nvars == 0) return fail(PE_EINVAL, "nvars must be >= 1");
+    if (!exponent_sets || !exponent_set_sizes) return fail(PE_EINVAL, "exponent sets are null");
+    if (coeff_type != PE_COEFF_F64 && coeff_type != PE_COEFF_I64) {
+      return fail(PE_EINVAL, "unknown coefficient type");
+    }
+    std::vector<ExponentSet> sets(nvars);
+    for (uint32_t v = 0; v < nvars; ++v) {
+      const size_t k = exponent_set_sizes[v];
+      if (k > 0 && !exponent_sets[v]) return fail(PE_EINVAL, "exponent set is null");
+      for (size_t i = 0; i < k; ++i) {
+        const uint32_t e = exponent_sets[v][i];
+        if (e == 0 || (i > 0 && e <= exponent_sets[v][i - 1])) {
+          return fail(PE_EINVAL, "exponent sets must be ascending, distinct and >= 1");
+        }
+        sets[v].exponents.push_back(e);
+      }
+    }
+    auto h = std::make_unique<pe_program>();
+    Program& p = h->impl;
+    p.nvars = nvars;
+    p.integer = coeff_type == PE_COEFF_I64;
+    if (p.integer) {
+      program_from_compiled(p, programs, nprograms, nvars, sets, p.prog_i);
+      p.i64_uniform_bound = uniform_bounds(p, 63);
+      p.i53_uniform_bound = uniform_bounds(p, 53);
+    } else {
+      program_from_compiled(p, programs, nprograms, nvars, sets, p.prog_f);
     }
     *out = h.release();
     return PE_OK;
@@ -223,6 +453,9 @@ pe_status pe_program_dot(const pe_program* program, char* out, size_t cap, size_
   return guarded([&]() -> pe_status {
     if (!program || !len) return fail(PE_EINVAL, "null argument");
     const Program& p = program->impl;
+    if (p.integer ? !p.tree_i : !p.tree_f) {
+      return fail(PE_EINVAL, "program was created from a compiled program and has no tree");
+    }
     const std::string dot = p.integer ? to_dot(*p.tree_i) : to_dot(*p.tree_f);
     *len = dot.size();
     if (out && cap) {
@@ -353,6 +586,13 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     for (uint32_t v = 0; v < p.nvars; ++v) {
       if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
     }
+    if (multi_device(exec)) {
+      return across_devices(*exec, n, out, [&](const pe_exec& e, size_t lo, size_t cnt) {
+        std::vector<const double*> c(p.nvars);
+        for (uint32_t v = 0; v < p.nvars; ++v) c[v] = coords[v] + lo;
+        return pe_eval_f64(program, c.data(), cnt, out + lo, &e);
+      });
+    }
     const bool strict = exec && exec->strict_f64;
     MemKind kind;
     const int dev = resolve_device(exec, out, &kind);
@@ -383,6 +623,15 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
     }
     for (uint32_t v = 0; v < nv; ++v) {
       if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
+    }
+    if (multi_device(exec)) {
+      return across_devices(*exec, n, outs[0], [&](const pe_exec& e, size_t lo, size_t cnt) {
+        std::vector<const double*> c(nv);
+        for (uint32_t v = 0; v < nv; ++v) c[v] = coords[v] + lo;
+        std::vector<double*> o(k);
+        for (size_t j = 0; j < k; ++j) o[j] = outs[j] + lo;
+        return pe_eval_f64_multi(programs, k, c.data(), cnt, o.data(), &e);
+      });
     }
     MemKind kind;
     const int dev = resolve_device(exec, outs[0], &kind);
@@ -417,6 +666,16 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
       if (!lo[v] || !hi[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
       ins.push_back(lo[v]);
       ins.push_back(hi[v]);
+    }
+    if (multi_device(exec)) {
+      return across_devices(*exec, n, out_lo, [&](const pe_exec& e, size_t off, size_t cnt) {
+        std::vector<const double*> l(p.nvars), h(p.nvars);
+        for (uint32_t v = 0; v < p.nvars; ++v) {
+          l[v] = lo[v] + off;
+          h[v] = hi[v] + off;
+        }
+        return pe_eval_interval(program, l.data(), h.data(), cnt, out_lo + off, out_hi + off, &e);
+      });
     }
     MemKind kind;
     const int dev = resolve_device(exec, out_lo, &kind);
@@ -462,6 +721,13 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
     if (!coords || !out) return fail(PE_EINVAL, "null buffer");
     for (uint32_t v = 0; v < p.nvars; ++v) {
       if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
+    }
+    if (multi_device(exec)) {
+      return across_devices(*exec, n, out, [&](const pe_exec& e, size_t lo, size_t cnt) {
+        std::vector<const int64_t*> c(p.nvars);
+        for (uint32_t v = 0; v < p.nvars; ++v) c[v] = coords[v] + lo;
+        return pe_eval_i64(program, c.data(), cnt, out + lo, &e);
+      });
     }
     MemKind kind;
     const int dev = resolve_device(exec, out, &kind);

@@ -143,7 +143,7 @@ Artifact& Program::loaded(lower::Domain d, int device) const {
 }
 
 std::size_t Program::slice_count() const {
-  if (integer) return 1;
+  if (integer || !poly_f) return 1;  // no terms/schemes (pe_program_from_compiled): unsliced
   std::size_t k = 0;
   if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
   if (k == 0) {

@@ -390,3 +390,39 @@ def test_interval_fast_path_extreme_magnitudes(scheme, cuda_device):
     glo, ghi = glo.cpu().numpy(), ghi.cpu().numpy()
     assert np.array_equal(glo.view(np.int64), olo.view(np.int64))
     assert np.array_equal(ghi.view(np.int64), ohi.view(np.int64))
+
+
+def test_multi_device_host_batches_shard_and_gather(cuda_device):
+    # pe_exec.devices: contiguous slices per listed device, results gathered
+    # into the host output. One GPU on the box: the list repeats device 0
+    # (each slice still runs its own pipeline); results must equal the
+    # single-device call bit for bit.
+    import torch
+    ndev = torch.cuda.device_count()
+    devs = list(range(ndev)) if ndev > 1 else [0, 0, 0]
+    wl = W.c2(1000, "balanced")
+    prog = pe.compile(wl.poly, wl.schemes)
+    pts = wl.points(1_000_003)
+    one = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(pts)
+    many = pe.Evaluator(pe.DoubleDomain(), prog, devices=devs).evaluate(pts)
+    assert np.array_equal(one.view(np.int64), many.view(np.int64))
+    outs = pe.evaluate_many([prog, prog], pts, devices=devs)
+    assert np.array_equal(outs[1].view(np.int64), one.view(np.int64))
+
+    w3 = W.c3()
+    p3 = pe.compile(w3.poly, w3.schemes)
+    x3 = w3.points(300_001)
+    assert np.array_equal(pe.Evaluator(pe.BigIntDomain(), p3, devices=devs).evaluate(x3),
+                          pe.Evaluator(pe.BigIntDomain(), p3).evaluate(x3))
+
+    w5 = W.c5()
+    p5 = pe.compile(w5.poly, w5.schemes)
+    lo, hi = w5.points(300_007)
+    a = pe.Evaluator(pe.IntervalDomain(), p5, devices=devs).evaluate((lo, hi))
+    b = pe.Evaluator(pe.IntervalDomain(), p5).evaluate((lo, hi))
+    assert np.array_equal(a[0].view(np.int64), b[0].view(np.int64))
+    assert np.array_equal(a[1].view(np.int64), b[1].view(np.int64))
+
+    with pytest.raises(ValueError):  # device buffers live on one device
+        pe.Evaluator(pe.DoubleDomain(), prog, devices=devs).evaluate(
+            [_t(pts[0][:1000], cuda_device)])
