@@ -74,8 +74,19 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     const unsigned fix_grid = static_cast<unsigned>(
         std::min<std::uint64_t>(4 * static_cast<std::uint64_t>(sm_count(device)),
                                 (la.cap + 127) / 128));
+    cudaStream_t fs = stream;
+    if (la.fix_stream) {
+      // hand the list over to the side stream: the latency-bound replay then
+      // runs beside the next chunk's fast path instead of after it
+      cudaEvent_t ev;
+      check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventRecord(ev, stream), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(la.fix_stream, ev, 0), "cudaStreamWaitEvent");
+      cudaEventDestroy(ev);
+      fs = la.fix_stream;
+    }
     check_cuda(cudaLaunchKernel(reinterpret_cast<const void*>(a.fix_kernel), dim3(fix_grid ? fix_grid : 1),
-                                dim3(128), args.data(), 0, stream),
+                                dim3(128), args.data(), 0, fs),
                "cudaLaunchKernel(fixup)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   }
@@ -202,19 +213,42 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     }
   };
   if (kind == MemKind::Device) {
-    const size_t max_chunk = size_t{1} << 30;
+    size_t max_chunk = size_t{1} << 30;
     // a caller-bound list (deferred checks) is reused; otherwise per call
     const bool own_list = proto.list == 0;
+    // deferred interval calls with a side stream: chunks of >= 1M points, each
+    // with its own list region and counter; chunk k's fixup kernel overlaps
+    // chunk k+1's fast path
+    const bool overlap = !own_list && proto.fix_stream && a.image.interval_fast_path;
+    if (overlap) {
+      const size_t k = std::clamp<size_t>(n >> 20, 1, StreamState::kMaxChunks);
+      max_chunk = (n + k - 1) / k;
+    }
     FixupLists fix(a, own_list ? std::min(n, max_chunk) : 0, full_fixup, {user_stream});
-    for (size_t off = 0; off < n; off += max_chunk) {
+    size_t idx = 0;
+    for (size_t off = 0; off < n; off += max_chunk, ++idx) {
       LaunchArgs la = proto;
       if (own_list) fix.bind(la, 0);
       la.n = std::min(max_chunk, n - off);
+      if (overlap) {
+        la.list = proto.list + 4 * off;
+        la.count = proto.count + 4 * idx;
+        la.cap = la.n;
+      } else {
+        la.fix_stream = nullptr;
+      }
       la.ins.clear();
       la.outs.clear();
       for (auto p : ins) la.ins.push_back(reinterpret_cast<std::uint64_t>(static_cast<const char*>(p) + off * elem));
       for (auto p : outs) la.outs.push_back(reinterpret_cast<std::uint64_t>(static_cast<char*>(p) + off * elem));
       launch_all(la, user_stream);
+    }
+    if (overlap) {  // the caller's stream resumes after the last replay
+      cudaEvent_t ev;
+      check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventRecord(ev, proto.fix_stream), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(user_stream, ev, 0), "cudaStreamWaitEvent");
+      cudaEventDestroy(ev);
     }
     if (sync) check_cuda(cudaStreamSynchronize(user_stream), "cudaStreamSynchronize");
     return;

@@ -27,6 +27,9 @@ struct LaunchArgs {
   std::vector<std::uint64_t> bounds;
   // interval fast path: fixup list (u32 point indices), counter, capacity
   std::uint64_t list = 0, count = 0, cap = 0;
+  // interval fast path: run the fixup kernel on this stream (after an event
+  // from the launching stream) so it overlaps the next chunk's fast path
+  cudaStream_t fix_stream = nullptr;
 };
 
 int sm_count(int device);
@@ -41,10 +44,12 @@ MemKind classify(const void* p, int* device);
 // Deferred-check state of one caller stream: an accumulating status word and
 // a grow-only full-capacity interval fixup list, both stream-ordered.
 struct StreamState {
+  static constexpr int kMaxChunks = 16;  // fixup counters: one per overlapped chunk
   unsigned* status = nullptr;
   void* list = nullptr;
-  unsigned* count = nullptr;
+  unsigned* count = nullptr;            // kMaxChunks words
   std::uint64_t list_cap = 0;
+  cudaStream_t side = nullptr;          // fixup kernels (overlap with the next chunk)
 };
 
 struct DeviceCtx {
@@ -61,14 +66,18 @@ struct DeviceCtx {
     std::lock_guard<std::mutex> lock(state_mu);
     StreamState& st = states[s];
     if (!st.status) {
-      check_cuda(cudaMalloc(reinterpret_cast<void**>(&st.status), 2 * sizeof(unsigned)),
+      const size_t words = 1 + StreamState::kMaxChunks;
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&st.status), words * sizeof(unsigned)),
                  "cudaMalloc(status)");
-      check_cuda(cudaMemsetAsync(st.status, 0, 2 * sizeof(unsigned), s), "cudaMemsetAsync(status)");
+      check_cuda(cudaMemsetAsync(st.status, 0, words * sizeof(unsigned), s),
+                 "cudaMemsetAsync(status)");
       st.count = st.status + 1;
+      check_cuda(cudaStreamCreateWithFlags(&st.side, cudaStreamNonBlocking), "cudaStreamCreate(side)");
     }
     if (need_list > st.list_cap) {
       if (st.list) {
         check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        check_cuda(cudaStreamSynchronize(st.side), "cudaStreamSynchronize(side)");
         cudaFree(st.list);
       }
       check_cuda(cudaMalloc(&st.list, 4 * need_list), "cudaMalloc(fixup list)");
