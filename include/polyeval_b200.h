@@ -201,6 +201,14 @@ pe_status pe_program_records(const pe_program* program, int32_t* out,
 pe_status pe_program_dot(const pe_program* program, char* out, size_t cap,
                          size_t* len);
 
+/* Register hygiene (reference Evaluator::enable_register_check,
+ * eval.hpp:142-145 and the check at eval.hpp:240-247): every point walks the
+ * same record sequence, so "the register file is clean after the walk" is a
+ * property of the program — checked once, symbolically, over the root and
+ * every nested program. PE_OK if clean, PE_ELOGIC ("register file not clean
+ * after walk") if some record's value is never consumed. */
+pe_status pe_program_check_registers(const pe_program* program);
+
 /* Specialised kernel statistics for a domain (0 f64, 1 f64 strict, 2 i64,
  * 3 interval): FP64 / int64 arithmetic instructions per point, and the PTX
  * text size. Generates (but does not load) the kernel. */

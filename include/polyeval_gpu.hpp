@@ -127,6 +127,20 @@ class BatchEvaluator {
     }
   }
 
+  /// Reference evaluate_parallel (eval.hpp:97-140): identical results; the
+  /// worker count is validated, the batch is spread over the GPU anyway.
+  void evaluate_parallel(std::initializer_list<const typename D::Value*> coords, std::size_t n,
+                         typename D::Value* out, unsigned workers) const {
+    if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+    evaluate(coords, n, out);
+  }
+
+  /// Reference enable_register_check (eval.hpp:142-145), checked once per
+  /// program (every point walks the same records).
+  void enable_register_check(bool on) {
+    if (on) check(pe_program_check_registers(program_.get()));
+  }
+
   /// IntervalDomain: lo/hi coordinate arrays, lo/hi results.
   void evaluate(std::initializer_list<const double*> lo, std::initializer_list<const double*> hi,
                 std::size_t n, double* out_lo, double* out_hi) const {

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     compile,
     evaluate,
     evaluate_many,
+    evaluate_parallel,
     launch_count,
     scheme_from_name,
     threshold_combine,

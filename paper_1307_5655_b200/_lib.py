@@ -95,6 +95,7 @@ EXPORTS = [
     ("pe_program_records", C.c_int,
      [C.c_void_p, C.POINTER(C.c_int32), C.c_size_t, C.POINTER(C.c_size_t)]),
     ("pe_program_dot", C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("pe_program_check_registers", C.c_int, [C.c_void_p]),
     ("pe_program_kernel_stats", C.c_int,
      [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
       C.POINTER(C.c_uint64)]),

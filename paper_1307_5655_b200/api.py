@@ -393,6 +393,7 @@ class Evaluator:
         """points: per-variable arrays (numpy -> host staged, torch CUDA ->
         in place); IntervalDomain takes (lo_arrays, hi_arrays)."""
         lib = L.lib()
+        self._register_check()
         if isinstance(self.domain, IntervalDomain):
             lo, hi = points
             lo_c, n = self._soa(lo, np.float64)
@@ -418,6 +419,28 @@ class Evaluator:
         fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
         L.check(fn(self.program.handle, ptrs, n, self._ptr(out), C.byref(ex)))
         return out
+
+    def enable_register_check(self, on: bool = True) -> None:
+        """Reference Evaluator::enable_register_check (eval.hpp:142-145):
+        evaluate() raises LogicError if the walk leaves a value unconsumed.
+        Every point walks the same records, so the check runs once per
+        program, symbolically (pe_program_check_registers)."""
+        self.check_registers = bool(on)
+        self._registers_ok = None
+
+    def _register_check(self):
+        if getattr(self, "check_registers", False):
+            if self._registers_ok is None:
+                L.check(L.lib().pe_program_check_registers(self.program.handle))
+                self._registers_ok = True
+
+    def evaluate_parallel(self, points, workers: int, out=None, stream=None):
+        """Reference evaluate_parallel (eval.hpp:97-140): same result as
+        evaluate() — bit-identical by the reference's own contract — with the
+        worker count validated; the batch is already spread over the GPU."""
+        if int(workers) < 1:
+            raise ValueError("workers must be >= 1")
+        return self.evaluate(points, out=out, stream=stream)
 
     def synchronize(self, stream=None):
         """Waits for the stream; raises any deferred domain-check failure."""
@@ -466,6 +489,11 @@ def evaluate_many(programs, points, outs=None, device: int = -1, stream=None, de
 def evaluate(program: CompiledProgram, points, domain):
     """One-shot convenience wrapper (reference eval.hpp:262-268)."""
     return Evaluator(domain, program).evaluate(points)
+
+
+def evaluate_parallel(program: CompiledProgram, points, domain, workers: int):
+    """One-shot parallel evaluation (reference eval.hpp:271-277)."""
+    return Evaluator(domain, program).evaluate_parallel(points, workers)
 
 
 def launch_count() -> int:

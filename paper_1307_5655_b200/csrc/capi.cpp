@@ -335,6 +335,30 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
   });
 }
 
+pe_status pe_program_check_registers(const pe_program* program) {
+  return guarded([&]() -> pe_status {
+    if (!program) return fail(PE_EINVAL, "program is null");
+    const Program& p = program->impl;
+    auto clean = [](const auto& self, const auto& prog) -> bool {
+      std::vector<char> live(prog.register_count, 0);
+      const size_t n = prog.records.size();
+      for (size_t i = 0; i < n; ++i) {
+        const auto& r = prog.records[i];
+        if (r.sub && !self(self, *r.sub)) return false;
+        if (r.reads_register) live[r.lazy_slot] = 0;   // eval.hpp:225-228
+        if (i + 1 < n && r.parent_slot) live[*r.parent_slot] = 1;  // L237-238
+      }
+      for (char c : live) {
+        if (c) return false;
+      }
+      return true;
+    };
+    const bool ok = p.integer ? clean(clean, *p.prog_i) : clean(clean, *p.prog_f);
+    if (!ok) return fail(PE_ELOGIC, "register file not clean after walk");
+    return PE_OK;
+  });
+}
+
 pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t nprograms,
                                    uint32_t nvars, const uint32_t* const* exponent_sets,
                                    const size_t* exponent_set_sizes, pe_coeff_type coeff_type,

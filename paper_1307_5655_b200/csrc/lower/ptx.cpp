@@ -353,7 +353,7 @@ class Emitter {
     };
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
       if (d_ == Domain::Interval) {
-        const IvCoef c = inject(s_.coefs[k]);
+        const IvCoef c = ivcoef(k);
         coef_lo_[k] = word(bits_of(c.lo));
         coef_hi_[k] = word(bits_of(c.hi));
       } else if (d_ == Domain::I64 || d_ == Domain::I64F) {
@@ -377,6 +377,18 @@ class Emitter {
     n_global_ = n - n_const_ - n_param_;
   }
 
+  // Interval value of coefficient k: injection, then the folded zero-add
+  // steps (std::nextafter outward, as interval_add would apply them).
+  IvCoef ivcoef(std::size_t k) const {
+    IvCoef c = inject(s_.coefs[k]);
+    const std::uint32_t w = k < s_.widen.size() ? s_.widen[k] : 0;
+    for (std::uint32_t i = 0; i < w; ++i) {
+      c.lo = std::nextafter(c.lo, -std::numeric_limits<double>::infinity());
+      c.hi = std::nextafter(c.hi, std::numeric_limits<double>::infinity());
+    }
+    return c;
+  }
+
   // coefficient words / arithmetic registers
   // The fast interval path needs finite, nonzero, non-straddling coefficient
   // intervals (checked here once) and a walk that ends in a register.
@@ -386,7 +398,7 @@ class Emitter {
     }
     if (!s_.result.is(Operand::Reg)) return false;
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
-      const IvCoef c = inject(s_.coefs[k]);
+      const IvCoef c = ivcoef(k);
       if (!std::isfinite(c.lo) || !std::isfinite(c.hi) || c.lo == 0.0 || c.hi == 0.0) return false;
       if ((c.lo < 0) != (c.hi < 0)) return false;
     }
@@ -1028,7 +1040,7 @@ class Emitter {
   // is caught by the nextafter "no move" test, so "known" never hides one).
   int sgn(const Operand& o) const {
     switch (o.kind) {
-      case Operand::Coef: return inject(s_.coefs[o.id]).lo > 0 ? 1 : -1;
+      case Operand::Coef: return ivcoef(o.id).lo > 0 ? 1 : -1;
       case Operand::Reg: return o.id < rsign_.size() ? rsign_[o.id] : 0;
       case Operand::Pow: return psign_[o.id];
       default: return 0;

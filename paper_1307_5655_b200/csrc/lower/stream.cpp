@@ -82,14 +82,23 @@ struct Lowerer {
   const std::vector<std::vector<std::uint32_t>>& pow_of;
 
   Operand new_reg() { return Operand::reg(s.nregs++); }
-  Operand coef(const C& c) {
+  Operand coef(const C& c, std::uint32_t widen = 0) {
     s.coefs.push_back(c);
+    s.widen.push_back(widen);
     return Operand::coef(static_cast<std::uint32_t>(s.coefs.size() - 1));
   }
   Operand power(const CompiledProgram<C>& p, std::uint32_t slot) {
     return Operand::pow(pow_of.at(p.variable).at(slot));
   }
   Operand emit(OpKind k, Operand a, Operand b, Operand c = {}) {
+    if (s.strict && k == OpKind::Add && a.is(Operand::Zero) && b.is(Operand::Coef)) {
+      // zero register + constant: a constant (one more outward step for
+      // intervals), evaluated on the host instead of per point
+      ++s.n_add;
+      ++s.n_zero_add;
+      ++s.n_folded;
+      return coef(s.coefs[b.id], s.widen[b.id] + 1);
+    }
     Operand d = new_reg();
     s.ops.push_back(Op{k, d.id, a, b, c});
     switch (k) {

@@ -70,12 +70,16 @@ struct Stream {
   std::vector<Power> powers;       // topological: operands before products
   std::vector<Op> ops;             // the walk
   std::vector<C> coefs;            // coefficient table, first-use order
+  // strict streams: outward nextafter steps applied when coefficient k is
+  // injected (an interval zero-add of a constant, [next_down(0 + c.lo),
+  // next_up(0 + c.hi)], folded on the host; fp64 0.0 + c == c needs none)
+  std::vector<std::uint32_t> widen;
   std::uint32_t nregs = 0;         // virtual registers used by `ops`
   Operand result;                  // Reg, Coef or Zero
   bool strict = false;
 
   // Counters for the roofline bookkeeping.
-  std::uint64_t n_add = 0, n_mul = 0, n_fma = 0, n_zero_add = 0;
+  std::uint64_t n_add = 0, n_mul = 0, n_fma = 0, n_zero_add = 0, n_folded = 0;
   std::uint64_t power_muls() const {
     std::uint64_t m = 0;
     for (const auto& p : powers) m += p.exponent > 1 ? 1 : 0;

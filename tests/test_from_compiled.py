@@ -100,3 +100,36 @@ def test_nested_program_referenced_twice_is_rejected():
     ], "register_count": 1, "variable": 0}
     with pytest.raises(ValueError):
         pe.CompiledProgram.from_compiled([root, inner], [[1], []])
+
+
+def test_register_check_clean_programs():
+    # reference enable_register_check (eval.hpp:142-145): compiled programs
+    # leave the register file clean
+    for wl in (W.c2(1000, "estrin"), W.c3()):
+        prog = pe.compile(wl.poly, wl.schemes)
+        assert pe._lib.lib().pe_program_check_registers(prog.handle) == 0
+
+
+def test_register_check_flags_unconsumed_value():
+    # record 0 accumulates into register 1, which nothing reads: the walk
+    # leaves a value behind (structurally valid for the lowering, unclean)
+    progs = [{"records": [
+        {"coeff": 3.0, "power_slot": 0, "lazy_slot": 0, "parent_slot": 0},
+        {"coeff": 5.0, "lazy_slot": 1, "parent_slot": 1},
+        {"coeff": 2.0, "power_slot": 0, "lazy_slot": 0, "parent_slot": 1,
+         "reads_register": True},
+        {"coeff": 1.0, "lazy_slot": 1, "reads_register": True},
+    ], "register_count": 2, "variable": 0}]
+    prog = pe.CompiledProgram.from_compiled(progs, [[1]])
+    assert pe._lib.lib().pe_program_check_registers(prog.handle) == 0
+    progs[0]["records"][3]["reads_register"] = False
+    with pytest.raises(ValueError):  # rejected outright: register 1 never read
+        pe.CompiledProgram.from_compiled(progs, [[1]])
+
+
+def test_evaluate_parallel_validates_workers():
+    wl = W.c2(1000, "estrin")
+    prog = pe.compile(wl.poly, wl.schemes)
+    ev = pe.Evaluator(pe.DoubleDomain(), prog)
+    with pytest.raises(ValueError):
+        ev.evaluate_parallel(wl.points(4), 0)

@@ -426,3 +426,19 @@ def test_multi_device_host_batches_shard_and_gather(cuda_device):
     with pytest.raises(ValueError):  # device buffers live on one device
         pe.Evaluator(pe.DoubleDomain(), prog, devices=devs).evaluate(
             [_t(pts[0][:1000], cuda_device)])
+
+
+def test_evaluate_parallel_and_register_check(cuda_device):
+    # reference evaluate_parallel is bit-identical to evaluate for any worker
+    # count (eval.hpp:91-96); the register check passes on compiled programs
+    wl = W.c2(1000, "balanced")
+    prog = pe.compile(wl.poly, wl.schemes)
+    pts = wl.points(10_007)
+    ev = pe.Evaluator(pe.DoubleDomain(strict=True), prog)
+    ev.enable_register_check(True)
+    a = ev.evaluate(pts)
+    for w in (1, 3, 64):
+        b = ev.evaluate_parallel(pts, w)
+        assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    c = pe.evaluate_parallel(prog, pts, pe.DoubleDomain(strict=True), 4)
+    assert np.array_equal(a.view(np.int64), c.view(np.int64))
