@@ -115,7 +115,12 @@ DeviceCtx& device_ctx(int device) {
   auto& c = ctxs[device];
   if (!c) {
     c = std::make_unique<DeviceCtx>();
-    for (auto& s : c->streams) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (const char* e = std::getenv("PE_STAGE_SLOTS")) {
+      c->slots = std::clamp(std::atoi(e), 2, DeviceCtx::kMaxSlots);
+    }
+    for (int i = 0; i < c->slots; ++i) {
+      check_cuda(cudaStreamCreateWithFlags(&c->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
+    }
     check_cuda(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device),
                "cudaDeviceGetAttribute");
   }
@@ -129,7 +134,8 @@ static void ensure_buffers(DeviceCtx& c, size_t arrays, size_t bytes) {
     slot.clear();
   }
   c.cap = std::max(bytes, c.cap);
-  for (auto& slot : c.buffers) {
+  for (int k = 0; k < c.slots; ++k) {
+    auto& slot = c.buffers[k];
     for (size_t i = 0; i < arrays; ++i) {
       void* p = nullptr;
       check_cuda(cudaMalloc(&p, c.cap), "cudaMalloc(staging)");
@@ -268,13 +274,15 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     // the flag was initialised on user_stream: order the slots after it
     check_cuda(cudaEventCreateWithFlags(&flag_ready, cudaEventDisableTiming), "cudaEventCreate");
     check_cuda(cudaEventRecord(flag_ready, user_stream), "cudaEventRecord");
-    for (auto s : c.streams) check_cuda(cudaStreamWaitEvent(s, flag_ready, 0), "cudaStreamWaitEvent");
+    for (int i = 0; i < c.slots; ++i) {
+      check_cuda(cudaStreamWaitEvent(c.streams[i], flag_ready, 0), "cudaStreamWaitEvent");
+    }
   }
   FixupLists fix(a, chunk, full_fixup,
-                 std::vector<cudaStream_t>(c.streams, c.streams + DeviceCtx::kSlots));
+                 std::vector<cudaStream_t>(c.streams, c.streams + c.slots));
   size_t k = 0;
   for (size_t off = 0; off < n; off += chunk, ++k) {
-    const int slot = static_cast<int>(k % DeviceCtx::kSlots);
+    const int slot = static_cast<int>(k % static_cast<size_t>(c.slots));
     cudaStream_t s = c.streams[slot];
     const size_t m = std::min(chunk, n - off);
     LaunchArgs la = proto;
@@ -299,7 +307,7 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
                  "cudaMemcpyAsync(D2H)");
     }
   }
-  for (auto s : c.streams) check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  for (int i = 0; i < c.slots; ++i) check_cuda(cudaStreamSynchronize(c.streams[i]), "cudaStreamSynchronize");
   if (flag_ready) cudaEventDestroy(flag_ready);
 }
 

@@ -53,9 +53,10 @@ struct StreamState {
 };
 
 struct DeviceCtx {
-  static constexpr int kSlots = 3;
-  cudaStream_t streams[kSlots] = {};
-  std::vector<void*> buffers[kSlots];  // per slot: arrays of `cap` bytes
+  static constexpr int kMaxSlots = 8;
+  int slots = 3;                          // pipeline depth (PE_STAGE_SLOTS, 2..8)
+  cudaStream_t streams[kMaxSlots] = {};
+  std::vector<void*> buffers[kMaxSlots];  // per slot: arrays of `cap` bytes
   size_t cap = 0;
   std::mutex mu;  // serialises host-staged calls on a device
   int sms = 0;

@@ -11,7 +11,9 @@ x = [torch.from_numpy(a).pin_memory() for a in wls[0].points()]
 outs = [torch.empty(x[0].shape[0], dtype=torch.float64).pin_memory() for _ in wls]
 xs = [a.numpy() for a in x]
 os_ = [o.numpy() for o in outs]
-for chunk in [0, 1 << 18, 1 << 19, 625000, 1 << 21, 1250000]:
+chunks = [int(c) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
+    [0, 1 << 18, 1 << 19, 625000, 1 << 21, 1250000]
+for chunk in chunks:
     if chunk:
         os.environ["PE_STAGE_CHUNK"] = str(chunk)
     else:
@@ -21,4 +23,5 @@ for chunk in [0, 1 << 18, 1 << 19, 625000, 1 << 21, 1250000]:
     for _ in range(5):
         pe.evaluate_many(progs, xs, outs=os_)
     el = (time.perf_counter() - t) / 5
-    print(f"chunk={chunk or 'default'}: {el * 1e3:.2f} ms/step -> {4e7 / el:.3e} points/s", flush=True)
+    print(f"slots={os.environ.get('PE_STAGE_SLOTS', 3)} chunk={chunk or 'default'}: "
+          f"{el * 1e3:.2f} ms/step -> {4e7 / el:.3e} points/s", flush=True)
