@@ -17,6 +17,8 @@
  *                          evaluate(point) per point   eval.hpp:74-90, ring.hpp:40-48
  *   pe_eval_i64            Evaluator<BigIntDomain> on a proven int64 range
  *                                                       eval.hpp:74-90, ring.hpp:30-38
+ *   pe_eval_limbs          Evaluator<BigIntDomain> beyond int64 (K x 64-bit limbs)
+ *                                                       ring.hpp:30-38, bigint.cpp
  *   pe_eval_interval       Evaluator<IntervalDomain>    ring.hpp:50-65, interval.cpp:36-52
  *   pe_program_info        CompiledProgram fields (register_count, records,
  *                          exponent_sets, root_child_ends)  eval.hpp:32-54
@@ -210,8 +212,10 @@ pe_status pe_program_dot(const pe_program* program, char* out, size_t cap,
 pe_status pe_program_check_registers(const pe_program* program);
 
 /* Specialised kernel statistics for a domain (0 f64, 1 f64 strict, 2 i64,
- * 3 interval): FP64 / int64 arithmetic instructions per point, and the PTX
- * text size. Generates (but does not load) the kernel. */
+ * 3 interval, 4 i64 on the FP64 pipe, PE_DOMAIN_LIMBS(K) the K-limb exact
+ * kernel): FP64 / int64 arithmetic instructions per point, and the PTX text
+ * size. Generates (but does not load) the kernel. */
+#define PE_DOMAIN_LIMBS(k) (0x100 | (k))
 pe_status pe_program_kernel_stats(const pe_program* program, int32_t domain,
                                   uint64_t* fp_ops, uint64_t* int_ops,
                                   uint64_t* ptx_bytes);
@@ -249,6 +253,20 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
 
 pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords,
                       size_t n, int64_t* out, const pe_exec* exec);
+
+/* Exact integer evaluation beyond int64 (reference BigIntDomain,
+ * ring.hpp:30-38, bigint.cpp): every value is `limbs` 64-bit words, two's
+ * complement, little-endian; out_limbs[k][i] is word k of point i's result.
+ * Runs when the host proof bounds every intermediate below 2^(64*limbs-1)
+ * for the batch's coordinate maxima (computed on the device / host), else
+ * PE_EOVERFLOW — choose `limbs` with pe_program_limbs_needed. 1 <= limbs <= 8. */
+pe_status pe_eval_limbs(const pe_program* program, const int64_t* const* coords, size_t n,
+                        uint32_t limbs, uint64_t* const* out_limbs, const pe_exec* exec);
+
+/* Smallest limb count (1..8) the proof allows for |x_v| <= bounds[v]
+ * (nvars entries); *limbs = 0 when 8 limbs do not suffice. */
+pe_status pe_program_limbs_needed(const pe_program* program, const uint64_t* bounds,
+                                  uint32_t* limbs);
 
 /* Interval points [lo[v][i], hi[v][i]]; results [out_lo[i], out_hi[i]].
  * Endpoints must be non-NaN with lo <= hi (reference Interval ctor). */

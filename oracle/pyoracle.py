@@ -92,6 +92,8 @@ def ref_lib():
         lib.ref_export.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                    C.POINTER(C.c_size_t)]
+        lib.ref_eval_limbs.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32,
+                                        C.c_void_p, C.c_int]
         lib.ref_last_error.restype = C.c_char_p
         _ref = lib
     return _ref
@@ -191,7 +193,10 @@ class Reference:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            ref_lib().ref_destroy(self._h)
+            try:
+                ref_lib().ref_destroy(self._h)
+            except Exception:  # noqa: BLE001 — interpreter shutdown
+                pass
             self._h = None
 
     def _check(self, st):
@@ -253,6 +258,15 @@ class Reference:
         self._check(ref_lib().ref_eval_parallel_f64(self._h, _ptrs(cols), out.shape[0],
                                                     out.ctypes.data, workers))
         return out
+
+    def eval_limbs(self, coords, limbs, threads=1):
+        """Exact BigInt results as `limbs` uint64 arrays (two's complement)."""
+        cols = [np.ascontiguousarray(c, dtype=np.int64) for c in coords]
+        n = cols[0].shape[0]
+        out = np.zeros((limbs, n), dtype=np.uint64)
+        self._check(ref_lib().ref_eval_limbs(self._h, _ptrs(cols), n, limbs, out.ctypes.data,
+                                             threads))
+        return list(out)
 
     def eval_interval(self, lo, hi, threads=1):
         lo = [np.ascontiguousarray(c, dtype=np.float64) for c in lo]

@@ -315,6 +315,49 @@ int ref_eval_i64(void* h, const std::int64_t* const* coords, std::size_t n, std:
   });
 }
 
+// BigInt results as K 64-bit limbs (little-endian two's complement):
+// out[k * n + i] = word k of point i. Throws if a result needs more than
+// 64K-1 bits. Decimal round trip, so the harness needs no BigInt internals.
+int ref_eval_limbs(void* h, const std::int64_t* const* coords, std::size_t n, std::uint32_t K,
+                   std::uint64_t* out, int threads) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    if (!rp.integer) throw std::invalid_argument("integer evaluation needs integer coefficients");
+    auto pt = [&](std::size_t i, std::vector<BigInt>& p) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = BigInt(coords[v][i]);
+    };
+    std::vector<std::string> dec(n);
+    run_sharded(rp, BigIntDomain{}, n, threads, pt, dec.data(),
+                [](const BigInt& b) { return b.to_decimal(); });
+    for (std::size_t i = 0; i < n; ++i) {
+      const std::string& d = dec[i];
+      const bool neg = !d.empty() && d[0] == '-';
+      std::vector<std::uint64_t> mag(K + 1, 0);  // one spare limb detects overflow
+      for (std::size_t c = neg ? 1 : 0; c < d.size(); ++c) {
+        unsigned __int128 carry = static_cast<unsigned>(d[c] - '0');
+        for (auto& w : mag) {
+          const unsigned __int128 t = static_cast<unsigned __int128>(w) * 10 + carry;
+          w = static_cast<std::uint64_t>(t);
+          carry = t >> 64;
+        }
+      }
+      // |value| must be < 2^(64K-1) (or == 2^(64K-1) when negative)
+      const bool top_clear = mag[K] == 0 && (mag[K - 1] >> 63) == 0;
+      if (!top_clear) throw std::overflow_error("result does not fit the limb count");
+      if (neg) {  // two's complement
+        unsigned __int128 c = 1;
+        for (std::uint32_t k = 0; k < K; ++k) {
+          const unsigned __int128 t = static_cast<unsigned __int128>(~mag[k]) + c;
+          mag[k] = static_cast<std::uint64_t>(t);
+          c = t >> 64;
+        }
+      }
+      for (std::uint32_t k = 0; k < K; ++k) out[k * n + i] = mag[k];
+    }
+    return 0;
+  });
+}
+
 // evaluate_parallel (intra-point threading, eval.hpp:97-140) for `n` points
 int ref_eval_parallel_f64(void* h, const double* const* coords, std::size_t n, double* out,
                           unsigned workers) {

@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     evaluate_many,
     evaluate_parallel,
     launch_count,
+    limbs_to_int,
     scheme_from_name,
     threshold_combine,
 )
@@ -28,6 +29,7 @@ from ._lib import (  # noqa: F401
     DOMAIN_I64,
     DOMAIN_INTERVAL,
     DOMAIN_I64F,
+    DOMAIN_LIMBS,
     CudaError,
     LogicError,
     PolyEvalError,

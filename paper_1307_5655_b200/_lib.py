@@ -16,6 +16,11 @@ PE_OK, PE_EINVAL, PE_EOVERFLOW, PE_ECUDA, PE_ELOGIC = 0, 1, 2, 3, 4
 
 DOMAIN_F64, DOMAIN_F64_STRICT, DOMAIN_I64, DOMAIN_INTERVAL, DOMAIN_I64F = 0, 1, 2, 3, 4
 
+
+def DOMAIN_LIMBS(k: int) -> int:
+    """Domain code of the K-limb exact integer kernel (PE_DOMAIN_LIMBS)."""
+    return 0x100 | int(k)
+
 COEFF_F64, COEFF_I64 = 0, 1
 
 
@@ -112,6 +117,11 @@ EXPORTS = [
       C.POINTER(C.c_void_p), C.POINTER(pe_exec)]),
     ("pe_eval_i64", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_eval_limbs", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_uint32, C.POINTER(C.c_void_p),
+      C.POINTER(pe_exec)]),
+    ("pe_program_limbs_needed", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     ("pe_eval_interval", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p,
       C.c_void_p, C.POINTER(pe_exec)]),

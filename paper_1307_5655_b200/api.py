@@ -218,6 +218,14 @@ class CompiledProgram:
         self._h = h
         return self
 
+    def limbs_needed(self, bounds) -> int:
+        """Smallest K (1..8) of 64-bit limbs the overflow proof allows for
+        |x_v| <= bounds[v]; 0 if more than 8 would be needed."""
+        b = (C.c_uint64 * self.nvars)(*[int(x) for x in bounds])
+        k = C.c_uint32()
+        L.check(L.lib().pe_program_limbs_needed(self._h, b, C.byref(k)))
+        return k.value
+
     def info(self) -> dict:
         inf = L.pe_program_info_t()
         L.check(L.lib().pe_program_info(self._h, C.byref(inf)))
@@ -305,14 +313,18 @@ class IntervalDomain:
 
 
 class BigIntDomain:
-    """Exact integer domain on a host-proven int64 range.
+    """Exact integer domain on a host-proven range.
 
     By default the runtime evaluates on the FP64 FMA pipe whenever the host
     proves every intermediate stays below 2^53 (exact), else with int64
-    multiply-adds; int_pipe=True forces the int64 kernel."""
+    multiply-adds; int_pipe=True forces the int64 kernel. wide=True lifts the
+    int64 limit: values are carried in K 64-bit limbs (K = the smallest the
+    proof allows for the batch, up to 8 = 511-bit values) and evaluate()
+    returns Python ints (pe_eval_limbs)."""
 
-    def __init__(self, int_pipe: bool = False):
+    def __init__(self, int_pipe: bool = False, wide: bool = False):
         self.int_pipe = bool(int_pipe)
+        self.wide = bool(wide)
 
 
 def _is_torch_cuda(x) -> bool:
@@ -410,6 +422,9 @@ class Evaluator:
                                          self._ptr(out[1]), C.byref(ex)))
             return out
         integer = isinstance(self.domain, BigIntDomain)
+        if integer and self.domain.wide:
+            k, limbs = self.evaluate_limbs(points, stream=stream)
+            return limbs_to_int(limbs)
         cols, n = self._soa(points, np.int64 if integer else np.float64)
         dev = _is_torch_cuda(cols[0])
         if out is None:
@@ -419,6 +434,32 @@ class Evaluator:
         fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
         L.check(fn(self.program.handle, ptrs, n, self._ptr(out), C.byref(ex)))
         return out
+
+    def evaluate_limbs(self, points, limbs: int | None = None, stream=None):
+        """K-limb exact evaluation (pe_eval_limbs): returns (K, [K arrays of
+        uint64 words, little-endian two's complement]); K defaults to the
+        smallest the overflow proof allows for this batch's coordinates."""
+        cols, n = self._soa(points, np.int64)
+        dev = _is_torch_cuda(cols[0])
+        if limbs is None:
+            maxima = []
+            for c in cols:
+                if dev:
+                    maxima.append(int(c.abs().max().item()) if n else 0)
+                else:
+                    maxima.append(int(np.abs(c.astype(np.int64)).max()) if n else 0)
+            maxima = [min(m, 2**63) for m in maxima]
+            limbs = self.program.limbs_needed(maxima)
+            if limbs == 0:
+                raise OverflowError("values need more than 8 limbs (511 bits)")
+        outs = [Evaluator._alloc(n, "i64", dev, cols[0]) for _ in range(limbs)]
+        ptrs = (C.c_void_p * len(cols))(*[self._ptr(a) for a in cols])
+        optrs = (C.c_void_p * limbs)(*[self._ptr(o) for o in outs])
+        ex = self._exec(self._stream(stream, cols[0]))
+        L.check(L.lib().pe_eval_limbs(self.program.handle, ptrs, n, limbs, optrs, C.byref(ex)))
+        if not dev:
+            outs = [o.view(np.uint64) for o in outs]
+        return limbs, outs
 
     def enable_register_check(self, on: bool = True) -> None:
         """Reference Evaluator::enable_register_check (eval.hpp:142-145):
@@ -489,6 +530,21 @@ def evaluate_many(programs, points, outs=None, device: int = -1, stream=None, de
 def evaluate(program: CompiledProgram, points, domain):
     """One-shot convenience wrapper (reference eval.hpp:262-268)."""
     return Evaluator(domain, program).evaluate(points)
+
+
+def limbs_to_int(limbs) -> np.ndarray:
+    """K arrays of 64-bit words (little-endian two's complement) -> object
+    array of Python ints."""
+    host = [np.asarray(l.cpu() if hasattr(l, "cpu") else l).view(np.uint64) for l in limbs]
+    k = len(host)
+    out = np.empty(host[0].shape[0], dtype=object)
+    top = 1 << (64 * k)
+    for i in range(out.shape[0]):
+        v = 0
+        for j in range(k - 1, -1, -1):
+            v = (v << 64) | int(host[j][i])
+        out[i] = v - top if v >> (64 * k - 1) else v
+    return out
 
 
 def evaluate_parallel(program: CompiledProgram, points, domain, workers: int):

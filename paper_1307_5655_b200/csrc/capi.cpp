@@ -496,11 +496,17 @@ static lower::Domain to_domain(int32_t d) {
   return static_cast<lower::Domain>(d);
 }
 
+// domain codes 0..4, or PE_DOMAIN_LIMBS(K) = 0x100 | K for the K-limb kernel
+static const Artifact& artifact_for(const Program& p, int32_t domain, bool need_cubin) {
+  if (domain & 0x100) return p.limb_artifact(static_cast<std::uint32_t>(domain & 0xff), need_cubin);
+  return p.artifact(to_domain(domain), need_cubin);
+}
+
 pe_status pe_program_kernel_stats(const pe_program* program, int32_t domain, uint64_t* fp_ops,
                                   uint64_t* int_ops, uint64_t* ptx_bytes) {
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "null argument");
-    const Artifact& a = program->impl.artifact(to_domain(domain), false);
+    const Artifact& a = artifact_for(program->impl, domain, false);
     if (fp_ops) *fp_ops = a.image.fp_ops;
     if (int_ops) *int_ops = a.image.int_ops;
     if (ptx_bytes) *ptx_bytes = a.image.ptx.size();
@@ -512,7 +518,7 @@ pe_status pe_program_ptx(const pe_program* program, int32_t domain, char* out, s
                          size_t* len) {
   return guarded([&]() -> pe_status {
     if (!program || !len) return fail(PE_EINVAL, "null argument");
-    const Artifact& a = program->impl.artifact(to_domain(domain), false);
+    const Artifact& a = artifact_for(program->impl, domain, false);
     *len = a.image.ptx.size();
     if (out && cap) {
       const size_t k = std::min(cap - 1, a.image.ptx.size());
@@ -547,7 +553,7 @@ pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices) {
 pe_status pe_program_compile_only(const pe_program* program, int32_t domain, uint64_t* cubin_bytes) {
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "null argument");
-    const Artifact& a = program->impl.artifact(to_domain(domain), true);
+    const Artifact& a = artifact_for(program->impl, domain, true);
     if (cubin_bytes) *cubin_bytes = a.cubin.size();
     return PE_OK;
   });
@@ -738,6 +744,100 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
       // re-run with a list as large as the batch (cannot overflow)
     }
     return fail(PE_ELOGIC, "interval fixup list overflowed at full capacity");
+  });
+}
+
+// Per-variable max |x| of an int64 SoA batch (device reduction kernel or a
+// host loop).
+std::vector<std::uint64_t> batch_abs_max(const Program& p, const int64_t* const* coords, size_t n,
+                                         MemKind kind, int dev, cudaStream_t s) {
+  std::vector<std::uint64_t> actual(p.nvars, 0);
+  if (kind == MemKind::Device) {
+    unsigned long long* dmax = nullptr;
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dmax), 8 * p.nvars, s), "cudaMallocAsync");
+    check_cuda(cudaMemsetAsync(dmax, 0, 8 * p.nvars, s), "cudaMemsetAsync");
+    const int sms = device_ctx(dev).sms;
+    for (uint32_t v = 0; v < p.nvars; ++v) {
+      check_cuda(pe_launch_max_abs_i64(reinterpret_cast<const long long*>(coords[v]), n, dmax + v,
+                                       sms, s),
+                 "max_abs_i64");
+      launch_counter().fetch_add(1, std::memory_order_relaxed);
+    }
+    check_cuda(cudaMemcpyAsync(actual.data(), dmax, 8 * p.nvars, cudaMemcpyDeviceToHost, s), "D2H");
+    check_cuda(cudaFreeAsync(dmax, s), "cudaFreeAsync");
+    check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  } else {
+    for (uint32_t v = 0; v < p.nvars; ++v) {
+      std::uint64_t m = 0;
+      for (size_t i = 0; i < n; ++i) {
+        const int64_t x = coords[v][i];
+        m = std::max<std::uint64_t>(m, x < 0 ? 0ull - static_cast<std::uint64_t>(x) : static_cast<std::uint64_t>(x));
+      }
+      actual[v] = m;
+    }
+  }
+  return actual;
+}
+
+pe_status pe_program_limbs_needed(const pe_program* program, const uint64_t* bounds,
+                                  uint32_t* limbs) {
+  return guarded([&]() -> pe_status {
+    if (!program || !bounds || !limbs) return fail(PE_EINVAL, "null argument");
+    if (!program->impl.integer) return fail(PE_EINVAL, "multi-limb evaluation needs int64 coefficients");
+    *limbs = limbs_needed(program->impl, bounds);
+    return PE_OK;
+  });
+}
+
+pe_status pe_eval_limbs(const pe_program* program, const int64_t* const* coords, size_t n,
+                        uint32_t limbs, uint64_t* const* out_limbs, const pe_exec* exec) {
+  return guarded([&]() -> pe_status {
+    if (!program) return fail(PE_EINVAL, "program is null");
+    const Program& p = program->impl;
+    if (!p.integer) return fail(PE_EINVAL, "pe_eval_limbs needs a program with int64 coefficients");
+    if (limbs < 1 || limbs > 8) return fail(PE_EINVAL, "limbs must be 1..8");
+    if (n == 0) return PE_OK;
+    if (!coords || !out_limbs) return fail(PE_EINVAL, "null buffer");
+    for (uint32_t v = 0; v < p.nvars; ++v) {
+      if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
+    }
+    for (uint32_t k = 0; k < limbs; ++k) {
+      if (!out_limbs[k]) return fail(PE_EINVAL, "null output limb array");
+    }
+    if (multi_device(exec)) {
+      return across_devices(*exec, n, out_limbs[0], [&](const pe_exec& e, size_t lo, size_t cnt) {
+        std::vector<const int64_t*> c(p.nvars);
+        for (uint32_t v = 0; v < p.nvars; ++v) c[v] = coords[v] + lo;
+        std::vector<uint64_t*> o(limbs);
+        for (uint32_t k = 0; k < limbs; ++k) o[k] = out_limbs[k] + lo;
+        return pe_eval_limbs(program, c.data(), cnt, limbs, o.data(), &e);
+      });
+    }
+    MemKind kind;
+    const int dev = resolve_device(exec, out_limbs[0], &kind);
+    check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    // the batch's own maxima: the proof then covers exactly these points and
+    // the kernel's per-point bound check cannot fire
+    const std::vector<std::uint64_t> bounds =
+        exec && exec->i64_bounds
+            ? std::vector<std::uint64_t>(exec->i64_bounds, exec->i64_bounds + p.nvars)
+            : batch_abs_max(p, coords, n, kind, dev, s);
+    const std::uint32_t need = limbs_needed(p, bounds.data());
+    if (need == 0 || need > limbs) {
+      return fail(PE_EOVERFLOW, "values need " + (need ? std::to_string(need) : std::string("> 8")) +
+                                    " limbs for these coordinates");
+    }
+    const Artifact& a = p.loaded_limbs(limbs, dev);
+    std::vector<const void*> ins(coords, coords + p.nvars);
+    std::vector<void*> outs(out_limbs, out_limbs + limbs);
+    Flag flag(s);
+    LaunchArgs la;
+    la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
+    la.bounds = bounds;
+    run_batch(a, dev, kind, n, ins, outs, la, s, false);
+    if (flag.read() != 0) return fail(PE_EOVERFLOW, "a coordinate exceeds the asserted bound");
+    return PE_OK;
   });
 }
 

@@ -39,6 +39,7 @@ const char* domain_name(Domain d) {
     case Domain::I64: return "i64";
     case Domain::Interval: return "interval";
     case Domain::I64F: return "i64f";
+    case Domain::I64K: return "i64k";
   }
   return "?";
 }
@@ -57,6 +58,8 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   // (profiles/r1_imm_sweep.txt).
   if (d == Domain::Interval) {
     s = {1, 512, 32, 0};  // integer-pipe bound; no coefficient pressure
+  } else if (d == Domain::I64K) {
+    s = {1, 256, 0, 0};   // K-limb registers: one point per thread
   } else if (powers > 32) {
     // very wide programs (large power tables): registers are the limit
     s = {1, 512, 0, 2};
@@ -188,8 +191,10 @@ class Emitter {
  public:
   Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
-        imm_mode_(shape.imm_mode), accumulate_(shape.accumulate) {
+        imm_mode_(shape.imm_mode), accumulate_(shape.accumulate),
+        K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1) {
     if (accumulate_ && d_ != Domain::F64) throw std::logic_error("accumulate is fp64-only");
+    if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
 
   KernelImage run() {
@@ -199,9 +204,10 @@ class Emitter {
     img.lanes = P_;
     img.block = block_;
     const bool iv = d_ == Domain::Interval;
-    const bool i64 = d_ == Domain::I64 || d_ == Domain::I64F;
+    const bool i64 = d_ == Domain::I64 || d_ == Domain::I64F || d_ == Domain::I64K;
     img.n_in = iv ? 2 * s_.nvars : s_.nvars;
-    img.n_out = iv ? 2 : 1;
+    img.n_out = iv ? 2 : K_;
+    img.limbs = K_;
     img.has_flag = iv || i64;
     img.has_bounds = i64;
     if ((d_ == Domain::F64Strict || d_ == Domain::Interval) && !s_.strict) {
@@ -356,12 +362,12 @@ class Emitter {
         const IvCoef c = ivcoef(k);
         coef_lo_[k] = word(bits_of(c.lo));
         coef_hi_[k] = word(bits_of(c.hi));
-      } else if (d_ == Domain::I64 || d_ == Domain::I64F) {
+      } else if (d_ == Domain::I64 || d_ == Domain::I64F || d_ == Domain::I64K) {
         std::uint64_t w;
         if constexpr (std::is_same_v<C, std::int64_t>) {
           // I64F: |c| <= M < 2^53 by the host proof, so the double is exact
-          w = d_ == Domain::I64 ? static_cast<std::uint64_t>(s_.coefs[k])
-                                : bits_of(static_cast<double>(s_.coefs[k]));
+          w = d_ != Domain::I64F ? static_cast<std::uint64_t>(s_.coefs[k])
+                                 : bits_of(static_cast<double>(s_.coefs[k]));
         } else {
           throw std::invalid_argument("int64 domain needs integer coefficients");
         }
@@ -405,10 +411,11 @@ class Emitter {
     return true;
   }
 
-  const char* ldty() const { return d_ == Domain::I64 ? "b64" : "f64"; }
-  const char* rty() const { return d_ == Domain::I64 ? "s64" : "f64"; }
+  bool intk() const { return d_ == Domain::I64 || d_ == Domain::I64K; }
+  const char* ldty() const { return intk() ? "b64" : "f64"; }
+  const char* rty() const { return intk() ? "s64" : "f64"; }
   // coordinates and results in memory
-  bool int_io() const { return d_ == Domain::I64 || d_ == Domain::I64F; }
+  bool int_io() const { return d_ == Domain::I64 || d_ == Domain::I64F || d_ == Domain::I64K; }
   const char* ioty() const { return int_io() ? "b64" : "f64"; }
   static std::string ln(std::uint32_t lane) { return "_" + std::to_string(lane); }
 
@@ -451,9 +458,11 @@ class Emitter {
   }
   // integer coordinate as loaded (I64: the arithmetic register itself)
   std::string xi(std::uint32_t v, std::uint32_t lane) const {
-    if (d_ == Domain::I64F) return "%xi" + std::to_string(v) + ln(lane);
+    if (d_ == Domain::I64F || d_ == Domain::I64K) return "%xi" + std::to_string(v) + ln(lane);
     return xr(v, lane);
   }
+  // I64K: limb j of a K-limb register name
+  static std::string lb(const std::string& r, std::uint32_t j) { return r + "_l" + std::to_string(j); }
 
   // Coefficients are loaded once per op (before the lane loop) and shared.
   struct Loaded {
@@ -514,6 +523,9 @@ class Emitter {
           decls_ << "  .reg .f64 " << xr(v, k, false) << ", " << xr(v, k, true) << ";\n";
         } else if (d_ == Domain::I64F) {
           decls_ << "  .reg .f64 " << xr(v, k) << ";\n  .reg .b64 " << xi(v, k) << ";\n";
+        } else if (d_ == Domain::I64K) {
+          decls_ << "  .reg .b64 " << xi(v, k) << ";\n";
+          for (std::uint32_t j = 0; j < K_; ++j) decls_ << "  .reg .b64 " << lb(xr(v, k), j) << ";\n";
         } else {
           decls_ << "  .reg ." << ldty() << " " << xr(v, k) << ";\n";
         }
@@ -529,6 +541,11 @@ class Emitter {
         if (d_ == Domain::I64F) {
           // exact: |x| <= bound < 2^53 is checked below before any result is used
           body_ << "  cvt.rn.f64.s64 " << xr(i, k) << ", " << xi(i, k) << ";\n";
+        } else if (d_ == Domain::I64K) {  // sign-extend to K limbs
+          body_ << "  mov.b64 " << lb(xr(i, k), 0) << ", " << xi(i, k) << ";\n";
+          for (std::uint32_t j = 1; j < K_; ++j) {
+            body_ << "  shr.s64 " << lb(xr(i, k), j) << ", " << xi(i, k) << ", 63;\n";
+          }
         }
       }
     }
@@ -567,6 +584,8 @@ class Emitter {
       for (std::uint32_t k = 0; k < P_; ++k) {
         if (d_ == Domain::Interval) {
           decls_ << "  .reg .f64 " << pw(id, k, false) << ", " << pw(id, k, true) << ";\n";
+        } else if (d_ == Domain::I64K) {
+          for (std::uint32_t j = 0; j < K_; ++j) decls_ << "  .reg .b64 " << lb(pw(id, k), j) << ";\n";
         } else {
           decls_ << "  .reg ." << rty() << " " << pw(id, k) << ";\n";
         }
@@ -586,6 +605,10 @@ class Emitter {
               fcheck_finite(pw(id, k, false));
               fcheck_finite(pw(id, k, true));
             }
+          } else if (d_ == Domain::I64K) {
+            for (std::uint32_t j = 0; j < K_; ++j) {
+              body_ << "  mov.b64 " << lb(pw(id, k), j) << ", " << lb(xr(p.var, k), j) << ";\n";
+            }
           } else {
             body_ << "  mov." << ldty() << " " << pw(id, k) << ", " << xr(p.var, k) << ";\n";
           }
@@ -603,6 +626,9 @@ class Emitter {
         } else if (d_ == Domain::Interval) {
           iv_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
                  {pw(p.hi, k, false), pw(p.hi, k, true)}, k == 0);
+        } else if (d_ == Domain::I64K) {
+          kmul(limbs_of(pw(id, k)), limbs_of(pw(p.lo, k)), limbs_of(pw(p.hi, k)));
+          if (k == 0) ++int_ops_;
         } else if (d_ == Domain::I64) {
           body_ << "  mul.lo.s64 " << pw(id, k) << ", " << pw(p.lo, k) << ", " << pw(p.hi, k) << ";\n";
           if (k == 0) ++int_ops_;
@@ -622,11 +648,13 @@ class Emitter {
     for (std::uint32_t id = 0; id < s_.nregs; ++id) {
       std::ostringstream line;
       line << "  .reg .f64 ";
-      if (d_ == Domain::I64) line.str("  .reg .s64 ");
+      if (intk()) line.str("  .reg .s64 ");
       line.seekp(0, std::ios_base::end);
       for (std::uint32_t k = 0; k < P_; ++k) {
         if (d_ == Domain::Interval) {
           line << (k ? ", " : "") << reg(id, k, false) << ", " << reg(id, k, true);
+        } else if (d_ == Domain::I64K) {
+          for (std::uint32_t j = 0; j < K_; ++j) line << (k || j ? ", " : "") << lb(reg(id, k), j);
         } else {
           line << (k ? ", " : "") << reg(id, k);
         }
@@ -729,7 +757,117 @@ class Emitter {
     (d_ == Domain::I64 ? int_ops_ : fp_ops_) += L;
   }
 
+  // ---------------- K-limb exact integers (Domain::I64K) ----------------
+  // Values are K 64-bit limbs, two's complement, little-endian; arithmetic is
+  // mod 2^(64K), which equals exact integer arithmetic because the host proof
+  // bounds every intermediate below 2^(64K-1) in magnitude.
+  std::vector<std::string> limbs_of(const std::string& r) const {
+    std::vector<std::string> v;
+    for (std::uint32_t j = 0; j < K_; ++j) v.push_back(lb(r, j));
+    return v;
+  }
+
+  // Limbs of an operand; a coefficient is its int64 word, sign-extended by
+  // immediates (0 / all ones).
+  std::vector<std::string> opl(const Operand& o, const Loaded& l, std::uint32_t lane) const {
+    switch (o.kind) {
+      case Operand::Reg: return limbs_of(reg(o.id, lane));
+      case Operand::Pow: return limbs_of(pw(o.id, lane));
+      case Operand::Coef: {
+        std::vector<std::string> v{l.lo};
+        std::int64_t c = 0;
+        if constexpr (std::is_same_v<C, std::int64_t>) c = s_.coefs[o.id];
+        for (std::uint32_t j = 1; j < K_; ++j) v.push_back(c < 0 ? "-1" : "0");
+        return v;
+      }
+      case Operand::Zero: return std::vector<std::string>(K_, "0");
+      default: throw std::logic_error("bad operand");
+    }
+  }
+
+  std::string reg_of(const std::string& x) {
+    if (x.rfind('%', 0) == 0) return x;
+    const std::string t = tmp_u();
+    body_ << "  mov.b64 " << t << ", " << x << ";\n";
+    return t;
+  }
+
+  // r = a + b (carry chain)
+  void kadd(const std::vector<std::string>& r, const std::vector<std::string>& a,
+            const std::vector<std::string>& b) {
+    if (K_ == 1) {
+      body_ << "  add.u64 " << r[0] << ", " << reg_of(a[0]) << ", " << b[0] << ";\n";
+      return;
+    }
+    for (std::uint32_t j = 0; j < K_; ++j) {
+      const char* op = j == 0 ? "add.cc" : (j + 1 < K_ ? "addc.cc" : "addc");
+      body_ << "  " << op << ".u64 " << r[j] << ", " << reg_of(a[j]) << ", " << b[j] << ";\n";
+    }
+  }
+
+  // One multiply-add carry chain: r[base + t] += half(a_i * b[t]) for t in [0, len).
+  void mad_chain(const char* half, const std::vector<std::string>& r, std::uint32_t base,
+                 const std::string& ai, const std::vector<std::string>& b, std::uint32_t len) {
+    for (std::uint32_t t = 0; t < len; ++t) {
+      std::string op = (t == 0 ? "mad." : "madc.") + std::string(half);
+      if (t + 1 < len) op += ".cc";
+      body_ << "  " << op << ".u64 " << r[base + t] << ", " << ai << ", " << reg_of(b[t]) << ", "
+            << r[base + t] << ";\n";
+    }
+  }
+
+  // r = a * b mod 2^(64K): truncated schoolbook, row i adds a_i * b shifted by
+  // i limbs (low halves, then high halves, each one carry chain). A
+  // coefficient operand goes in `a`, whose zero high limbs skip their rows.
+  void kmul(const std::vector<std::string>& r, std::vector<std::string> a,
+            std::vector<std::string> b) {
+    if (a[0].rfind('%', 0) == 0 && a.size() > 1 && a[1].rfind('%', 0) == 0 &&
+        !(b.size() > 1 && b[1].rfind('%', 0) == 0)) {
+      std::swap(a, b);  // immediate-limbed operand (coefficient) first
+    }
+    const std::string a0 = reg_of(a[0]);
+    for (std::uint32_t j = 0; j < K_; ++j) {
+      body_ << "  mul.lo.u64 " << r[j] << ", " << a0 << ", " << reg_of(b[j]) << ";\n";
+    }
+    if (K_ > 1) mad_chain("hi", r, 1, a0, b, K_ - 1);
+    for (std::uint32_t i = 1; i < K_; ++i) {
+      if (a[i] == "0") continue;
+      const std::string ai = reg_of(a[i]);
+      mad_chain("lo", r, i, ai, b, K_ - i);
+      if (K_ - i > 1) mad_chain("hi", r, i + 1, ai, b, K_ - i - 1);
+    }
+  }
+
+  void emit_limb_op(const Op& op) {
+    const Loaded la = load(op.a), lbd = load(op.b), lc = load(op.c);
+    for (std::uint32_t k = 0; k < P_; ++k) {
+      const auto d = limbs_of(reg(op.dst, k));
+      const auto A = opl(op.a, la, k), B = opl(op.b, lbd, k);
+      switch (op.kind) {
+        case OpKind::Add:
+          if (op.a.is(Operand::Zero)) {
+            for (std::uint32_t j = 0; j < K_; ++j) body_ << "  mov.b64 " << d[j] << ", " << B[j] << ";\n";
+          } else {
+            kadd(d, A, B);
+          }
+          break;
+        case OpKind::Mul:
+          kmul(d, A, B);
+          break;
+        case OpKind::Fma:
+          kmul(d, A, B);
+          kadd(d, d, opl(op.c, lc, k));
+          break;
+      }
+      if (k == 0) ++int_ops_;
+    }
+  }
+
   void emit_scalar_op(const Op& op) {
+    if (d_ == Domain::I64K) {
+      emit_limb_op(op);
+      return;
+    }
     const Loaded la = load(op.a), lb = load(op.b), lc = load(op.c);
     for (std::uint32_t k = 0; k < P_; ++k) {
       const std::string d = reg(op.dst, k);
@@ -1164,6 +1302,17 @@ class Emitter {
   void emit_store() {
     const bool iv = d_ == Domain::Interval;
     const Loaded lr = load(s_.result);
+    if (d_ == Domain::I64K) {
+      for (std::uint32_t j = 0; j < K_; ++j) {
+        body_ << "  ld.param.u64 %rd9, [pe_out" << j << "];\n  cvta.to.global.u64 %rd9, %rd9;\n";
+        for (std::uint32_t k = 0; k < P_; ++k) {
+          const std::string v = reg_of(opl(s_.result, lr, k)[j]);
+          body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  @%pv" << k << " st.global.b64 [%rd10], "
+                << v << ";\n";
+        }
+      }
+      return;
+    }
     for (std::uint32_t o = 0; o < (iv ? 2u : 1u); ++o) {
       body_ << "  ld.param.u64 %rd9, [pe_out" << o << "];\n  cvta.to.global.u64 %rd9, %rd9;\n";
       for (std::uint32_t k = 0; k < P_; ++k) {
@@ -1203,6 +1352,7 @@ class Emitter {
   std::uint32_t sync_every_;
   std::uint32_t imm_mode_;
   bool accumulate_ = false;
+  std::uint32_t K_ = 1;  // I64K limbs
   bool fast_ = false;  // emitting the interval fast path
   bool fix_ = false;   // emitting the fixup entry
   // fast-path nextafter on the FP64 pipe (default) or as integer +-1 with
@@ -1267,6 +1417,7 @@ KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape) 
   if (shape.block == 0) shape.block = def.block;
   if (shape.sync_every == 0) shape.sync_every = def.sync_every;
   if (shape.imm_mode == 0) shape.imm_mode = def.imm_mode;
+  if (shape.limbs == 0) shape.limbs = 1;
   Emitter<C> e(stream, domain, shape);
   return e.run();
 }

@@ -21,6 +21,9 @@ enum class Domain : int {
                   // integer results, computed on the FP64 FMA pipe (every
                   // intermediate is an integer of magnitude < 2^53, hence a
                   // double, hence every DFMA/DMUL is exact)
+  I64K = 5,       // BigIntDomain on a range proven below 2^(64K-1): K-limb
+                  // two's-complement integers (KernelShape::limbs), carry-chain
+                  // multiply-adds mod 2^(64K) — exact by the proof
 };
 
 const char* domain_name(Domain d);
@@ -49,6 +52,7 @@ struct KernelImage {
   std::uint32_t block = 128;
   std::uint32_t lanes = 1;         // points per thread (tile = block * lanes)
   bool interval_fast_path = false; // fast exact path + fixup entry (strict replay)
+  std::uint32_t limbs = 1;         // I64K: 64-bit words per value (= result arrays)
   std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
   // instruction counts per point (roofline bookkeeping)
@@ -75,6 +79,8 @@ struct KernelShape {
   // fp64 slices of a wide program: add the slice value into the result
   // instead of storing it (out[i] += v)
   bool accumulate = false;
+  // I64K: 64-bit limbs per value (1..8)
+  std::uint32_t limbs = 0;
 };
 
 /// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC

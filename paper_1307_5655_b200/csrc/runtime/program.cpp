@@ -4,6 +4,7 @@
 #include "runtime/program.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <future>
 #include <memory>
@@ -140,6 +141,58 @@ Artifact& Program::loaded(lower::Domain d, int device) const {
   std::lock_guard<std::mutex> lock(mu);
   ensure_loaded(a, device);
   return a;
+}
+
+Artifact& Program::limb_artifact(std::uint32_t limbs, bool need_cubin) const {
+  if (!integer) throw std::invalid_argument("multi-limb evaluation needs int64 coefficients");
+  if (limbs < 1 || limbs > 8) throw std::invalid_argument("limbs must be 1..8");
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = limb_arts[limbs];
+  if (!slot) {
+    slot = std::make_unique<Artifact>();
+    lower::KernelShape shape;
+    shape.limbs = limbs;
+    slot->image = lower::emit_ptx(lower::lower_fused(*prog_i), lower::Domain::I64K, shape);
+  }
+  if (need_cubin && slot->cubin.empty()) {
+    CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);
+    if (!r.ok) throw std::logic_error(r.log);
+    slot->cubin = std::move(r.cubin);
+    slot->compile_seconds = r.seconds;
+  }
+  return *slot;
+}
+
+Artifact& Program::loaded_limbs(std::uint32_t limbs, int device) const {
+  Artifact& a = limb_artifact(limbs, true);
+  std::lock_guard<std::mutex> lock(mu);
+  ensure_loaded(a, device);
+  return a;
+}
+
+std::uint32_t limbs_needed(const Program& p, const std::uint64_t* bounds) {
+  if (p.terms_i.empty()) return 1;
+  std::vector<double> lx(p.nvars);
+  for (std::uint32_t v = 0; v < p.nvars; ++v) {
+    lx[v] = std::log2(std::max<double>(1.0, static_cast<double>(bounds[v])));
+  }
+  double worst = 0.0, max_pow = 0.0;
+  for (const auto& t : p.terms_i) {
+    const double c = std::fabs(static_cast<double>(t.coefficient));
+    double bits = c > 0 ? std::log2(c) : 0.0;
+    for (std::uint32_t v = 0; v < p.nvars; ++v) {
+      bits += t.exponents[v] * lx[v];
+      max_pow = std::max(max_pow, t.exponents[v] * lx[v]);
+    }
+    worst = std::max(worst, bits);
+  }
+  // M <= T * max term; 1e-6 relative + 1 bit of slack for log2 rounding
+  const double need = std::max(worst + std::log2(static_cast<double>(p.terms_i.size())), max_pow) *
+                          (1 + 1e-6) + 1.0;
+  for (std::uint32_t k = 1; k <= 8; ++k) {
+    if (need < 64.0 * k - 1.0) return k;
+  }
+  return 0;
 }
 
 std::size_t Program::slice_count() const {

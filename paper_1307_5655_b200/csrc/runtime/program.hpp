@@ -64,6 +64,7 @@ struct Program {
 
   mutable std::mutex mu;
   mutable std::array<std::unique_ptr<Artifact>, 5> artifacts;
+  mutable std::map<std::uint32_t, std::unique_ptr<Artifact>> limb_arts;  // I64K by limb count
 
   /// Generated (and compiled) artifact for a domain; thread-safe.
   Artifact& artifact(lower::Domain d, bool need_cubin) const;
@@ -73,7 +74,16 @@ struct Program {
   /// its slices for wide programs.
   std::vector<const Artifact*> f64_kernels(int device) const;
   std::size_t slice_count() const;
+  /// K-limb exact integer kernel (Domain::I64K): generated (+ compiled), or
+  /// loaded on `device`.
+  Artifact& limb_artifact(std::uint32_t limbs, bool need_cubin) const;
+  Artifact& loaded_limbs(std::uint32_t limbs, int device) const;
 };
+
+/// Smallest K (1..8) with every intermediate provably below 2^(64K-1) for
+/// |x_v| <= bounds[v] (log-domain bound: M <= T * max_t |c_t| prod X_v^a_tv,
+/// with a safety margin); 0 if none.
+std::uint32_t limbs_needed(const Program& p, const std::uint64_t* bounds);
 
 /// Overflow proof for the exact int64 path: every intermediate of the walk
 /// (fused or strict) is a partial sum of terms c_t * prod x_v^(a_tv - s_v),
