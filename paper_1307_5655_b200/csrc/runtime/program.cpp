@@ -278,6 +278,7 @@ std::vector<const Artifact*> Program::f64_kernels(int device) const {
 
 namespace {
 void ensure_loaded(Artifact& a, int device) {
+  if (a.library) bind_functions(a, device);
   if (!a.library) {
     check_cuda(cudaLibraryLoadData(&a.library, a.cubin.data(), nullptr, nullptr, 0, nullptr,
                                    nullptr, 0),
@@ -288,6 +289,7 @@ void ensure_loaded(Artifact& a, int device) {
       check_cuda(cudaLibraryGetKernel(&a.fix_kernel, a.library, a.image.fix_entry.c_str()),
                  "cudaLibraryGetKernel(fix)");
     }
+    bind_functions(a, device);
   }
   if (!a.image.global_words.empty() && !a.global_coefs.count(device)) {
     void* p = nullptr;

@@ -33,7 +33,16 @@ struct Artifact {
   cudaKernel_t kernel = nullptr;
   cudaKernel_t fix_kernel = nullptr;  // interval fast path: strict replay of listed points
   std::map<int, void*> global_coefs;  // per device: global-tier coefficient words
+  // per device ordinal: CUfunction of kernel / fix_kernel in that device's
+  // primary context (driver-API launches skip the runtime's per-launch
+  // library-kernel lookup); written once under the program mutex
+  static constexpr int kMaxDevices = 64;
+  std::array<void*, kMaxDevices> fn{};
+  std::array<void*, kMaxDevices> fix_fn{};
 };
+
+/// Resolves a.fn / a.fix_fn for `device` (current device = `device`).
+void bind_functions(Artifact& a, int device);
 
 struct Program {
   std::uint32_t nvars = 0;
