@@ -122,29 +122,41 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- ncu
 
-NCU_CAPTURES = {  # committed `ncu --set full` captures of the dominant kernels
+# committed `ncu --set full` captures of the dominant kernels, taken with the
+# bench's own per-launch sizes (scripts/gpu_full_round.sh); a capture with
+# several rows (C4: the slice kernels of one evaluate call) is summed
+NCU_CAPTURES = {
     ("c2", "C2_estrin_d1000"): "profiles/r1_ncu_c2_estrin_d1000_raw.csv",
     ("c2", "C2_balanced_d1000"): "profiles/r1_ncu_c2_balanced_d1000_raw.csv",
     ("c2", "C2_estrin_d1023"): "profiles/r1_ncu_c2_estrin_d1023_raw.csv",
     ("c2", "C2_balanced_d1023"): "profiles/r1_ncu_c2_balanced_d1023_raw.csv",
+    ("c1", "C1_horner_d1000"): "profiles/r1_ncu_c1_raw.csv",
+    ("c3", "C3_bivariate_td40_i64"): "profiles/r1_ncu_c3_raw.csv",
+    ("c4", "C4_trivariate_sparse10k"): "profiles/r1_ncu_c4_raw.csv",
+    ("c5", "C5_interval_estrin_d200"): "profiles/r1_ncu_c5_raw.csv",
 }
 
 
-def ncu_traffic(cfg, program):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed ncu capture of this kernel (None when not captured)."""
+def ncu_traffic(cfg, program, points):
+    """(dram__bytes_read.sum + dram__bytes_write.sum per launch, source) from
+    the committed ncu capture of this kernel; None when there is no capture
+    at this launch size."""
     import csv
     path = NCU_CAPTURES.get((cfg, program))
     if not path or not os.path.exists(os.path.join(ROOT, path)):
-        return None
+        return None, None
     rows = list(csv.reader(open(os.path.join(ROOT, path))))
-    head, units, vals = rows[0], rows[1], rows[2]
+    head, units = rows[0], rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total = 0.0
-    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        i = head.index(name)
-        total += float(vals[i]) * scale.get(units[i], 1)
-    return {"bytes_per_launch": total, "source": path}
+    for vals in rows[2:]:
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = head.index(name)
+            total += float(vals[i]) * scale.get(units[i], 1)
+    meta = os.path.join(ROOT, path.replace("_raw.csv", "_points.txt"))
+    if os.path.exists(meta) and int(open(meta).read().split()[0]) != points:
+        return None, f"{path} captured at a different size"
+    return total, path
 
 
 # ----------------------------------------------------------------- dist
@@ -406,23 +418,33 @@ def run_native(args, world, rank, local):
     else:
         algo_per_pt = 2 * info["walk_adds"] + 4 * (info["walk_muls"] + info["power_muls"])
         unit_ops = "fp64 add/mul (interval endpoints)"
-    achieved = algo_per_pt * n / (avg[top] * 1e-3)  # ops/s
+    achieved = algo_per_pt * n / (avg[top] * 1e-3)  # FP64-pipe ops/s (or int64 MAD/s)
     nominal = sms.value * 64 * 1.965e9
+    fp_pipe = domain != "i64" or int_tier == "fp64-exact"
+    # FLOP accounting: a DFMA is 2 FLOP, an interval endpoint add/mul 1; the
+    # FP64 pipe issues one of either per lane per clock, so the peak FLOP
+    # rate is 2x (FMA code) or 1x (add/mul code) the measured DFMA rate
+    flop_per_op = 1.0 if domain == "interval" else 2.0
+    traffic, traffic_src = ncu_traffic(args.config, wls[top].name, n)
     roofline = {
-        "bound": "fp64" if (domain != "i64" or int_tier == "fp64-exact") else "int64_mad",
+        "bound": "fp64" if fp_pipe else "int64_mad",
         "int64_tier": int_tier if domain == "i64" else None,
         "frac_vs_int64_mad_peak": (achieved / int_peak.value) if domain == "i64" else None,
-        "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "Tops/s",
+        "achieved": (achieved * flop_per_op / 1e12) if fp_pipe else achieved / 1e12,
+        "peak": (peak.value * flop_per_op / 1e12) if fp_pipe else peak.value / 1e12,
+        "unit": "TFLOP/s" if fp_pipe else "T int64-MAD/s",
         "frac": achieved / peak.value,
+        "achieved_pipe_ops_per_s": achieved, "peak_pipe_ops_per_s": peak.value,
         "peak_source": "measured live: pe_measure_peak microbenchmark (8 independent chains/thread, "
                        "full occupancy) on this GPU; nominal FP64 FMA pipe = "
-                       f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes",
+                       f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes "
+                       "(MEASURED_PEAKS.json has no FP64 entry)",
         "ops": f"{algo_per_pt} {unit_ops} per point (SURVEY 8d F) x {n} points per launch",
         "kernel": f"pe_walk_{domain} [{wls[top].name}]",
         "issued_fp64_per_point": st["fp_ops"], "issued_int64_per_point": st["int_ops"],
         "hbm_frac": (bytes_in + bytes_out) / (avg[top] * 1e-3) / 1e9 /
                     json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else None,
-        "traffic": ncu_traffic(args.config, wls[top].name),
+        "traffic": traffic, "traffic_source": traffic_src,
         "algorithmic_bytes_per_launch": bytes_in + bytes_out,
         "per_program_ms": {w.name: round(a, 4) for w, a in zip(wls, avg)},
     }
