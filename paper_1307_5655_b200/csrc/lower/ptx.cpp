@@ -70,6 +70,10 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   } else {
     s = {4, 256, 0, 2};
   }
+  // strict fp64 keeps every reference add: more live temporaries; a 512-wide
+  // CTA caps ptxas at 128 registers so two CTAs fit an SM (C2 balanced d1000
+  // strict: 174 registers at 256 wide, 2.54 -> 1.46 ms per 1e7 points)
+  if (d == Domain::F64Strict && s.block < 512) s.block = 512;
   auto env = [](const char* name, std::uint32_t lo, std::uint32_t hi, std::uint32_t& out) {
     if (const char* e = std::getenv(name)) {
       const long v = std::atol(e);
