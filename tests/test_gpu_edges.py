@@ -442,3 +442,29 @@ def test_evaluate_parallel_and_register_check(cuda_device):
         assert np.array_equal(a.view(np.int64), b.view(np.int64))
     c = pe.evaluate_parallel(prog, pts, pe.DoubleDomain(strict=True), 4)
     assert np.array_equal(a.view(np.int64), c.view(np.int64))
+
+
+def test_chain_loops_inside_nested_programs(cuda_device):
+    # bivariate Hörner: each y-program is a 150-step chain (a loop), nested
+    # inside the x-chain; f64 fused within tolerance, strict bit-exact, and
+    # the int64 domain exact
+    rng = np.random.default_rng(77)
+    ex = np.array([(i, j) for i in range(4) for j in range(151)], dtype=np.uint32)
+    schemes = [pe.builtin_scheme("horner")] * 2
+    pf = pe.Polynomial(ex, rng.uniform(-1, 1, len(ex)), ("x", "y"))
+    prog = pe.compile(pf, schemes)
+    assert prog.ptx(pe.DOMAIN_F64).count("bra.uni $Lrun") == 4
+    x = [rng.uniform(-1, 1, 5003), rng.uniform(-1, 1, 5003)]
+    orc = pyoracle.Oracle(pf, schemes)
+    ref = orc.eval_f64(x)
+    got = pe.Evaluator(pe.DoubleDomain(), prog).evaluate([_t(a, cuda_device) for a in x]).cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 1e-12 * pyoracle.abs_term_sum(pf, x))
+    pi = pe.Polynomial(ex, rng.choice([-3, -1, 1, 2, 5], len(ex)).astype(np.int64), ("x", "y"))
+    prog_i = pe.compile(pi, schemes)
+    assert "$Lrun" in prog_i.ptx(pe.DOMAIN_I64)
+    xi = [rng.integers(-1, 2, 5003).astype(np.int64) for _ in range(2)]
+    want = pyoracle.Oracle(pi, schemes).eval_i64(xi)
+    for int_pipe in (False, True):
+        got = pe.Evaluator(pe.BigIntDomain(int_pipe=int_pipe), prog_i).evaluate(
+            [_t(a, cuda_device) for a in xi]).cpu().numpy()
+        assert np.array_equal(got, want)
