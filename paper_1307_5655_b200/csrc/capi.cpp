@@ -30,6 +30,9 @@ extern "C" cudaError_t pe_launch_max_abs_i64(const long long* x, size_t n,
                                              unsigned long long* out, int sms,
                                              cudaStream_t stream);
 extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s);
+extern "C" cudaError_t pe_launch_narrow_limbs(const unsigned long long* const* limbs, int k,
+                                              size_t n, long long* out, unsigned* flag, int sms,
+                                              cudaStream_t stream);
 extern "C" cudaError_t pe_measure_dfma_latency(double* cycles_per_op);
 
 struct pe_program {
@@ -942,8 +945,55 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
       if (!i64_proof_holds(p, actual.data())) break;
       bounds = actual;
     }
-    return fail(PE_EOVERFLOW,
-                "int64 evaluation could overflow for these coordinates (no CPU fallback)");
+    if (caller_bounds) {
+      return fail(PE_EOVERFLOW, "a coordinate exceeds the asserted int64 bound");
+    }
+    // Tier 3: intermediates may leave int64, results may still fit: evaluate
+    // in K 64-bit limbs (exact, the batch's own maxima) and narrow, flagging
+    // results that do not fit (the reference's int64 conversion fails there).
+    const std::vector<std::uint64_t> actual = batch_abs_max(p, coords, n, kind, dev, s);
+    const std::uint32_t K = limbs_needed(p, actual.data());
+    if (K == 0) {
+      return fail(PE_EOVERFLOW, "intermediates exceed 511 bits for these coordinates");
+    }
+    const Artifact& ak = p.loaded_limbs(K, dev);
+    std::vector<void*> limbs(K, nullptr);
+    std::vector<std::vector<std::uint64_t>> host_limbs;
+    if (kind == MemKind::Device) {
+      for (auto& l : limbs) check_cuda(cudaMallocAsync(&l, 8 * n, s), "cudaMallocAsync(limbs)");
+    } else {
+      host_limbs.assign(K, std::vector<std::uint64_t>(n));
+      for (std::uint32_t k = 0; k < K; ++k) limbs[k] = host_limbs[k].data();
+    }
+    Flag flag(s);
+    LaunchArgs la;
+    la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
+    la.bounds = actual;
+    run_batch(ak, dev, kind, n, ins, limbs, la, s, false);
+    bool fits = true;
+    if (kind == MemKind::Device) {
+      std::vector<const unsigned long long*> lp(K);
+      for (std::uint32_t k = 0; k < K; ++k) lp[k] = static_cast<const unsigned long long*>(limbs[k]);
+      check_cuda(pe_launch_narrow_limbs(lp.data(), static_cast<int>(K), n,
+                                        reinterpret_cast<long long*>(out), flag.dev,
+                                        device_ctx(dev).sms, s),
+                 "narrow_limbs");
+      launch_counter().fetch_add(1, std::memory_order_relaxed);
+      for (auto l : limbs) check_cuda(cudaFreeAsync(l, s), "cudaFreeAsync(limbs)");
+      const unsigned f = flag.read();
+      if (f & 1) return fail(PE_ELOGIC, "limb evaluation saw a coordinate beyond its own maxima");
+      fits = (f & 8) == 0;
+    } else {
+      if (flag.read() & 1) return fail(PE_ELOGIC, "limb evaluation saw a coordinate beyond its own maxima");
+      for (size_t i = 0; i < n; ++i) {
+        const std::uint64_t v0 = host_limbs[0][i];
+        const std::uint64_t ext = static_cast<std::uint64_t>(static_cast<std::int64_t>(v0) >> 63);
+        for (std::uint32_t k = 1; k < K; ++k) fits = fits && host_limbs[k][i] == ext;
+        out[i] = static_cast<int64_t>(v0);
+      }
+    }
+    if (!fits) return fail(PE_EOVERFLOW, "a result does not fit int64 (use pe_eval_limbs)");
+    return PE_OK;
   });
 }
 

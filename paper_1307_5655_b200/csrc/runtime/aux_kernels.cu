@@ -54,6 +54,46 @@ extern "C" cudaError_t pe_launch_max_abs_i64(const long long* x, size_t n,
 }
 
 // ---------------------------------------------------------------------------
+// narrow_limbs: K-limb two's-complement results -> int64, flagging (bit 8 of
+// the status word) any value whose high limbs are not the sign extension of
+// limb 0, i.e. that does not fit int64. Lets pe_eval_i64 stay exact when the
+// int64 overflow proof fails but the results themselves fit (the reference
+// BigInt has no overflow; its int64 conversion is what fails).
+namespace {
+struct LimbPtrs {
+  const unsigned long long* p[8];
+};
+
+__global__ void __launch_bounds__(256) narrow_limbs_kernel(LimbPtrs l, int k, size_t n,
+                                                           long long* __restrict__ out,
+                                                           unsigned* __restrict__ flag) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  bool bad = false;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const unsigned long long v0 = l.p[0][i];
+    const unsigned long long ext = static_cast<unsigned long long>(static_cast<long long>(v0) >> 63);
+    for (int j = 1; j < k; ++j) bad |= l.p[j][i] != ext;
+    out[i] = static_cast<long long>(v0);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 8u);
+}
+}  // namespace
+
+extern "C" cudaError_t pe_launch_narrow_limbs(const unsigned long long* const* limbs, int k,
+                                              size_t n, long long* out, unsigned* flag, int sms,
+                                              cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  if (k < 1 || k > 8) return cudaErrorInvalidValue;
+  LimbPtrs l{};
+  for (int j = 0; j < k; ++j) l.p[j] = limbs[j];
+  const size_t want = (n + 255) / 256;
+  const int grid = static_cast<int>(want < static_cast<size_t>(sms) * 8 ? want
+                                                                        : static_cast<size_t>(sms) * 8);
+  narrow_limbs_kernel<<<grid, 256, 0, stream>>>(l, k, n, out, flag);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Pipe-peak microbenchmarks: the roofline denominators for the FP64-bound
 // (C1/C2/C4/C5) and int64-MAD-bound (C3) walks. MEASURED_PEAKS.json carries
 // only HBM and bf16 peaks, so bench.py measures these live on the same GPU.

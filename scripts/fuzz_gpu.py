@@ -78,12 +78,23 @@ def check(seed):
         xi = [rng.integers(-span, span + 1, n).astype(np.int64) for _ in range(p.nvars)]
         try:
             ref = orc.eval_i64(xi)
-        except OverflowError:
+        except OverflowError:  # some intermediate leaves int64: the reference BigInt decides
             ref = None
         if ref is not None:
             got = pe.Evaluator(pe.BigIntDomain(), prog).evaluate(xi)
             assert np.array_equal(got, ref), "i64"
             done.append("i64")
+        elif pyoracle.ref_available() and 0 < prog.limbs_needed([span] * p.nvars) <= 8:
+            k = prog.limbs_needed([span] * p.nvars)
+            big = pe.limbs_to_int(pyoracle.Reference(p, sch).eval_limbs(xi, k, 8))
+            fits = all(-(2**63) <= int(v) < 2**63 for v in big)
+            try:
+                got = pe.Evaluator(pe.BigIntDomain(), prog).evaluate(xi)
+                assert fits and [int(v) for v in got] == [int(v) for v in big], "i64 via limbs"
+                done.append("i64_limbs")
+            except OverflowError:
+                assert not fits, "i64 refused although the results fit"
+                done.append("i64_refused")
         k = prog.limbs_needed([span] * p.nvars)
         if 0 < k <= 8 and pyoracle.ref_available():
             want = pyoracle.Reference(p, sch).eval_limbs(xi, k, 8)

@@ -66,3 +66,24 @@ def test_wide_domain_big_coefficients(scheme, cuda_device):
     assert list(got) == list(want)
     py = [sum(int(c) * int(v) ** (d - i) for i, c in enumerate(coefs)) for v in x[0][:50]]
     assert list(got[:50]) == py
+
+
+def test_int64_results_exact_when_only_intermediates_overflow(cuda_device):
+    # (x^40 - x^40 y^2 ...) style cancellation: intermediates leave int64, the
+    # results fit — pe_eval_i64 evaluates in limbs and narrows (tier 3); a
+    # result that does not fit is refused like the reference's conversion
+    rng = np.random.default_rng(8)
+    ex = np.array([[30, 0], [30, 1], [0, 0]], dtype=np.uint32)
+    poly = pe.Polynomial(ex, np.array([1, -1, 5], dtype=np.int64), ("x", "y"))
+    schemes = [pe.builtin_scheme("horner")] * 2
+    prog = pe.compile(poly, schemes)
+    x = rng.integers(-8, 9, 3000).astype(np.int64)
+    y = np.ones(3000, dtype=np.int64)  # x^30 * (1 - y) + 5 = 5, intermediates ~2^90
+    for dev in (False, True):
+        cols = [_t(x, cuda_device), _t(y, cuda_device)] if dev else [x, y]
+        got = pe.Evaluator(pe.BigIntDomain(), prog).evaluate(cols)
+        got = got.cpu().numpy() if dev else got
+        assert np.array_equal(got, np.full(3000, 5))
+    y2 = np.zeros(3000, dtype=np.int64)  # x^30 + 5: does not fit for |x| = 8
+    with pytest.raises(OverflowError):
+        pe.Evaluator(pe.BigIntDomain(), prog).evaluate([x, y2])
