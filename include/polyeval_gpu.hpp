@@ -18,6 +18,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -75,6 +76,24 @@ class Program {
     return Program(p, nvars);
   }
 
+  /// An already compiled program (reference CompiledProgram, flattened; see
+  /// pe_program_from_compiled and INTEGRATION.md).
+  static Program from_compiled(const pe_compiled_program* programs, std::size_t nprograms,
+                               std::uint32_t nvars, const std::uint32_t* const* exponent_sets,
+                               const std::size_t* exponent_set_sizes, bool integer) {
+    pe_program* p = nullptr;
+    check(pe_program_from_compiled(programs, nprograms, nvars, exponent_sets, exponent_set_sizes,
+                                   integer ? PE_COEFF_I64 : PE_COEFF_F64, &p));
+    return Program(p, nvars);
+  }
+
+  /// Smallest 64-bit limb count (1..8) for |x_v| <= bounds[v]; 0 if > 8.
+  std::uint32_t limbs_needed(const std::uint64_t* bounds) const {
+    std::uint32_t k = 0;
+    check(pe_program_limbs_needed(h_.get(), bounds, &k));
+    return k;
+  }
+
   const pe_program* get() const { return h_.get(); }
   std::uint32_t nvars() const { return nvars_; }
 
@@ -125,6 +144,18 @@ class BatchEvaluator {
     } else {
       check(pe_eval_f64(program_.get(), c.data(), n, out, &exec_));
     }
+  }
+
+  /// BigIntDomain beyond int64: `limbs` 64-bit words per result (two's
+  /// complement, little-endian), out_limbs[k][i] = word k of point i.
+  void evaluate_limbs(std::initializer_list<const std::int64_t*> coords, std::size_t n,
+                      std::uint32_t limbs, std::uint64_t* const* out_limbs) const {
+    static_assert(std::is_same_v<D, BigIntDomain>, "exact integer domain only");
+    if (coords.size() != program_.nvars()) {
+      throw std::invalid_argument("evaluation point arity mismatch");
+    }
+    std::vector<const std::int64_t*> c(coords);
+    check(pe_eval_limbs(program_.get(), c.data(), n, limbs, out_limbs, &exec_));
   }
 
   /// Reference evaluate_parallel (eval.hpp:97-140): identical results; the

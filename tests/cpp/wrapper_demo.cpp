@@ -28,6 +28,20 @@ int main() {
     bad |= !(oi[0] == 793 && oi[1] == 1 && oi[2] == 6 && of[0] == 793 && of[1] == 1 && of[2] == 6 &&
              lo[0] <= 793 && hi[0] >= 793);
   }
+  {  // BigInt beyond int64: 2 limbs, equal to the int64 path where both apply
+    Program p = Program::from_terms(exps, ci, 9, 1, {"balanced"});
+    const std::int64_t xs[] = {2, -3, 5};
+    std::uint64_t l0[3], l1[3];
+    std::uint64_t* limbs[] = {l0, l1};
+    BatchEvaluator<BigIntDomain>(p).evaluate_limbs({xs}, 3, 2, limbs);
+    std::int64_t ref[3];
+    BatchEvaluator<BigIntDomain>(p).evaluate({xs}, 3, ref);
+    for (int i = 0; i < 3; ++i) {
+      const std::uint64_t ext = ref[i] < 0 ? ~0ull : 0ull;
+      bad |= !(l0[i] == static_cast<std::uint64_t>(ref[i]) && l1[i] == ext);
+    }
+    std::printf("limbs %lld %lld %lld\n", (long long)ref[0], (long long)ref[1], (long long)ref[2]);
+  }
   try {
     Program p = Program::from_terms(exps, ci, 9, 1, {"estrin"});
     BatchEvaluator<BigIntDomain>(p).evaluate({xi, xi}, 3, nullptr);
