@@ -52,24 +52,30 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   // SM (ptxas capped at 128 registers) beats several 128-thread CTAs.
   KernelShape s;
   (void)ops;
-  // Coefficients alternate between constant-bank loads (LDCU, uniform pipe)
-  // and immediates (MOV pairs, ALU/FMA/uniform pipes): ptxas otherwise turns
-  // half the constant loads into per-thread LDC on the MIO queue
-  // (profiles/r1_imm_sweep.txt).
+  // Coefficient delivery (imm_mode): a DFMA reads at most one uniform
+  // register, so the walk's coefficients split into uniform-bound words
+  // (paired LDCU.128) and the register-bound second coefficient of
+  // fma(c, x^d, c') leaves (per-thread LDC); the earlier alternation of
+  // constant loads and immediates (mode 2, profiles/r1_imm_sweep.txt) spent
+  // two ALU/uniform MOVs per immediate and left C4 issue-bound.
   if (d == Domain::Interval) {
     s = {1, 512, 32, 0};  // integer-pipe bound; no coefficient pressure
   } else if (d == Domain::I64K) {
     s = {1, 256, 0, 0};   // K-limb registers: one point per thread
   } else if (powers > 32) {
     // very wide programs (large power tables): registers are the limit
-    s = {1, 512, 0, 2};
+    s = {1, 512, 0, 6};
   } else if (distinct_coefs < 64) {
-    // few distinct coefficients: ptxas encodes them as immediates or keeps
-    // them in uniform registers; independent sub-chains give enough ILP
-    s = {1, 512, 0, 0};
+    // few distinct coefficients: independent sub-chains give enough ILP
+    s = {1, 512, 0, 6};
   } else {
-    s = {4, 256, 0, 2};
+    s = {4, 256, 0, 6};
+    s.min_ctas = 2;  // <= 128 registers: two CTAs (16 warps) per SM
   }
+  // imm_mode 6 (profiles/r1_imm6_sweep.txt): uniform-bound coefficients in
+  // paired 16-byte LDCUs, the second coefficient of two-coefficient FMAs as
+  // per-thread LDCs — C4 4.23 -> 3.71 ms per 4e6 points (with 4 slices), C2
+  // 0.683 -> 0.646 ms per 1e7, C3 0.610 -> 0.579 ms per 1e7.
   // strict fp64 keeps every reference add: more live temporaries; a 512-wide
   // CTA caps ptxas at 128 registers so two CTAs fit an SM (C2 balanced d1000
   // strict: 174 registers at 256 wide, 2.54 -> 1.46 ms per 1e7 points)
@@ -83,7 +89,8 @@ KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
   env("PE_LANES", 1, 8, s.lanes);
   env("PE_BLOCK", 32, 1024, s.block);
   env("PE_SYNC", 0, 1u << 20, s.sync_every);
-  env("PE_IMM", 0, 3, s.imm_mode);
+  env("PE_IMM", 0, 6, s.imm_mode);
+  env("PE_MINCTAS", 0, 32, s.min_ctas);
   return s;
 }
 
@@ -195,7 +202,7 @@ class Emitter {
  public:
   Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
-        imm_mode_(shape.imm_mode), accumulate_(shape.accumulate),
+        imm_mode_(shape.imm_mode), min_ctas_(shape.min_ctas), accumulate_(shape.accumulate),
         K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1) {
     if (accumulate_ && d_ != Domain::F64) throw std::logic_error("accumulate is fp64-only");
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
@@ -248,7 +255,7 @@ class Emitter {
       emit_walk();
       emit_epilogue();
     }
-    const std::string main_entry = entry_text(img, img.entry);
+    const std::string main_entry = entry_text(img, img.entry, 0, min_ctas_);
 
     // fixup entry: strict replay of the listed points (grid-stride loop)
     std::string fix_entry;
@@ -268,7 +275,12 @@ class Emitter {
       fix_ = false;
       // launched with 128 threads, 4 CTAs per SM (<= 128 registers): the
       // replay is latency-bound, so every listed point gets its own thread
-      fix_entry = entry_text(img, img.fix_entry, 128, 4);
+      // (PE_FIX_BLOCK / PE_FIX_CTAS override for tuning)
+      img.fix_block = 128;
+      img.fix_ctas_per_sm = 4;
+      if (const char* e = std::getenv("PE_FIX_BLOCK")) img.fix_block = static_cast<std::uint32_t>(std::atoi(e));
+      if (const char* e = std::getenv("PE_FIX_CTAS")) img.fix_ctas_per_sm = static_cast<std::uint32_t>(std::atoi(e));
+      fix_entry = entry_text(img, img.fix_entry, img.fix_block, img.fix_ctas_per_sm);
       P_ = lanes;
       sync_every_ = sync;
     }
@@ -279,7 +291,7 @@ class Emitter {
       << " lanes=" << P_ << (fast ? " interval-fast-path+fixup" : "") << "\n//\n";
     m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
     if (n_const_ > 0) {
-      m << ".const .align 8 .b64 pe_coef[" << n_const_ << "] = {";
+      m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
       for (std::uint32_t i = 0; i < n_const_; ++i) {
         if (i) m << (i % 8 == 0 ? ",\n  " : ", ");
         m << hex64(words_[i]);
@@ -303,6 +315,7 @@ class Emitter {
     decls_.clear();
     n_creg_ = n_tf_ = n_tu_ = n_tp_ = n_tr_ = 0;
     loop_decls_ = false;
+    pending_.clear();
   }
 
   void finish_entry() {
@@ -339,7 +352,7 @@ class Emitter {
       param(".param .u64 pe_count");
       param(".param .u64 pe_cap");
     }
-    if (n_param_ > 0) param(".param .align 8 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
+    if (n_param_ > 0) param(".param .align 16 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
     m << ")\n.maxntid " << maxntid << ", 1, 1\n";
     if (min_ctas) m << ".minnctapersm " << min_ctas << "\n";
     m << "{\n";
@@ -361,7 +374,28 @@ class Emitter {
       dedup.emplace(w, idx);
       return idx;
     };
+    // imm_mode 5 (scalar domains): an FMA can take one uniform-register
+    // operand, so the second coefficient of a two-coefficient op
+    // (fma(c, x^d, c'), the leaves of every scheme) is register-bound. Those
+    // become immediates; every other coefficient is uniform-bound, and only
+    // those words go to the constant bank, in first-use order, where they
+    // arrive two per 16-byte LDCU (load_word).
+    reg_bound_.assign(s_.coefs.size(), 0);
+    // imm_mode 6: the register-bound words are not immediates but a second
+    // constant-bank region (first-use order, paired loads: ptxas turns those
+    // into per-thread 16-byte LDCs, one issue slot per two coefficients).
+    const bool split = (imm_mode_ == 5 || imm_mode_ == 6) && d_ != Domain::Interval &&
+                       d_ != Domain::I64K;
+    if (split) {
+      for (const Op& op : s_.ops) {
+        const int nc = op.a.is(Operand::Coef) + op.b.is(Operand::Coef) + op.c.is(Operand::Coef);
+        if (nc < 2) continue;
+        const Operand& r = op.c.is(Operand::Coef) ? op.c : op.b;  // keep one uniform operand
+        reg_bound_[r.id] = 1;
+      }
+    }
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
+      if (split && reg_bound_[k]) continue;  // emitted as an immediate (load())
       if (d_ == Domain::Interval) {
         const IvCoef c = ivcoef(k);
         coef_lo_[k] = word(bits_of(c.lo));
@@ -381,10 +415,28 @@ class Emitter {
         coef_lo_[k] = coef_hi_[k] = word(bits_of(c));
       }
     }
+    if (split && imm_mode_ == 6) {
+      if (words_.size() & 1) words_.push_back(0);  // region starts on a pair
+      for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
+        if (!reg_bound_[k]) continue;
+        coef_lo_[k] = coef_hi_[k] = static_cast<std::uint32_t>(words_.size());
+        words_.push_back(scalar_word(k));
+      }
+    }
     const auto n = static_cast<std::uint32_t>(words_.size());
     n_const_ = std::min(n, CoefTiers::kConstCap);
     n_param_ = std::min(n - n_const_, CoefTiers::kParamCap);
     n_global_ = n - n_const_ - n_param_;
+  }
+
+  // 64-bit word of scalar coefficient k as the kernel consumes it: the raw
+  // integer for the int64 / K-limb kernels, otherwise the double (exact for
+  // I64F by the host proof; RN for an integer polynomial evaluated in fp64)
+  std::uint64_t scalar_word(std::size_t k) const {
+    if constexpr (std::is_same_v<C, std::int64_t>) {
+      if (d_ == Domain::I64 || d_ == Domain::I64K) return static_cast<std::uint64_t>(s_.coefs[k]);
+    }
+    return bits_of(static_cast<double>(s_.coefs[k]));
   }
 
   // Interval value of coefficient k: injection, then the folded zero-add
@@ -425,6 +477,32 @@ class Emitter {
 
   // Loads coefficient word w into a fresh register (shared by all lanes).
   std::string load_word(std::uint32_t w) {
+    if (imm_mode_ >= 4) {
+      // paired uniform loads: words sit in first-use order, so an even word
+      // and its odd neighbour arrive in one 16-byte LDCU (half the
+      // coefficient-delivery issue slots of one LDCU per word)
+      auto it = pending_.find(w);
+      if (it != pending_.end()) {
+        std::string r = it->second;
+        pending_.erase(it);
+        return r;
+      }
+      const bool pair_const = w < n_const_ && (w & 1) == 0 && w + 1 < n_const_;
+      const bool pair_param = w >= n_const_ && w < n_const_ + n_param_ && ((w - n_const_) & 1) == 0 &&
+                              w + 1 < n_const_ + n_param_;
+      if (pair_const || pair_param) {
+        std::string r = "%c" + std::to_string(n_creg_++);
+        std::string r2 = "%c" + std::to_string(n_creg_++);
+        if (pair_const) {
+          body_ << "  ld.const.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_coef+" << 8 * w << "];\n";
+        } else {
+          body_ << "  ld.param.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_pcoef+"
+                << 8 * (w - n_const_) << "];\n";
+        }
+        pending_[w + 1] = r2;
+        return r;
+      }
+    }
     std::string r = "%c" + std::to_string(n_creg_++);
     if (imm_mode_ == 1 || (imm_mode_ == 2 && (w & 1)) || (imm_mode_ == 3 && w >= n_const_)) {
       // immediate: ptxas materialises it with two 32-bit moves on the ALU /
@@ -474,6 +552,11 @@ class Emitter {
   };
   Loaded load(const Operand& o) {
     if (!o.is(Operand::Coef)) return {};
+    if (o.id < reg_bound_.size() && reg_bound_[o.id] && imm_mode_ == 5) {
+      const std::string r = "%c" + std::to_string(n_creg_++);
+      body_ << "  mov.b64 " << r << ", " << hex64(scalar_word(o.id)) << ";\n";
+      return {r, r};
+    }
     const std::string lo = load_word(coef_lo_[o.id]);
     const std::string hi = coef_hi_[o.id] == coef_lo_[o.id] ? lo : load_word(coef_hi_[o.id]);
     return {lo, hi};
@@ -1022,7 +1105,18 @@ class Emitter {
       const std::string a = tmp_f();
       body_ << "  abs.f64 " << a << ", " << src << ";\n";
       if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
-      body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
+      if (dir_next_) {
+        // Directed variant: RD(v - |v| 2^-60) / RU(v + |v| 2^-60). The exact
+        // value lies strictly between v and its neighbour on that side for
+        // every finite nonzero v, subnormals included (|v| 2^-60 is below
+        // the spacing), so directed rounding lands on the neighbour; only
+        // +-0 does not move (flagged by the test below), and DBL_MAX up /
+        // -DBL_MAX down give +-inf as std::nextafter does.
+        body_ << "  fma." << (up ? "rp" : "rm") << ".f64 " << dst << ", " << a
+              << ", 0d3C30000000000000, " << src << ";\n";
+      } else {
+        body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
+      }
       // "Did not move" test: either an FP64 compare, or (same answer) a
       // 32-bit integer compare of the low words on the ALU pipe — a step of
       // one ulp changes the bit pattern by +-1, so the low words differ iff
@@ -1355,6 +1449,7 @@ class Emitter {
   std::uint32_t block_;
   std::uint32_t sync_every_;
   std::uint32_t imm_mode_;
+  std::uint32_t min_ctas_ = 0;
   bool accumulate_ = false;
   std::uint32_t K_ = 1;  // I64K limbs
   bool fast_ = false;  // emitting the interval fast path
@@ -1371,6 +1466,12 @@ class Emitter {
   bool hybrid_next_ = [] {
     const char* e = std::getenv("PE_IV_NEXT");
     return e && std::string(e) == "hybrid";
+  }();
+  // PE_IV_NEXT=dir: the FP64-pipe step with directed rounding (exact for
+  // subnormals too, so fewer points need the strict replay)
+  bool dir_next_ = [] {
+    const char* e = std::getenv("PE_IV_NEXT");
+    return e && std::string(e) == "dir";
   }();
   std::uint32_t nb_ = 0;
   std::vector<int> rsign_, psign_;  // fast path: static signs of registers / powers
@@ -1397,6 +1498,8 @@ class Emitter {
   std::string run_arrays_;
   bool loop_decls_ = false;
   std::vector<std::uint64_t> words_;
+  std::unordered_map<std::uint32_t, std::string> pending_;  // imm_mode 4/5: second word of a pair
+  std::vector<char> reg_bound_;  // imm_mode 5: coefficient emitted as an immediate
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
   std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0, n_tr_ = 0;
@@ -1421,6 +1524,7 @@ KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape) 
   if (shape.block == 0) shape.block = def.block;
   if (shape.sync_every == 0) shape.sync_every = def.sync_every;
   if (shape.imm_mode == 0) shape.imm_mode = def.imm_mode;
+  if (shape.min_ctas == 0) shape.min_ctas = def.min_ctas;
   if (shape.limbs == 0) shape.limbs = 1;
   Emitter<C> e(stream, domain, shape);
   return e.run();

@@ -55,6 +55,8 @@ struct KernelImage {
   std::uint32_t limbs = 1;         // I64K: 64-bit words per value (= result arrays)
   std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
+  std::uint32_t fix_block = 128;   // fixup kernel CTA size (.maxntid)
+  std::uint32_t fix_ctas_per_sm = 4;  // fixup grid: CTAs per SM (.minnctapersm)
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
   std::uint64_t int_ops = 0;       // int64 add/mul/mad per point
@@ -81,6 +83,9 @@ struct KernelShape {
   bool accumulate = false;
   // I64K: 64-bit limbs per value (1..8)
   std::uint32_t limbs = 0;
+  // .minnctapersm of the walk entry (0 = none): caps ptxas at
+  // 65536 / (block * min_ctas) registers
+  std::uint32_t min_ctas = 0;
 };
 
 /// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC

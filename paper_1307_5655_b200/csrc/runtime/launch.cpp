@@ -129,9 +129,10 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   if (img.interval_fast_path) {
     // strict replay of the points the fast path could not prove; it reads
     // the list length on the device, so no host round trip in between
+    const std::uint64_t fb = img.fix_block;
     const unsigned fix_grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(4 * static_cast<std::uint64_t>(sm_count(device)),
-                                (la.cap + 127) / 128));
+        std::min<std::uint64_t>(img.fix_ctas_per_sm * static_cast<std::uint64_t>(sm_count(device)),
+                                (la.cap + fb - 1) / fb));
     cudaStream_t fs = stream;
     if (la.fix_stream) {
       // hand the list over to the side stream: the latency-bound replay then
@@ -144,7 +145,7 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
       fs = la.fix_stream;
     }
     launch_one(a.fix_kernel, device >= 0 && device < Artifact::kMaxDevices ? a.fix_fn[device] : nullptr,
-               dim3(fix_grid ? fix_grid : 1), dim3(128), args.data(), fs, "launch(fixup)");
+               dim3(fix_grid ? fix_grid : 1), dim3(static_cast<unsigned>(fb)), args.data(), fs, "launch(fixup)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   }
 }

@@ -200,10 +200,11 @@ std::size_t Program::slice_count() const {
   std::size_t k = 0;
   if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
   if (k == 0) {
-    // measured on C4 (profiles/r1_slices_c4.txt): straight-line kernels
-    // beyond a few thousand records pay for instruction fetch and register
-    // pressure (power tables); ~2k records per slice
-    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 2100, 2, 256) : 1;
+    // measured on C4 (profiles/r1_slices_c4.txt, r1_imm6_sweep.txt):
+    // straight-line kernels beyond a few thousand records pay for
+    // instruction fetch and register pressure (power tables); ~3k records
+    // per slice with paired coefficient loads (2k before them)
+    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 3000, 2, 256) : 1;
   }
   return std::min<std::size_t>(std::max<std::size_t>(1, k), std::max<std::size_t>(1, nterms));
 }

@@ -115,3 +115,39 @@ def test_sparse_horner_splits_runs_at_gaps():
     ptx = prog.ptx(pe.DOMAIN_F64)
     assert ptx.count("bra.uni $Lrun") == 1  # the 200-long dense tail
     assert prog.compile_only(pe.DOMAIN_F64) > 0
+
+
+def _kernel_words(ptx):
+    """Every 64-bit coefficient word a kernel can read: the constant-bank
+    array, the parameter tier is absent at these sizes, plus immediates."""
+    import re
+    words = set()
+    for m in re.finditer(r"\.const \.align \d+ \.b64 pe_coef\[\d+\] = \{([^}]*)\}", ptx, re.S):
+        words |= {int(w, 16) for w in re.findall(r"0x[0-9A-Fa-f]{16}", m.group(1))}
+    words |= {int(w, 16) for w in re.findall(r"mov\.b64 %c\d+, (0x[0-9A-Fa-f]{16});", ptx)}
+    return words
+
+
+@pytest.mark.parametrize("imm", ["0", "2", "5", "6"])
+@pytest.mark.parametrize("domain", ["f64", "f64strict", "i64", "i64f"])
+def test_coefficient_words_every_delivery_mode(monkeypatch, imm, domain):
+    # The reference worked example (eval_test.cpp:80-93) with int64
+    # coefficients; whatever the coefficient delivery (constant bank, paired
+    # loads, register-bound second coefficients, immediates), the kernel
+    # reads each coefficient in the domain's own word format: doubles for the
+    # FP64 kernels, raw integers for the int64 kernel.
+    import struct
+    monkeypatch.setenv("PE_IMM", imm)
+    e, c = [8, 7, 6, 5, 4, 3, 2, 1, 0], [3, -1, 2, 1, -4, 9, -3, -2, 1]
+    d = {"f64": pe.DOMAIN_F64, "f64strict": pe.DOMAIN_F64_STRICT, "i64": pe.DOMAIN_I64,
+         "i64f": pe.DOMAIN_I64F}[domain]
+    p = pe.Polynomial(np.array(e).reshape(-1, 1), np.array(c, dtype=np.int64))
+    for scheme in ("direct", "horner", "estrin", "balanced"):
+        ptx = pe.compile(p, pe.builtin_scheme(scheme)).ptx(d)
+        if domain == "i64":
+            want = {v & (2**64 - 1) for v in c}
+        else:
+            want = {struct.unpack("<Q", struct.pack("<d", float(v)))[0] for v in c}
+        got = _kernel_words(ptx) - {0}
+        assert want <= got, (scheme, sorted(want - got))
+        assert got <= want, (scheme, sorted(got - want))
