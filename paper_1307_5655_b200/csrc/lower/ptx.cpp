@@ -267,10 +267,29 @@ class Emitter {
       reset_entry();
       fix_ = true;
       emit_fix_prologue();
+      if (mid_replay_) {
+        // finite-case replay first; the bit-level replay only on %pmid
+        decls_ << "  .reg .pred %pmid;\n  .reg .f64 %macc;\n";
+        body_ << "  mov.f64 %macc, 0d0000000000000000;\n";
+        for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+          for (bool hi : {false, true}) {
+            body_ << "  fma.rn.f64 %macc, " << xr(v, 0, hi) << ", 0d0000000000000000, %macc;\n";
+          }
+        }
+        medium_ = true;
+        emit_powers();
+        emit_walk();
+        body_ << "  setp.nan.f64 %pmid, %macc, %macc;\n  @%pmid bra $Lexact;\n";
+        emit_store();
+        body_ << "  bra $Lnextpt;\n$Lexact:\n";
+        medium_ = false;
+      }
       emit_powers();
       emit_walk();
       emit_store();
-      body_ << "  add.u64 %rd1, %rd1, %rd2;\n  bra $Lfix;\n";
+      // one listed point per thread, no grid-stride loop: a loop would let
+      // ptxas hoist every coefficient load out of it and spill them
+      body_ << "$Lnextpt:\n";
       finish_entry();
       fix_ = false;
       // launched with 128 threads, 4 CTAs per SM (<= 128 registers): the
@@ -524,13 +543,13 @@ class Emitter {
   // ---------------- operands ----------------
   std::string reg(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) {
-      return std::string(fast_ ? "%f" : "%") + (hi ? "vh" : "vl") + std::to_string(id) + ln(lane);
+      return std::string(fast_ ? "%f" : medium_ ? "%m" : "%") + (hi ? "vh" : "vl") + std::to_string(id) + ln(lane);
     }
     return "%v" + std::to_string(id) + ln(lane);
   }
   std::string pw(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) {
-      return std::string(fast_ ? "%f" : "%") + (hi ? "ph" : "pl") + std::to_string(id) + ln(lane);
+      return std::string(fast_ ? "%f" : medium_ ? "%m" : "%") + (hi ? "ph" : "pl") + std::to_string(id) + ln(lane);
     }
     return "%q" + std::to_string(id) + ln(lane);
   }
@@ -710,6 +729,9 @@ class Emitter {
                    psign_[p.hi]);
           fcheck_finite(pw(id, k, false));
           fcheck_finite(pw(id, k, true));
+        } else if (d_ == Domain::Interval && medium_) {
+          mid_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
+                  {pw(p.hi, k, false), pw(p.hi, k, true)});
         } else if (d_ == Domain::Interval) {
           iv_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
                  {pw(p.hi, k, false), pw(p.hi, k, true)}, k == 0);
@@ -1073,6 +1095,66 @@ class Emitter {
     next(dhi, mx, true);
   }
 
+  // ---------------- interval replay, finite case ----------------
+  // The fixup entry first replays a listed point with cheap primitives that
+  // are exact as long as every value stays finite, and falls back to the
+  // bit-level replay (next / iv_add / iv_mul above) only when a non-finite
+  // value appeared (%pmid). With finite operands:
+  //  * next_down(v) = RD(v - RN(|v| 2^-60 + dmin)): the subtracted amount is
+  //    at least dmin and below the spacing of v, so the exact difference lies
+  //    in [neighbour, v) — std::nextafter for every finite v including +-0
+  //    (-> -dmin) and subnormals; next_up symmetric with RU.
+  //  * interval_mul's zero rule only differs from RN(x*y) when the other
+  //    operand is inf/NaN, or in the sign of a zero product; a zero's sign
+  //    never survives the nextafter step that follows min/max (both +-0 step
+  //    to -/+dmin), so plain products and min/max give the same endpoints.
+  void mnext(const std::string& dst, const std::string& src, bool up) {
+    const std::string a = tmp_f(), t = tmp_f();
+    body_ << "  abs.f64 " << a << ", " << src << ";\n"
+          << "  fma.rn.f64 " << t << ", " << a << ", 0d3C30000000000000, 0d0000000000000001;\n"
+          << (up ? "  add.rp.f64 " : "  sub.rm.f64 ") << dst << ", " << src << ", " << t << ";\n";
+    // inf or NaN result (DBL_MAX up, +inf down, overflow) poisons the
+    // accumulator (0 * inf = NaN): the point then takes the exact replay
+    body_ << "  fma.rn.f64 %macc, " << dst << ", 0d0000000000000000, %macc;\n";
+  }
+
+  void mid_add(const std::string& dlo, const std::string& dhi,
+               const std::pair<std::string, std::string>& a,
+               const std::pair<std::string, std::string>& b, bool a_is_zero) {
+    if (a_is_zero) {
+      mnext(dlo, b.first, false);
+      mnext(dhi, b.second, true);
+      return;
+    }
+    const std::string lo = tmp_f(), hi = tmp_f();
+    body_ << "  add.rn.f64 " << lo << ", " << a.first << ", " << b.first << ";\n"
+          << "  add.rn.f64 " << hi << ", " << a.second << ", " << b.second << ";\n";
+    mnext(dlo, lo, false);
+    mnext(dhi, hi, true);
+  }
+
+  void mid_mul(const std::string& dlo, const std::string& dhi,
+               const std::pair<std::string, std::string>& a,
+               const std::pair<std::string, std::string>& b) {
+    const std::string p1 = tmp_f(), p2 = tmp_f(), p3 = tmp_f(), p4 = tmp_f();
+    const std::string mn = tmp_f(), mx = tmp_f();
+    body_ << "  mul.rn.f64 " << p1 << ", " << a.first << ", " << b.first << ";\n"
+          << "  mul.rn.f64 " << p2 << ", " << a.first << ", " << b.second << ";\n"
+          << "  mul.rn.f64 " << p3 << ", " << a.second << ", " << b.first << ";\n"
+          << "  mul.rn.f64 " << p4 << ", " << a.second << ", " << b.second << ";\n"
+          << "  mov.f64 " << mn << ", " << p1 << ";\n  mov.f64 " << mx << ", " << p1 << ";\n";
+    // std::min / std::max scan order (no NaN can occur with finite operands)
+    for (const std::string* p : {&p2, &p3, &p4}) {
+      const std::string q = tmp_p(), r = tmp_p();
+      body_ << "  setp.lt.f64 " << q << ", " << *p << ", " << mn << ";\n"
+            << "  selp.f64 " << mn << ", " << *p << ", " << mn << ", " << q << ";\n"
+            << "  setp.lt.f64 " << r << ", " << mx << ", " << *p << ";\n"
+            << "  selp.f64 " << mx << ", " << *p << ", " << mx << ", " << r << ";\n";
+    }
+    mnext(dlo, mn, false);
+    mnext(dhi, mx, true);
+  }
+
   // ---------------- interval fast path ----------------
   // Same op sequence as the strict replay, cheaper primitives that are exact
   // under preconditions, plus a per-thread accumulator (%facc, sign bit) that
@@ -1294,6 +1376,8 @@ class Emitter {
             const int sum_sign = op.a.is(Operand::Zero) ? sb : (sa == sb ? sa : 0);
             fast_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero),
                      sum_sign);
+          } else if (medium_) {
+            mid_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero));
           } else {
             iv_add(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Zero), k == 0);
           }
@@ -1303,6 +1387,8 @@ class Emitter {
             // coefficients are host-checked, powers checked where computed
             fast_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), op.a.is(Operand::Reg),
                      op.b.is(Operand::Reg), sa, sb);
+          } else if (medium_) {
+            mid_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k));
           } else {
             iv_mul(dlo, dhi, ivop(op.a, la, k), ivop(op.b, lb, k), k == 0);
           }
@@ -1453,6 +1539,11 @@ class Emitter {
   bool accumulate_ = false;
   std::uint32_t K_ = 1;  // I64K limbs
   bool fast_ = false;  // emitting the interval fast path
+  bool medium_ = false;  // emitting the finite-case replay of the fixup entry
+  bool mid_replay_ = [] {  // PE_IV_MID=0: fixup entry = bit-level replay only
+    const char* e = std::getenv("PE_IV_MID");
+    return !(e && std::atoi(e) == 0);
+  }();
   bool fix_ = false;   // emitting the fixup entry
   // fast-path nextafter on the FP64 pipe (default) or as integer +-1 with
   // sign-flip detection (PE_IV_NEXT=int)

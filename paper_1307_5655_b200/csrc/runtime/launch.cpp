@@ -129,10 +129,11 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   if (img.interval_fast_path) {
     // strict replay of the points the fast path could not prove; it reads
     // the list length on the device, so no host round trip in between
+    // one thread per list slot (the kernel has no grid-stride loop); threads
+    // past the device-side count exit at once
     const std::uint64_t fb = img.fix_block;
     const unsigned fix_grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(img.fix_ctas_per_sm * static_cast<std::uint64_t>(sm_count(device)),
-                                (la.cap + fb - 1) / fb));
+        std::min<std::uint64_t>(0x7fffffffull, (la.cap + fb - 1) / fb));
     cudaStream_t fs = stream;
     if (la.fix_stream) {
       // hand the list over to the side stream: the latency-bound replay then

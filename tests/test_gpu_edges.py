@@ -125,7 +125,7 @@ def test_repeatable_and_shard_invariant(cuda_device):
     assert torch.equal(full, again) and torch.equal(full, halves)
 
 
-@pytest.mark.parametrize("next_mode", ["hybrid", "fma", "int"])
+@pytest.mark.parametrize("next_mode", ["hybrid", "fma", "int", "dir"])
 def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch, next_mode):
     monkeypatch.setenv("PE_IV_NEXT", next_mode)
     # The fast interval path (sign-case products, integer nextafter with
