@@ -151,3 +151,21 @@ def test_coefficient_words_every_delivery_mode(monkeypatch, imm, domain):
         got = _kernel_words(ptx) - {0}
         assert want <= got, (scheme, sorted(want - got))
         assert got <= want, (scheme, sorted(got - want))
+
+
+def test_interval_fixup_entry_has_finite_case_replay(monkeypatch):
+    # The fixup entry replays a listed point with the finite-case primitives
+    # first (directed-rounding nextafter, plain products + scan-order
+    # min/max, NaN-poisoned accumulator) and keeps the bit-level replay
+    # behind the %pmid branch; one listed point per thread (no grid-stride
+    # loop, which would let ptxas hoist and spill the coefficient loads).
+    wl = W.c5()
+    prog = pe.compile(wl.poly, wl.schemes)
+    ptx = prog.ptx(pe.DOMAIN_INTERVAL)
+    fix = ptx[ptx.index(".entry pe_walk_interval_fix"):]
+    assert "%macc" in fix and "@%pmid bra $Lexact" in fix
+    assert "sub.rm.f64" in fix and "add.rp.f64" in fix
+    assert "bra $Lfix" not in fix
+    monkeypatch.setenv("PE_IV_MID", "0")
+    ptx0 = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
+    assert "%macc" not in ptx0
