@@ -608,6 +608,7 @@ class Emitter {
           << "  mul.wide.u32 %rd1, %r1, %r2;\n  mul.lo.u64 %rd1, %rd1, " << P_ << ";\n"
           << "  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
           << "  ld.param.u64 %rd3, [pe_n];\n";
+    emit_chain_warmup();
     if (sync_every_ == 0) {
       // no CTA barriers: threads past the end leave immediately; with
       // barriers every thread stays (clamped loads, predicated stores)
@@ -794,6 +795,36 @@ class Emitter {
 
   // ---------------- chain loops ----------------
   // (see chain_runs above)
+
+  // Constant-cache warm-up for the chain-loop arrays: thread t of every CTA
+  // touches line t (64 B) of each array once, so the loop's one-trip-ahead
+  // LDCU prefetch hits the SM's constant cache instead of paying one memory
+  // round trip per trip on a cold cache (small batches after an L2 flush:
+  // the loop is a single dependent chain of up to L/8 such misses). The
+  // loaded word feeds a never-true comparison (coefficient words are finite,
+  // the pattern is a NaN) so the load is not dead code. PE_WARM=0 disables.
+  void emit_chain_warmup() {
+    if (runs_.empty() || fix_) return;
+    int warm_mode = 1;
+    if (const char* e = std::getenv("PE_WARM")) warm_mode = std::atoi(e);
+    if (warm_mode == 0) return;
+    decls_ << "  .reg .b64 %wq<2>;\n  .reg .pred %wp<2>;\n  .reg .b32 %wl;\n";
+    for (std::size_t idx = 0; idx < runs_.size(); ++idx) {
+      const std::size_t words = runs_[idx].last - runs_[idx].head + kLoopU;
+      const std::size_t lines = (words + 7) / 8;
+      const std::string lbl = "$Lwarm" + std::to_string(idx);
+      // for (line = tid; line < lines; line += ntid) touch(line)
+      body_ << "  mov.u32 %wl, %r3;\n" << lbl << ":\n"
+            << "  setp.ge.u32 %wp0, %wl, " << lines << ";\n  @%wp0 bra " << lbl << "e;\n"
+            << (warm_mode == 2 ? "  mov.u64 %wq0, pe_run" : "  cvta.const.u64 %wq0, pe_run") << idx
+            << ";\n  mul.wide.u32 %wq1, %wl, 64;\n  add.u64 %wq0, %wq0, %wq1;\n"
+            << (warm_mode == 2 ? "  ld.const.b64 %wq1, [%wq0];\n  setp.eq.b64 %wp1, %wq1, "
+                                 "0x7FF8DEADBEEF0001;\n  @%wp1 trap;\n"
+                               : "  prefetchu.L1 [%wq0];\n")
+            << "  add.u32 %wl, %wl, %r2;\n  bra " << lbl << ";\n"
+            << lbl << "e:\n";
+    }
+  }
   void find_chain_runs() {
     const std::uint64_t budget =
         n_const_ < CoefTiers::kConstCap ? CoefTiers::kConstCap - n_const_ : 0;
