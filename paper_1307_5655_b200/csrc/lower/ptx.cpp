@@ -203,7 +203,8 @@ class Emitter {
   Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
         imm_mode_(shape.imm_mode), min_ctas_(shape.min_ctas), accumulate_(shape.accumulate),
-        K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1) {
+        K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1),
+        part_(shape.iv_partition) {
     if (accumulate_ && d_ != Domain::F64) throw std::logic_error("accumulate is fp64-only");
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
@@ -236,21 +237,32 @@ class Emitter {
     img.interval_fast_path = fast;
     img.entry = std::string("pe_walk_") + domain_name(d_);
 
+    const bool part = fast && part_ != 0 && s_.nvars == 1;
+    img.iv_partition = part ? part_ : 0;
+    if (part && part_ == 2) {
+      // mirrored program: only the negative-coordinate entry
+      img.entry += "_neg";
+      reset_entry();
+      gather_ = 2;
+      emit_fast_body();
+      gather_ = 0;
+      std::ostringstream m;
+      m << module_header(img, "interval-fast-path (x < 0, mirrored)");
+      m << run_arrays_ << entry_text(img, img.entry, 0, min_ctas_);
+      img.ptx = m.str();
+      img.fp_ops = fp_ops_;
+      img.int_ops = int_ops_;
+      img.hash = fnv1a(img.ptx.data(), img.ptx.size());
+      return img;
+    }
+
     // main entry
     reset_entry();
-    emit_prologue();
     if (fast) {
       // exact fast path; points it cannot prove go to the fixup list
-      decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n  .reg .pred %pb<4>;\n";
-      body_ << "  mov.b64 %facc, 0;\n";
-      for (int i = 0; i < 4; ++i) body_ << "  setp.ne.b32 %pb" << i << ", %r3, %r3;\n";
-      fast_ = true;
-      emit_powers();
-      emit_walk();
-      emit_fast_exit();
-      fast_ = false;
-      finish_entry();
+      emit_fast_body();
     } else {
+      emit_prologue();
       emit_powers();
       emit_walk();
       emit_epilogue();
@@ -304,20 +316,20 @@ class Emitter {
       sync_every_ = sync;
     }
 
-    std::ostringstream m;
-    m << "//\n// polyeval-b200 generated kernel: domain=" << domain_name(d_)
-      << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
-      << " lanes=" << P_ << (fast ? " interval-fast-path+fixup" : "") << "\n//\n";
-    m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
-    if (n_const_ > 0) {
-      m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
-      for (std::uint32_t i = 0; i < n_const_; ++i) {
-        if (i) m << (i % 8 == 0 ? ",\n  " : ", ");
-        m << hex64(words_[i]);
-      }
-      m << "};\n\n";
+    // positive-coordinate entry of the sign-partitioned fast path
+    std::string part_entry;
+    if (part) {
+      img.part_entry = img.entry + "_pos";
+      reset_entry();
+      gather_ = 1;
+      emit_fast_body();
+      gather_ = 0;
+      part_entry = entry_text(img, img.part_entry, 0, min_ctas_);
     }
-    m << run_arrays_ << main_entry << fix_entry;
+
+    std::ostringstream m;
+    m << module_header(img, fast ? "interval-fast-path+fixup" : "");
+    m << run_arrays_ << main_entry << fix_entry << part_entry;
     img.ptx = m.str();
     img.fp_ops = fp_ops_;
     img.int_ops = int_ops_;
@@ -327,6 +339,39 @@ class Emitter {
 
  private:
   // ---------------- entries ----------------
+  std::string module_header(const KernelImage& img, const char* note) const {
+    std::ostringstream m;
+    m << "//\n// polyeval-b200 generated kernel: domain=" << domain_name(d_)
+      << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
+      << " lanes=" << P_ << (*note ? " " : "") << note << "\n//\n";
+    m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
+    if (n_const_ > 0) {
+      m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
+      for (std::uint32_t i = 0; i < n_const_; ++i) {
+        if (i) m << (i % 8 == 0 ? ",\n  " : ", ");
+        m << hex64(words_[i]);
+      }
+      m << "};\n\n";
+    }
+    (void)img;
+    return m.str();
+  }
+
+  // Interval fast path entry body (main entry, or a partitioned entry when
+  // gather_ != 0): prologue, power DAG, walk, exit to the fixup list / store.
+  void emit_fast_body() {
+    emit_prologue();
+    decls_ << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n  .reg .pred %pb<4>;\n";
+    body_ << "  mov.b64 %facc, 0;\n";
+    for (int i = 0; i < 4; ++i) body_ << "  setp.ne.b32 %pb" << i << ", %r3, %r3;\n";
+    fast_ = true;
+    emit_powers();
+    emit_walk();
+    emit_fast_exit();
+    fast_ = false;
+    finish_entry();
+  }
+
   void reset_entry() {
     body_.str("");
     body_.clear();
@@ -370,6 +415,10 @@ class Emitter {
       param(".param .u64 pe_list");
       param(".param .u64 pe_count");
       param(".param .u64 pe_cap");
+    }
+    if (img.iv_partition) {
+      param(".param .u64 pe_pidx");
+      param(".param .u64 pe_pcnt");
     }
     if (n_param_ > 0) param(".param .align 16 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
     m << ")\n.maxntid " << maxntid << ", 1, 1\n";
@@ -608,6 +657,16 @@ class Emitter {
           << "  mul.wide.u32 %rd1, %r1, %r2;\n  mul.lo.u64 %rd1, %rd1, " << P_ << ";\n"
           << "  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
           << "  ld.param.u64 %rd3, [pe_n];\n";
+    if (gather_) {
+      // thread j of the grid takes list slot j; %rd3 becomes the list length
+      // (device counter), %rd19 keeps n; a CTA past the end leaves as a whole
+      body_ << "  mov.u64 %rd19, %rd3;\n  ld.param.u64 %rd22, [pe_pcnt];\n"
+            << "  cvta.to.global.u64 %rd22, %rd22;\n  ld.global.u32 %r4, [%rd22+"
+            << (gather_ == 2 ? 4 : 0) << "];\n  cvt.u64.u32 %rd3, %r4;\n"
+            << "  mul.wide.u32 %rd22, %r1, %r2;\n  mul.lo.u64 %rd22, %rd22, " << P_ << ";\n"
+            << "  setp.ge.u64 %p1, %rd22, %rd3;\n  @%p1 bra $Ldone;\n"
+            << "  ld.param.u64 %rd21, [pe_pidx];\n  cvta.to.global.u64 %rd21, %rd21;\n";
+    }
     emit_chain_warmup();
     if (sync_every_ == 0) {
       // no CTA barriers: threads past the end leave immediately; with
@@ -622,7 +681,14 @@ class Emitter {
     for (std::uint32_t k = 0; k < P_; ++k) {
       body_ << "  cvt.u64.u32 %rd13, %r2;\n  mul.lo.u64 %rd13, %rd13, " << k << ";\n"
             << "  add.u64 %rd13, %rd1, %rd13;\n  setp.lt.u64 %pv" << k << ", %rd13, %rd3;\n"
-            << "  min.u64 %rd13, %rd13, %rd12;\n  shl.b64 %ix" << k << ", %rd13, 3;\n";
+            << "  min.u64 %rd13, %rd13, %rd12;\n";
+      if (gather_) {
+        // list slot -> point index (front of the list, or back for x < 0)
+        if (gather_ == 2) body_ << "  sub.u64 %rd13, %rd19, %rd13;\n  sub.u64 %rd13, %rd13, 1;\n";
+        body_ << "  shl.b64 %rd22, %rd13, 2;\n  add.u64 %rd22, %rd21, %rd22;\n"
+              << "  ld.global.u32 %r5, [%rd22];\n  cvt.u64.u32 %rd13, %r5;\n";
+      }
+      body_ << "  shl.b64 %ix" << k << ", %rd13, 3;\n";
     }
     for (std::uint32_t v = 0; v < s_.nvars; ++v) {
       for (std::uint32_t k = 0; k < P_; ++k) {
@@ -653,6 +719,17 @@ class Emitter {
           for (std::uint32_t j = 1; j < K_; ++j) {
             body_ << "  shr.s64 " << lb(xr(i, k), j) << ", " << xi(i, k) << ", 63;\n";
           }
+        }
+      }
+    }
+    if (iv && gather_ == 2) {
+      // mirrored program: evaluate q at -x = [-hi, -lo]
+      for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+        for (std::uint32_t k = 0; k < P_; ++k) {
+          const std::string t = tmp_f();
+          body_ << "  neg.f64 " << t << ", " << xr(v, k, true) << ";\n"
+                << "  neg.f64 " << xr(v, k, true) << ", " << xr(v, k, false) << ";\n"
+                << "  mov.f64 " << xr(v, k, false) << ", " << t << ";\n";
         }
       }
     }
@@ -708,7 +785,8 @@ class Emitter {
             body_ << "  mov.f64 " << pw(id, k, false) << ", " << xr(p.var, k, false) << ";\n"
                   << "  mov.f64 " << pw(id, k, true) << ", " << xr(p.var, k, true) << ";\n";
             if (fast_) {
-              fcheck_straddle({pw(id, k, false), pw(id, k, true)});
+              // partitioned entries: the classifier guarantees 0 < lo
+              if (!gather_) fcheck_straddle({pw(id, k, false), pw(id, k, true)});
               fcheck_finite(pw(id, k, false));
               fcheck_finite(pw(id, k, true));
             }
@@ -751,6 +829,8 @@ class Emitter {
       if (p.exponent > 1 && static_signs_) {
         psign_[i] = p.lo == p.hi ? 1 : psign_[p.lo] * psign_[p.hi];
       }
+      if (p.exponent == 1 && fast_ && gather_ && static_signs_) psign_[i] = 1;  // 0 < x (classifier)
+      if (p.exponent == 1 && fast_ && xsign_probe_) psign_[i] = xsign_probe_;  // experiment only
     }
   }
 
@@ -1571,6 +1651,15 @@ class Emitter {
   std::uint32_t K_ = 1;  // I64K limbs
   bool fast_ = false;  // emitting the interval fast path
   bool medium_ = false;  // emitting the finite-case replay of the fixup entry
+  std::uint32_t part_ = 0;    // KernelShape::iv_partition
+  std::uint32_t gather_ = 0;  // emitting a partitioned entry: 1 front (x > 0), 2 back (x < 0)
+  // PE_IV_XSIGN=+1/-1: measurement probe only (NOT exact for other inputs):
+  // treat every coordinate as having that sign, to bound what a
+  // sign-partitioned fast path could gain
+  int xsign_probe_ = [] {
+    const char* e = std::getenv("PE_IV_XSIGN");
+    return e ? std::atoi(e) : 0;
+  }();
   bool mid_replay_ = [] {  // PE_IV_MID=0: fixup entry = bit-level replay only
     const char* e = std::getenv("PE_IV_MID");
     return !(e && std::atoi(e) == 0);

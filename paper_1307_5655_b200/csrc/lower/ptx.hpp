@@ -55,6 +55,13 @@ struct KernelImage {
   std::uint32_t limbs = 1;         // I64K: 64-bit words per value (= result arrays)
   std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
+  // sign-partitioned interval fast path (univariate): 1 = this module also
+  // has `part_entry` (points with x > 0, taken from the front of a device
+  // index list); 2 = module of the mirrored program q(y) = p(-y) whose only
+  // entry `entry` takes points with x < 0 from the back of the list and
+  // evaluates q at -x. Both entries take two extra parameters (list, counts).
+  std::uint32_t iv_partition = 0;
+  std::string part_entry;
   std::uint32_t fix_block = 128;   // fixup kernel CTA size (.maxntid)
   std::uint32_t fix_ctas_per_sm = 4;  // fixup grid: CTAs per SM (.minnctapersm)
   // instruction counts per point (roofline bookkeeping)
@@ -86,6 +93,8 @@ struct KernelShape {
   // .minnctapersm of the walk entry (0 = none): caps ptxas at
   // 65536 / (block * min_ctas) registers
   std::uint32_t min_ctas = 0;
+  // interval fast path partition role (KernelImage::iv_partition)
+  std::uint32_t iv_partition = 0;
 };
 
 /// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC

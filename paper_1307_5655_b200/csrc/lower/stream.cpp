@@ -3,6 +3,7 @@
 // power tables: powers.hpp:50-72.
 #include "lower/stream.hpp"
 
+#include <cstdint>
 #include <map>
 #include <stdexcept>
 
@@ -81,10 +82,13 @@ struct Lowerer {
   Stream<C>& s;
   const std::vector<std::vector<std::uint32_t>>& pow_of;
 
+  std::uint8_t cur_odd = 0;  // strict: parity of the record being lowered
+
   Operand new_reg() { return Operand::reg(s.nregs++); }
   Operand coef(const C& c, std::uint32_t widen = 0) {
     s.coefs.push_back(c);
     s.widen.push_back(widen);
+    s.odd.push_back(cur_odd);
     return Operand::coef(static_cast<std::uint32_t>(s.coefs.size() - 1));
   }
   Operand power(const CompiledProgram<C>& p, std::uint32_t slot) {
@@ -97,7 +101,11 @@ struct Lowerer {
       ++s.n_add;
       ++s.n_zero_add;
       ++s.n_folded;
-      return coef(s.coefs[b.id], s.widen[b.id] + 1);
+      const std::uint8_t keep = cur_odd;
+      cur_odd = s.odd[b.id];
+      Operand r = coef(s.coefs[b.id], s.widen[b.id] + 1);
+      cur_odd = keep;
+      return r;
     }
     Operand d = new_reg();
     s.ops.push_back(Op{k, d.id, a, b, c});
@@ -116,8 +124,24 @@ struct Lowerer {
   Operand strict(const CompiledProgram<C>& p) {
     std::vector<Operand> m(p.register_count, Operand::zero());
     const std::size_t last = p.records.size() - 1;
+    // parity of each record's absolute exponent: its own power plus its
+    // ancestors' (a record's value is added into the register its parent
+    // reads and multiplies by the parent's power)
+    std::vector<std::uint8_t> par(p.records.size(), 0);
+    if (!p.records.empty()) {
+      const auto parent = parent_records(p);
+      for (std::size_t i = p.records.size(); i-- > 0;) {
+        const auto& rec = p.records[i];
+        std::uint32_t d = 0;
+        if (rec.power_slot) d = p.exponent_sets.at(p.variable).exponents.at(*rec.power_slot);
+        const std::uint8_t up = parent[i] == UINT32_MAX ? 0 : par[parent[i]];
+        par[i] = static_cast<std::uint8_t>((d + up) & 1u);
+        if (rec.sub) s.mirrorable = false;
+      }
+    }
     for (std::size_t i = 0; i <= last; ++i) {
       const auto& rec = p.records[i];
+      cur_odd = par[i];
       Operand v = rec.sub ? strict(*rec.sub) : coef(rec.coeff);  // L224
       if (rec.reads_register) {                                   // L225-228
         v = emit(OpKind::Add, m[rec.lazy_slot], v);
@@ -215,11 +239,29 @@ Stream<C> lower_strict(const CompiledProgram<C>& program) {
   Stream<C> s;
   s.strict = true;
   s.nvars = static_cast<std::uint32_t>(program.variable_count);
+  s.mirrorable = s.nvars == 1;
   const auto pow_of = build_powers(program, s);
   Lowerer<C> L{s, pow_of};
   s.result = L.strict(program);
   return s;
 }
+
+template <typename C>
+bool mirror_stream(const Stream<C>& s, Stream<C>* out) {
+  if (!s.strict || !s.mirrorable || s.odd.size() != s.coefs.size()) return false;
+  *out = s;
+  for (std::size_t k = 0; k < s.coefs.size(); ++k) {
+    if (!s.odd[k]) continue;
+    if constexpr (std::is_same_v<C, std::int64_t>) {
+      if (s.coefs[k] == INT64_MIN) return false;
+    }
+    out->coefs[k] = -s.coefs[k];
+  }
+  return true;
+}
+
+template bool mirror_stream(const Stream<double>&, Stream<double>*);
+template bool mirror_stream(const Stream<std::int64_t>&, Stream<std::int64_t>*);
 
 template <typename C>
 Stream<C> lower_fused(const CompiledProgram<C>& program) {

@@ -74,6 +74,11 @@ struct Stream {
   // injected (an interval zero-add of a constant, [next_down(0 + c.lo),
   // next_up(0 + c.hi)], folded on the host; fp64 0.0 + c == c needs none)
   std::vector<std::uint32_t> widen;
+  // strict univariate streams: parity of the absolute exponent of the term
+  // coefficient k belongs to (mirror_stream); `mirrorable` is false when the
+  // program has nested sub-programs
+  std::vector<std::uint8_t> odd;
+  bool mirrorable = false;
   std::uint32_t nregs = 0;         // virtual registers used by `ops`
   Operand result;                  // Reg, Coef or Zero
   bool strict = false;
@@ -92,6 +97,14 @@ Stream<C> lower_strict(const CompiledProgram<C>& program);
 
 template <typename C>
 Stream<C> lower_fused(const CompiledProgram<C>& program);
+
+/// The strict stream of q(y) = p(-y): the same walk with the coefficients of
+/// odd-exponent terms negated. Every primitive of the interval walk (RN
+/// add/mul, nextafter, the product hull) commutes with negation, so q's walk
+/// at -x mirrors p's at x register for register and ends in p(x) itself.
+/// Returns false (no mirror) for nested programs or an unnegatable int64.
+template <typename C>
+bool mirror_stream(const Stream<C>& s, Stream<C>* out);
 
 /// Stable 64-bit FNV-1a over arbitrary bytes (cache keys, stream hashes).
 inline std::uint64_t fnv1a(const void* data, std::size_t n,

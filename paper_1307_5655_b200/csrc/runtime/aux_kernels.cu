@@ -190,3 +190,106 @@ extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s
   *ops_per_s = static_cast<double>(blocks) * threads * iters * 8 / (best_ms * 1e-3);
   return e;
 }
+
+// ---------------------------------------------------------------------------
+// classify_intervals: the sign partition of the univariate interval fast path
+// (lower/ptx.cpp, KernelImage::iv_partition). Interval i = [lo_i, hi_i] goes
+//   lo > 0           -> idx[front++]      (x > 0 entry of the program)
+//   hi < 0           -> idx[n-1-back++]   (x < 0 entry of the mirrored program)
+//   otherwise        -> fixup list        (straddles / touches zero, NaN)
+// and invalid intervals (NaN endpoint, lo > hi: reference interval.cpp:21-26)
+// set bit 2 of the status word, a full fixup list bit 4 — the same status
+// contract as the walk kernels. Each warp owns 512 consecutive intervals
+// (16 rounds of 32, ballots kept in registers), so every list keeps point
+// order inside a warp's range and the walk kernels' gathers stay coalesced;
+// one atomicAdd per CTA and list. HBM-bound: 16 B read + <= 4 B written per
+// interval.
+namespace {
+constexpr int kClsThreads = 256, kClsRounds = 16;
+constexpr int kClsTile = kClsThreads * kClsRounds;
+
+__global__ void __launch_bounds__(kClsThreads) classify_intervals_kernel(
+    const double* __restrict__ lo, const double* __restrict__ hi, unsigned long long n,
+    unsigned* __restrict__ idx, unsigned* __restrict__ counts, unsigned* __restrict__ fix_list,
+    unsigned* __restrict__ fix_count, unsigned long long fix_cap, unsigned* __restrict__ flag) {
+  __shared__ unsigned s_pos[kClsThreads / 32], s_neg[kClsThreads / 32];
+  __shared__ unsigned s_base_pos, s_base_neg;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long w0 =
+      static_cast<unsigned long long>(blockIdx.x) * kClsTile + static_cast<unsigned long long>(warp) * 32 * kClsRounds;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned mpos[kClsRounds], mneg[kClsRounds];
+  unsigned npos = 0, nneg = 0;
+#pragma unroll
+  for (int r = 0; r < kClsRounds; ++r) {
+    const unsigned long long i = w0 + static_cast<unsigned long long>(r) * 32 + lane;
+    bool pos = false, neg = false, other = false;
+    if (i < n) {
+      const double l = __ldg(lo + i), h = __ldg(hi + i);
+      const bool valid = l <= h;  // false for NaN endpoints
+      if (!valid) atomicOr(flag, 2u);
+      pos = valid && l > 0.0;
+      neg = valid && h < 0.0;
+      other = !pos && !neg;
+    }
+    mpos[r] = __ballot_sync(0xffffffffu, pos);
+    mneg[r] = __ballot_sync(0xffffffffu, neg);
+    const unsigned mo = __ballot_sync(0xffffffffu, other);
+    if (mo) {  // rare: straddling / zero-touching / invalid intervals
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(fix_count, static_cast<unsigned>(__popc(mo)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (other) {
+        const unsigned long long slot = static_cast<unsigned long long>(base) + __popc(mo & lt);
+        if (slot < fix_cap) {
+          fix_list[slot] = static_cast<unsigned>(i);
+        } else {
+          atomicOr(flag, 4u);
+        }
+      }
+    }
+    npos += __popc(mpos[r]);
+    nneg += __popc(mneg[r]);
+  }
+  if (lane == 0) {
+    s_pos[warp] = npos;
+    s_neg[warp] = nneg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned tp = 0, tn = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      const unsigned p = s_pos[w], q = s_neg[w];
+      s_pos[w] = tp;
+      s_neg[w] = tn;
+      tp += p;
+      tn += q;
+    }
+    s_base_pos = tp ? atomicAdd(&counts[0], tp) : 0;
+    s_base_neg = tn ? atomicAdd(&counts[1], tn) : 0;
+  }
+  __syncthreads();
+  unsigned op = s_base_pos + s_pos[warp], on = s_base_neg + s_neg[warp];
+#pragma unroll
+  for (int r = 0; r < kClsRounds; ++r) {
+    const unsigned i = static_cast<unsigned>(w0 + static_cast<unsigned long long>(r) * 32 + lane);
+    if ((mpos[r] >> lane) & 1u) idx[op + __popc(mpos[r] & lt)] = i;
+    if ((mneg[r] >> lane) & 1u) idx[n - 1 - (on + __popc(mneg[r] & lt))] = i;
+    op += __popc(mpos[r]);
+    on += __popc(mneg[r]);
+  }
+}
+}  // namespace
+
+extern "C" cudaError_t pe_launch_classify_intervals(const double* lo, const double* hi,
+                                                    unsigned long long n, unsigned* idx,
+                                                    unsigned* counts, unsigned* fix_list,
+                                                    unsigned* fix_count,
+                                                    unsigned long long fix_cap, unsigned* flag,
+                                                    cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const unsigned long long grid = (n + kClsTile - 1) / kClsTile;
+  classify_intervals_kernel<<<static_cast<unsigned>(grid), kClsThreads, 0, stream>>>(
+      lo, hi, n, idx, counts, fix_list, fix_count, fix_cap, flag);
+  return cudaGetLastError();
+}

@@ -65,6 +65,12 @@ void bind_functions(Artifact& a, int device) {
       a.fix_fn[device] = f;
     }
   }
+  if (!a.part_fn[device] && a.part_kernel) {
+    CUfunction f = nullptr;
+    if (driver().get_function(&f, reinterpret_cast<CUkernel>(a.part_kernel)) == CUDA_SUCCESS) {
+      a.part_fn[device] = f;
+    }
+  }
 }
 
 std::atomic<std::uint64_t>& launch_counter() {
@@ -85,12 +91,23 @@ int sm_count(int device) {
   return n;
 }
 
-void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
+extern "C" cudaError_t pe_launch_classify_intervals(const double* lo, const double* hi,
+                                                    unsigned long long n, unsigned* idx,
+                                                    unsigned* counts, unsigned* fix_list,
+                                                    unsigned* fix_count,
+                                                    unsigned long long fix_cap, unsigned* flag,
+                                                    cudaStream_t stream);
+
+namespace {
+// Kernel argument values of one module, in entry_text's parameter order
+// (the parameter-tier coefficient array is appended by the caller).
+std::vector<std::uint64_t> arg_values(const Artifact& a, int device, const LaunchArgs& la,
+                                      std::uint64_t pidx, std::uint64_t pcnt) {
   const auto& img = a.image;
   std::uint64_t gcoef = 0;
   if (!img.global_words.empty()) gcoef = reinterpret_cast<std::uint64_t>(a.global_coefs.at(device));
   std::vector<std::uint64_t> vals;
-  vals.reserve(img.n_in + img.n_out + 4 + img.nvars);
+  vals.reserve(img.n_in + img.n_out + 8 + img.nvars);
   for (auto v : la.ins) vals.push_back(v);
   for (auto v : la.outs) vals.push_back(v);
   vals.push_back(la.n);
@@ -100,16 +117,78 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     for (std::uint32_t v = 0; v < img.nvars; ++v) vals.push_back(la.bounds.at(v));
   }
   if (img.interval_fast_path) {
-    if (!la.list || !la.count) throw std::logic_error("interval fast path needs a fixup list");
     vals.push_back(la.list);
     vals.push_back(la.count);
     vals.push_back(la.cap);
+  }
+  if (img.iv_partition) {
+    vals.push_back(pidx);
+    vals.push_back(pcnt);
+  }
+  return vals;
+}
+
+std::vector<void*> arg_ptrs(const Artifact& a, std::vector<std::uint64_t>& vals) {
+  std::vector<void*> args;
+  for (auto& v : vals) args.push_back(&v);
+  if (!a.image.param_words.empty()) {
+    args.push_back(const_cast<std::uint64_t*>(a.image.param_words.data()));
+  }
+  return args;
+}
+
+bool partition_min_batch(std::uint64_t n) {
+  // below ~64K intervals the extra launches outweigh the cheaper walk
+  const char* e = std::getenv("PE_IV_PART_MIN");
+  return n >= (e ? static_cast<std::uint64_t>(std::atoll(e)) : std::uint64_t{1} << 16);
+}
+}  // namespace
+
+void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
+  const auto& img = a.image;
+  if (img.interval_fast_path) {
+    if (!la.list || !la.count) throw std::logic_error("interval fast path needs a fixup list");
     check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(la.count), 0, sizeof(unsigned), stream),
                "cudaMemsetAsync(fixup count)");
   }
-  std::vector<void*> args;
-  for (auto& v : vals) args.push_back(&v);
-  if (!img.param_words.empty()) args.push_back(const_cast<std::uint64_t*>(img.param_words.data()));
+  const bool part = a.partitioned() && la.n <= 0xffffffffull && partition_min_batch(la.n);
+  void* scratch = nullptr;  // partition: n u32 point indices + 2 u32 list lengths
+  if (part) {
+    check_cuda(cudaMallocAsync(&scratch, 4 * la.n + 8, stream), "cudaMallocAsync(partition)");
+  }
+  const std::uint64_t pidx = reinterpret_cast<std::uint64_t>(scratch);
+  const std::uint64_t pcnt = part ? pidx + 4 * la.n : 0;
+  std::vector<std::uint64_t> vals = arg_values(a, device, la, pidx, pcnt);
+  std::vector<void*> args = arg_ptrs(a, vals);
+  const bool dev_ok = device >= 0 && device < Artifact::kMaxDevices;
+  if (part) {
+    // sign partition: classify, then the x > 0 entry of this module and the
+    // x < 0 entry of the mirror module, each over its list (device lengths);
+    // intervals touching zero go straight to the fixup list
+    check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(pcnt), 0, 8, stream),
+               "cudaMemsetAsync(partition counts)");
+    check_cuda(pe_launch_classify_intervals(
+                   reinterpret_cast<const double*>(la.ins.at(0)),
+                   reinterpret_cast<const double*>(la.ins.at(1)), la.n,
+                   reinterpret_cast<unsigned*>(pidx), reinterpret_cast<unsigned*>(pcnt),
+                   reinterpret_cast<unsigned*>(la.list), reinterpret_cast<unsigned*>(la.count),
+                   la.cap, reinterpret_cast<unsigned*>(la.flag), stream),
+               "launch(classify)");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    const std::uint64_t tile = static_cast<std::uint64_t>(img.block) * img.lanes;
+    const std::uint64_t grid = (la.n + tile - 1) / tile;
+    if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
+    launch_one(a.part_kernel, dev_ok ? a.part_fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
+               dim3(img.block), args.data(), stream, "launch(walk x>0)");
+    const Artifact& m = *a.mirror;
+    std::vector<std::uint64_t> mvals = arg_values(m, device, la, pidx, pcnt);
+    std::vector<void*> margs = arg_ptrs(m, mvals);
+    const std::uint64_t mtile = static_cast<std::uint64_t>(m.image.block) * m.image.lanes;
+    launch_one(m.kernel, dev_ok ? m.fn[device] : nullptr,
+               dim3(static_cast<unsigned>((la.n + mtile - 1) / mtile)), dim3(m.image.block),
+               margs.data(), stream, "launch(walk x<0)");
+    launch_counter().fetch_add(2, std::memory_order_relaxed);
+  }
   // Small batches: shrink the CTA (the kernel reads its tile size from
   // %ntid; .maxntid is only an upper bound) until every SM has work. Looped
   // kernels (tiny code, no instruction-fetch sharing to lose) split finer,
@@ -122,10 +201,11 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   const std::uint64_t tile = block * img.lanes;
   const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
-  launch_one(a.kernel, device >= 0 && device < Artifact::kMaxDevices ? a.fn[device] : nullptr,
-             dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)), args.data(),
-             stream, "launch(walk)");
-  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  if (!part) {
+    launch_one(a.kernel, dev_ok ? a.fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
+               dim3(static_cast<unsigned>(block)), args.data(), stream, "launch(walk)");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+  }
   if (img.interval_fast_path) {
     // strict replay of the points the fast path could not prove; it reads
     // the list length on the device, so no host round trip in between
@@ -145,10 +225,11 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
       cudaEventDestroy(ev);
       fs = la.fix_stream;
     }
-    launch_one(a.fix_kernel, device >= 0 && device < Artifact::kMaxDevices ? a.fix_fn[device] : nullptr,
+    launch_one(a.fix_kernel, dev_ok ? a.fix_fn[device] : nullptr,
                dim3(fix_grid ? fix_grid : 1), dim3(static_cast<unsigned>(fb)), args.data(), fs, "launch(fixup)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   }
+  if (scratch) check_cuda(cudaFreeAsync(scratch, stream), "cudaFreeAsync(partition)");
 }
 
 

@@ -103,13 +103,45 @@ std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits) {
   return out;
 }
 
+namespace {
+bool partition_enabled() {
+  const char* e = std::getenv("PE_IV_PART");
+  return !(e && std::atoi(e) == 0);
+}
+
+// Interval domain: the program's kernel (+ the mirror module when the sign
+// partition applies, see lower/ptx.cpp and lower::mirror_stream).
+template <typename C>
+void emit_interval(const CompiledProgram<C>& prog, std::uint32_t nvars, Artifact& a) {
+  lower::KernelShape shape;
+  if (nvars == 1 && partition_enabled()) shape.iv_partition = 1;
+  const auto s = lower::lower_strict(prog);
+  a.image = lower::emit_ptx(s, lower::Domain::Interval, shape);
+  lower::Stream<C> q;
+  if (a.image.iv_partition != 1 || !lower::mirror_stream(s, &q)) return;
+  lower::KernelShape ms;
+  ms.iv_partition = 2;
+  auto m = std::make_unique<Artifact>();
+  m->image = lower::emit_ptx(q, lower::Domain::Interval, ms);
+  if (m->image.iv_partition == 2) a.mirror = std::move(m);
+}
+}  // namespace
+
 Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
   std::lock_guard<std::mutex> lock(mu);
   auto& slot = artifacts[static_cast<int>(d)];
   if (!slot) {
     auto a = std::make_unique<Artifact>();
     const bool strict = d == lower::Domain::F64Strict || d == lower::Domain::Interval;
-    if (integer) {
+    if (d == lower::Domain::Interval) {
+      // univariate programs get the sign-partitioned fast path: this module
+      // gains an x > 0 entry, a mirror module evaluates q(y) = p(-y) at -x
+      if (integer) {
+        emit_interval(*prog_i, nvars, *a);
+      } else {
+        emit_interval(*prog_f, nvars, *a);
+      }
+    } else if (integer) {
       auto s = strict ? lower::lower_strict(*prog_i) : lower::lower_fused(*prog_i);
       a->image = lower::emit_ptx(s, d);
     } else {
@@ -126,6 +158,12 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
     if (!r.ok) throw std::logic_error(r.log);
     slot->cubin = std::move(r.cubin);
     slot->compile_seconds = r.seconds;
+  }
+  if (need_cubin && slot->mirror && slot->mirror->cubin.empty()) {
+    CompileResult r = compile_ptx_cached(slot->mirror->image.ptx, slot->mirror->image.entry);
+    if (!r.ok) throw std::logic_error(r.log);
+    slot->mirror->cubin = std::move(r.cubin);
+    slot->mirror->compile_seconds = r.seconds;
   }
   return *slot;
 }
@@ -290,8 +328,13 @@ void ensure_loaded(Artifact& a, int device) {
       check_cuda(cudaLibraryGetKernel(&a.fix_kernel, a.library, a.image.fix_entry.c_str()),
                  "cudaLibraryGetKernel(fix)");
     }
+    if (!a.image.part_entry.empty()) {
+      check_cuda(cudaLibraryGetKernel(&a.part_kernel, a.library, a.image.part_entry.c_str()),
+                 "cudaLibraryGetKernel(part)");
+    }
     bind_functions(a, device);
   }
+  if (a.mirror) ensure_loaded(*a.mirror, device);
   if (!a.image.global_words.empty() && !a.global_coefs.count(device)) {
     void* p = nullptr;
     const size_t bytes = a.image.global_words.size() * 8;

@@ -32,6 +32,10 @@ struct Artifact {
   cudaLibrary_t library = nullptr;
   cudaKernel_t kernel = nullptr;
   cudaKernel_t fix_kernel = nullptr;  // interval fast path: strict replay of listed points
+  cudaKernel_t part_kernel = nullptr; // sign-partitioned fast path: x > 0 entry
+  // sign-partitioned fast path: the mirrored program q(y) = p(-y), whose
+  // kernel takes the x < 0 points (KernelImage::iv_partition == 2)
+  std::unique_ptr<Artifact> mirror;
   std::map<int, void*> global_coefs;  // per device: global-tier coefficient words
   // per device ordinal: CUfunction of kernel / fix_kernel in that device's
   // primary context (driver-API launches skip the runtime's per-launch
@@ -39,6 +43,12 @@ struct Artifact {
   static constexpr int kMaxDevices = 64;
   std::array<void*, kMaxDevices> fn{};
   std::array<void*, kMaxDevices> fix_fn{};
+  std::array<void*, kMaxDevices> part_fn{};
+  /// The sign partition can run: this module has the x > 0 entry and the
+  /// mirror module was generated with its x < 0 entry.
+  bool partitioned() const {
+    return image.iv_partition == 1 && mirror && mirror->image.iv_partition == 2;
+  }
 };
 
 /// Resolves a.fn / a.fix_fn for `device` (current device = `device`).

@@ -468,3 +468,60 @@ def test_chain_loops_inside_nested_programs(cuda_device):
         got = pe.Evaluator(pe.BigIntDomain(int_pipe=int_pipe), prog_i).evaluate(
             [_t(a, cuda_device) for a in xi]).cpu().numpy()
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [1, 5, 33, 4097, 150_001])
+@pytest.mark.parametrize("scheme", ["estrin", "horner", "balanced"])
+def test_interval_sign_partition_bit_exact(n, scheme, cuda_device, monkeypatch):
+    # Sign-partitioned fast path: x > 0 intervals run the program's x > 0
+    # entry, x < 0 intervals the mirrored program q(y) = p(-y) at -x, the
+    # rest (touching / straddling zero, invalid) the fixup replay. Results
+    # must equal the unpartitioned kernel and the oracle bit for bit, for
+    # every list length (empty lists, partial CTAs, ragged tails).
+    rng = np.random.default_rng(1000 + n)
+    deg = {"estrin": 200, "horner": 37, "balanced": 64}[scheme]
+    p = pe.Polynomial(np.arange(deg, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, deg + 1))
+    x = rng.uniform(-1, 1, n)
+    w = np.where(rng.uniform(size=n) < 0.05, rng.uniform(0, 0.3, n), 1e-6)
+    lo, hi = x.copy(), x + w
+    k = min(n, 40)
+    lo[: k // 4] = 0.0                         # touches zero
+    hi[: k // 4] = np.abs(hi[: k // 4]) + 1e-9
+    lo[k // 4: k // 2] = -np.abs(lo[k // 4: k // 2])
+    hi[k // 4: k // 2] = -0.0                  # negative side touching -0
+    if n > 100:
+        lo[50:60], hi[50:60] = 1e-200, 2e-200  # tiny positive: underflow -> fixup
+        lo[60:70], hi[60:70] = -2e-200, -1e-200
+        lo[70:80], hi[70:80] = 1e150, 2e150    # overflow
+        lo[80:90], hi[80:90] = -2e150, -1e150
+    monkeypatch.setenv("PE_IV_PART_MIN", "1")
+    part = pe.compile(p, pe.builtin_scheme(scheme))
+    f = pe.Evaluator(pe.IntervalDomain(), part).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
+    assert "pe_walk_interval_pos" in part.ptx(pe.DOMAIN_INTERVAL)
+    monkeypatch.setenv("PE_IV_PART", "0")
+    plain = pe.compile(p, pe.builtin_scheme(scheme))
+    g = pe.Evaluator(pe.IntervalDomain(), plain).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
+    assert "pe_walk_interval_pos" not in plain.ptx(pe.DOMAIN_INTERVAL)
+    o = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
+    for a, b, c in zip(f, g, o):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.array_equal(a.view(np.int64), c.view(np.int64))
+        assert np.array_equal(b.view(np.int64), c.view(np.int64))
+
+
+def test_interval_sign_partition_host_buffers_and_errors(cuda_device, monkeypatch):
+    # host (pinned-staging) path through the partition, and the invalid-
+    # interval status raised by the classifier
+    monkeypatch.setenv("PE_IV_PART_MIN", "1")
+    wl = W.c5()
+    prog = pe.compile(wl.poly, wl.schemes)
+    lo, hi = wl.points(300_000)
+    ev = pe.Evaluator(pe.IntervalDomain(), prog)
+    got = ev.evaluate((lo, hi))
+    o = pyoracle.Oracle(wl.poly, wl.schemes).eval_interval([lo[0][:2000]], [hi[0][:2000]])
+    for a, c in zip(got, o):
+        assert np.array_equal(np.asarray(a)[:2000].view(np.int64), c.view(np.int64))
+    bad_lo = lo[0].copy()
+    bad_lo[12345] = hi[0][12345] + 1.0
+    with pytest.raises(ValueError):
+        ev.evaluate(([bad_lo], hi))
