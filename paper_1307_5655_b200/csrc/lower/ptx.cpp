@@ -1219,11 +1219,24 @@ class Emitter {
   //    operand is inf/NaN, or in the sign of a zero product; a zero's sign
   //    never survives the nextafter step that follows min/max (both +-0 step
   //    to -/+dmin), so plain products and min/max give the same endpoints.
+  //  * the one zero this produces has the wrong sign: RD(dmin - dmin) is -0
+  //    (std::nextafter(dmin, -inf) is +0), so the difference gets + (+0)
+  //    in RN (-0 -> +0, everything else unchanged; next_down never returns
+  //    -0); next_up(v) = -next_down(-v).
   void mnext(const std::string& dst, const std::string& src, bool up) {
-    const std::string a = tmp_f(), t = tmp_f();
+    const std::string a = tmp_f(), t = tmp_f(), r = tmp_f();
     body_ << "  abs.f64 " << a << ", " << src << ";\n"
-          << "  fma.rn.f64 " << t << ", " << a << ", 0d3C30000000000000, 0d0000000000000001;\n"
-          << (up ? "  add.rp.f64 " : "  sub.rm.f64 ") << dst << ", " << src << ", " << t << ";\n";
+          << "  fma.rn.f64 " << t << ", " << a << ", 0d3C30000000000000, 0d0000000000000001;\n";
+    if (up) {
+      const std::string ns = tmp_f(), q = tmp_f();
+      body_ << "  neg.f64 " << ns << ", " << src << ";\n"
+            << "  sub.rm.f64 " << r << ", " << ns << ", " << t << ";\n"
+            << "  add.rn.f64 " << q << ", " << r << ", 0d0000000000000000;\n"
+            << "  neg.f64 " << dst << ", " << q << ";\n";
+    } else {
+      body_ << "  sub.rm.f64 " << r << ", " << src << ", " << t << ";\n"
+            << "  add.rn.f64 " << dst << ", " << r << ", 0d0000000000000000;\n";
+    }
     // inf or NaN result (DBL_MAX up, +inf down, overflow) poisons the
     // accumulator (0 * inf = NaN): the point then takes the exact replay
     body_ << "  fma.rn.f64 %macc, " << dst << ", 0d0000000000000000, %macc;\n";

@@ -128,7 +128,7 @@ struct Lowerer {
     // ancestors' (a record's value is added into the register its parent
     // reads and multiplies by the parent's power)
     std::vector<std::uint8_t> par(p.records.size(), 0);
-    if (!p.records.empty()) {
+    if (s.mirrorable && !p.records.empty()) {  // univariate only
       const auto parent = parent_records(p);
       for (std::size_t i = p.records.size(); i-- > 0;) {
         const auto& rec = p.records[i];

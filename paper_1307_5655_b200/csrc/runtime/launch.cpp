@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 
 namespace polyeval::rt {
@@ -137,6 +139,22 @@ std::vector<void*> arg_ptrs(const Artifact& a, std::vector<std::uint64_t>& vals)
   return args;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; with its default release threshold (0) every synchronisation hands
+// the memory back to the driver and the next call maps it again (C5: 400 MB
+// per 1e8-interval call, ~4 ms). Keep it pooled instead.
+void keep_pool_memory(int device) {
+  static std::mutex m;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lock(m);
+  if (!done.insert(device).second) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    std::uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+
 bool partition_min_batch(std::uint64_t n) {
   // below ~64K intervals the extra launches outweigh the cheaper walk
   const char* e = std::getenv("PE_IV_PART_MIN");
@@ -154,6 +172,7 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   const bool part = a.partitioned() && la.n <= 0xffffffffull && partition_min_batch(la.n);
   void* scratch = nullptr;  // partition: n u32 point indices + 2 u32 list lengths
   if (part) {
+    keep_pool_memory(device);
     check_cuda(cudaMallocAsync(&scratch, 4 * la.n + 8, stream), "cudaMallocAsync(partition)");
   }
   const std::uint64_t pidx = reinterpret_cast<std::uint64_t>(scratch);

@@ -164,7 +164,7 @@ def test_interval_fixup_entry_has_finite_case_replay(monkeypatch):
     ptx = prog.ptx(pe.DOMAIN_INTERVAL)
     fix = ptx[ptx.index(".entry pe_walk_interval_fix"):]
     assert "%macc" in fix and "@%pmid bra $Lexact" in fix
-    assert "sub.rm.f64" in fix and "add.rp.f64" in fix
+    assert "sub.rm.f64" in fix and "add.rn.f64 %tf" in fix
     assert "bra $Lfix" not in fix
     monkeypatch.setenv("PE_IV_MID", "0")
     ptx0 = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
