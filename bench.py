@@ -440,7 +440,10 @@ def run_native(args, world, rank, local):
                        f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes "
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "ops": f"{algo_per_pt} {unit_ops} per point (SURVEY 8d F) x {n} points per launch",
-        "kernel": f"pe_walk_{domain} [{wls[top].name}]",
+        "kernel": (f"classify_intervals + pe_walk_interval_pos + pe_walk_interval_neg + "
+                   f"pe_walk_interval_fix [{wls[top].name}] (one evaluate call, sign-partitioned)"
+                   if domain == "interval" and "pe_walk_interval_pos" in progs[top].ptx(pe.DOMAIN_INTERVAL)
+                   else f"pe_walk_{domain} [{wls[top].name}]"),
         "issued_fp64_per_point": st["fp_ops"], "issued_int64_per_point": st["int_ops"],
         "hbm_frac": (bytes_in + bytes_out) / (avg[top] * 1e-3) / 1e9 /
                     json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else None,
