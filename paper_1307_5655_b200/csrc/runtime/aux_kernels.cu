@@ -220,12 +220,20 @@ __global__ void __launch_bounds__(kClsThreads) classify_intervals_kernel(
   const unsigned lt = (1u << lane) - 1u;
   unsigned mpos[kClsRounds], mneg[kClsRounds];
   unsigned npos = 0, nneg = 0;
+  // all 16 rounds' loads in flight before the first ballot
+  double vl[kClsRounds], vh[kClsRounds];
+#pragma unroll
+  for (int r = 0; r < kClsRounds; ++r) {
+    const unsigned long long i = w0 + static_cast<unsigned long long>(r) * 32 + lane;
+    vl[r] = i < n ? __ldg(lo + i) : 0.0;
+    vh[r] = i < n ? __ldg(hi + i) : 0.0;
+  }
 #pragma unroll
   for (int r = 0; r < kClsRounds; ++r) {
     const unsigned long long i = w0 + static_cast<unsigned long long>(r) * 32 + lane;
     bool pos = false, neg = false, other = false;
     if (i < n) {
-      const double l = __ldg(lo + i), h = __ldg(hi + i);
+      const double l = vl[r], h = vh[r];
       const bool valid = l <= h;  // false for NaN endpoints
       if (!valid) atomicOr(flag, 2u);
       pos = valid && l > 0.0;
