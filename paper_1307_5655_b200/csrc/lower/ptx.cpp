@@ -269,13 +269,13 @@ class Emitter {
     }
     const std::string main_entry = entry_text(img, img.entry, 0, min_ctas_);
 
-    // fixup entry: strict replay of the listed points (grid-stride loop)
+    // fixup entry: exact replay of the listed points, one per thread
     std::string fix_entry;
     if (fast) {
       img.fix_entry = img.entry + "_fix";
       const std::uint32_t lanes = P_, sync = sync_every_;
       P_ = 1;
-      sync_every_ = 0;  // threads leave the grid-stride loop at different trips
+      sync_every_ = 0;  // threads past the list length leave at once
       reset_entry();
       fix_ = true;
       emit_fix_prologue();
@@ -1578,13 +1578,13 @@ class Emitter {
     emit_store();
   }
 
-  // Fixup entry: grid-stride over the first min(count, cap) listed points,
-  // each re-evaluated by the strict replay (inputs were validated by the
-  // main entry).
+  // Fixup entry: thread j takes list slot j of the first min(count, cap)
+  // listed points and re-evaluates it (finite-case replay, then the
+  // bit-level replay if needed); inputs were validated by the main entry or
+  // the classifier.
   void emit_fix_prologue() {
     body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
           << "  mul.wide.u32 %rd1, %r1, %r2;\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
-          << "  mov.u32 %r4, %nctaid.x;\n  mul.wide.u32 %rd2, %r4, %r2;\n"
           << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
           << "  ld.global.u32 %r5, [%rd14];\n  cvt.u64.u32 %rd3, %r5;\n"
           << "  ld.param.u64 %rd16, [pe_cap];\n  min.u64 %rd3, %rd3, %rd16;\n"
