@@ -187,7 +187,7 @@ std::vector<ChainRun> chain_runs(const Stream<C>& s, Domain d, std::uint32_t syn
     std::size_t j = i;
     while (j < n && link(j, &mult)) ++j;
     const std::size_t len = j - i;  // ops i..j-1 continue the chain of op i-1
-    const std::uint64_t words = len + 8;  // + prefetch padding
+    const std::uint64_t words = len + 24;  // + prefetch padding (up to 3 trips)
     if (len >= min_run && words <= budget) {
       runs.push_back({i - 1, j - 1, mult});
       budget -= words;
@@ -890,7 +890,7 @@ class Emitter {
     if (warm_mode == 0) return;
     decls_ << "  .reg .b64 %wq<2>;\n  .reg .pred %wp<2>;\n  .reg .b32 %wl;\n";
     for (std::size_t idx = 0; idx < runs_.size(); ++idx) {
-      const std::size_t words = runs_[idx].last - runs_[idx].head + kLoopU;
+      const std::size_t words = runs_[idx].last - runs_[idx].head + loop_depth_ * kLoopU;
       const std::size_t lines = (words + 7) / 8;
       const std::string lbl = "$Lwarm" + std::to_string(idx);
       // for (line = tid; line < lines; line += ntid) touch(line)
@@ -918,20 +918,24 @@ class Emitter {
   // shared memory instead measured slower: 0.70 vs 0.59 ms per 1e7 C1 points,
   // per-thread LDS and +18 registers.)
   void emit_chain_loop(const ChainRun& run, std::size_t idx) {
-    const std::uint32_t U = kLoopU;
+    const std::uint32_t U = kLoopU, D = loop_depth_;
     const std::size_t L = run.last - run.head;
     const std::string arr = "pe_run" + std::to_string(idx);
     std::ostringstream a;
-    a << ".const .align 16 .b64 " << arr << "[" << L + U << "] = {";
-    for (std::size_t j = 0; j < L + U; ++j) {
+    a << ".const .align 16 .b64 " << arr << "[" << L + D * U << "] = {";
+    for (std::size_t j = 0; j < L + D * U; ++j) {
       if (j) a << (j % 8 == 0 ? ",\n  " : ", ");
       a << (j < L ? hex64(words_[coef_lo_[s_.ops[run.head + 1 + j].c.id]]) : "0");
     }
     a << "};\n\n";
     run_arrays_ += a.str();
+    // word sets: %lw0.. (this trip), %lw1.. (next trip), ... (depth D)
+    auto set = [](std::uint32_t d) { return "%lw" + std::to_string(d) + "_"; };
     if (!loop_decls_) {
-      decls_ << "  .reg .b64 %lp;\n  .reg .b32 %lc;\n  .reg .pred %lq;\n  .reg ." << ldty()
-             << " %lw<" << U << ">;\n  .reg ." << ldty() << " %lx<" << U << ">;\n";
+      decls_ << "  .reg .b64 %lp;\n  .reg .b32 %lc;\n  .reg .pred %lq;\n";
+      for (std::uint32_t d = 0; d <= D; ++d) {
+        decls_ << "  .reg ." << ldty() << " " << set(d) << "<" << U << ">;\n";
+      }
       loop_decls_ = true;
     }
     const std::uint32_t acc = s_.ops[run.head].dst;
@@ -940,33 +944,35 @@ class Emitter {
       for (std::uint32_t k = 0; k < P_; ++k) {
         const std::string r = reg(acc, k), m = opnd(run.mult, none, k);
         if (d_ == Domain::I64) {
-          body_ << "  mad.lo.s64 " << r << ", " << r << ", " << m << ", %lw" << u << ";\n";
+          body_ << "  mad.lo.s64 " << r << ", " << r << ", " << m << ", " << set(0) << u << ";\n";
         } else {
-          body_ << "  fma.rn.f64 " << r << ", " << r << ", " << m << ", %lw" << u << ";\n";
+          body_ << "  fma.rn.f64 " << r << ", " << r << ", " << m << ", " << set(0) << u << ";\n";
         }
       }
     };
-    auto load8 = [&](const char* set, std::uint32_t off) {
+    auto load8 = [&](const std::string& st, std::uint32_t off) {
       for (std::uint32_t u = 0; u < U; u += 2) {
-        body_ << "  ld.const.v2." << ldty() << " {" << set << u << ", " << set << u + 1 << "}, [%lp+"
+        body_ << "  ld.const.v2." << ldty() << " {" << st << u << ", " << st << u + 1 << "}, [%lp+"
               << off + 8 * u << "];\n";
       }
     };
     const std::size_t iters = L / U, rem = L % U;
     const std::string lbl = "$Lrun" + std::to_string(idx);
     body_ << "  mov.u64 %lp, " << arr << ";\n";
-    load8("%lw", 0);
+    for (std::uint32_t d = 0; d < D; ++d) load8(set(d), 8 * U * d);
     if (iters > 0) {
       body_ << "  mov.u32 %lc, " << iters << ";\n" << lbl << ":\n";
-      load8("%lx", 8 * U);  // next iteration's words (padding after the last)
+      load8(set(D), 8 * U * D);  // words D trips ahead (padding after the last)
       for (std::uint32_t u = 0; u < U; ++u) step(u);
-      for (std::uint32_t u = 0; u < U; ++u) {
-        body_ << "  mov.b64 %lw" << u << ", %lx" << u << ";\n";
+      for (std::uint32_t d = 0; d < D; ++d) {
+        for (std::uint32_t u = 0; u < U; ++u) {
+          body_ << "  mov.b64 " << set(d) << u << ", " << set(d + 1) << u << ";\n";
+        }
       }
       body_ << "  add.u64 %lp, %lp, " << 8 * U << ";\n  sub.u32 %lc, %lc, 1;\n"
             << "  setp.ne.u32 %lq, %lc, 0;\n  @%lq bra.uni " << lbl << ";\n";
     }
-    for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in %lw
+    for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in set 0
     const std::uint32_t dst = s_.ops[run.last].dst;
     if (dst != acc) {
       for (std::uint32_t k = 0; k < P_; ++k) {
@@ -1732,6 +1738,12 @@ class Emitter {
     return 1;
   }();
   static constexpr std::uint32_t kLoopU = 8;  // loop unroll (steps per trip)
+  // chain-loop prefetch distance in trips (PE_LOOP_DEPTH, 1..3)
+  std::uint32_t loop_depth_ = [] {
+    const char* e = std::getenv("PE_LOOP_DEPTH");
+    const int v = e ? std::atoi(e) : 1;
+    return static_cast<std::uint32_t>(v < 1 ? 1 : v > 3 ? 3 : v);
+  }();
   std::vector<ChainRun> runs_;
   std::string run_arrays_;
   bool loop_decls_ = false;
