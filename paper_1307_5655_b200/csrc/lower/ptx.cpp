@@ -316,25 +316,6 @@ class Emitter {
       sync_every_ = sync;
     }
 
-    // small-batch entry (chain loops read a shared-memory copy)
-    std::string small_entry;
-    std::size_t staged = 0;
-    for (const auto& r : runs_) staged += r.last - r.head + loop_depth_ * kLoopU;
-    if (!runs_.empty() && !fast && !iv && staged <= 5000 && small_entry_enabled()) {
-      img.small_entry = img.entry + "_s";
-      const std::uint64_t fp = fp_ops_, in = int_ops_;  // same walk: count it once
-      reset_entry();
-      smem_loop_ = true;
-      emit_prologue();
-      emit_powers();
-      emit_walk();
-      emit_epilogue();
-      smem_loop_ = false;
-      fp_ops_ = fp;
-      int_ops_ = in;
-      small_entry = entry_text(img, img.small_entry, 0, min_ctas_);
-    }
-
     // positive-coordinate entry of the sign-partitioned fast path
     std::string part_entry;
     if (part) {
@@ -348,8 +329,7 @@ class Emitter {
 
     std::ostringstream m;
     m << module_header(img, fast ? "interval-fast-path+fixup" : "");
-    m << run_arrays_ << (small_entry.empty() ? "" : small_arrays_) << main_entry << fix_entry
-      << part_entry << small_entry;
+    m << run_arrays_ << main_entry << fix_entry << part_entry;
     img.ptx = m.str();
     img.fp_ops = fp_ops_;
     img.int_ops = int_ops_;
@@ -687,11 +667,7 @@ class Emitter {
             << "  setp.ge.u64 %p1, %rd22, %rd3;\n  @%p1 bra $Ldone;\n"
             << "  ld.param.u64 %rd21, [pe_pidx];\n  cvta.to.global.u64 %rd21, %rd21;\n";
     }
-    if (smem_loop_) {
-      emit_smem_staging();
-    } else {
-      emit_chain_warmup();
-    }
+    emit_chain_warmup();
     if (sync_every_ == 0) {
       // no CTA barriers: threads past the end leave immediately; with
       // barriers every thread stays (clamped loads, predicated stores)
@@ -907,30 +883,6 @@ class Emitter {
   // the loop is a single dependent chain of up to L/8 such misses). The
   // loaded word feeds a never-true comparison (coefficient words are finite,
   // the pattern is a NaN) so the load is not dead code. PE_WARM=0 disables.
-  // Small-batch entry: the CTA copies each chain-loop array from its global
-  // copy into shared memory (coalesced 16-byte loads, one barrier) before
-  // any thread leaves; the loop then reads shared memory. After an L2 flush
-  // this replaces one cold constant-cache miss per loop trip (the main
-  // entry's LDCU prefetch is one trip ahead) with one round trip per CTA.
-  void emit_smem_staging() {
-    decls_ << "  .reg .b64 %sq<3>;\n  .reg .pred %sp0;\n  .reg .b32 %sl;\n  .reg .f64 %sv<2>;\n";
-    for (std::size_t idx = 0; idx < runs_.size(); ++idx) {
-      const std::size_t words = runs_[idx].last - runs_[idx].head + loop_depth_ * kLoopU;
-      const std::size_t pairs = (words + 1) / 2;
-      const std::string lbl = "$Lstage" + std::to_string(idx);
-      body_ << "  mov.u64 %sq0, pe_rung" << idx << ";\n  cvta.global.u64 %sq0, %sq0;\n"
-            << "  cvta.to.global.u64 %sq0, %sq0;\n  mov.u64 %sq1, pe_runs" << idx << ";\n"
-            << "  mov.u32 %sl, %r3;\n" << lbl << ":\n"
-            << "  setp.ge.u32 %sp0, %sl, " << pairs << ";\n  @%sp0 bra " << lbl << "e;\n"
-            << "  mul.wide.u32 %sq2, %sl, 16;\n  add.u64 %sq2, %sq0, %sq2;\n"
-            << "  ld.global.nc.v2.f64 {%sv0, %sv1}, [%sq2];\n"
-            << "  mul.wide.u32 %sq2, %sl, 16;\n  add.u64 %sq2, %sq1, %sq2;\n"
-            << "  st.shared.v2.f64 [%sq2], {%sv0, %sv1};\n"
-            << "  add.u32 %sl, %sl, %r2;\n  bra " << lbl << ";\n" << lbl << "e:\n";
-    }
-    body_ << "  bar.sync 0;\n";
-  }
-
   void emit_chain_warmup() {
     if (runs_.empty() || fix_) return;
     int warm_mode = 1;
@@ -968,27 +920,15 @@ class Emitter {
   void emit_chain_loop(const ChainRun& run, std::size_t idx) {
     const std::uint32_t U = kLoopU, D = loop_depth_;
     const std::size_t L = run.last - run.head;
-    // constant-bank array (main entry); the small-batch entry reads a shared
-    // copy staged from a global copy (emit_smem_staging)
-    const std::string arr = (smem_loop_ ? "pe_runs" : "pe_run") + std::to_string(idx);
-    if (!smem_loop_) {
-      std::ostringstream a;
-      a << ".const .align 16 .b64 " << arr << "[" << L + D * U << "] = {";
-      for (std::size_t j = 0; j < L + D * U; ++j) {
-        if (j) a << (j % 8 == 0 ? ",\n  " : ", ");
-        a << (j < L ? hex64(words_[coef_lo_[s_.ops[run.head + 1 + j].c.id]]) : "0");
-      }
-      a << "};\n\n";
-      run_arrays_ += a.str();
-      a.str("");
-      a << ".global .align 16 .b64 pe_rung" << idx << "[" << L + D * U << "] = {";
-      for (std::size_t j = 0; j < L + D * U; ++j) {
-        if (j) a << (j % 8 == 0 ? ",\n  " : ", ");
-        a << (j < L ? hex64(words_[coef_lo_[s_.ops[run.head + 1 + j].c.id]]) : "0");
-      }
-      a << "};\n.shared .align 16 .b64 pe_runs" << idx << "[" << L + D * U << "];\n\n";
-      small_arrays_ += a.str();
+    const std::string arr = "pe_run" + std::to_string(idx);
+    std::ostringstream a;
+    a << ".const .align 16 .b64 " << arr << "[" << L + D * U << "] = {";
+    for (std::size_t j = 0; j < L + D * U; ++j) {
+      if (j) a << (j % 8 == 0 ? ",\n  " : ", ");
+      a << (j < L ? hex64(words_[coef_lo_[s_.ops[run.head + 1 + j].c.id]]) : "0");
     }
+    a << "};\n\n";
+    run_arrays_ += a.str();
     // word sets: %lw0.. (this trip), %lw1.. (next trip), ... (depth D)
     auto set = [](std::uint32_t d) { return "%lw" + std::to_string(d) + "_"; };
     if (!loop_decls_) {
@@ -1012,8 +952,8 @@ class Emitter {
     };
     auto load8 = [&](const std::string& st, std::uint32_t off) {
       for (std::uint32_t u = 0; u < U; u += 2) {
-        body_ << "  ld." << (smem_loop_ ? "shared" : "const") << ".v2." << ldty() << " {" << st << u
-              << ", " << st << u + 1 << "}, [%lp+" << off + 8 * u << "];\n";
+        body_ << "  ld.const.v2." << ldty() << " {" << st << u << ", " << st << u + 1 << "}, [%lp+"
+              << off + 8 * u << "];\n";
       }
     };
     const std::size_t iters = L / U, rem = L % U;
@@ -1806,12 +1746,6 @@ class Emitter {
   }();
   std::vector<ChainRun> runs_;
   std::string run_arrays_;
-  std::string small_arrays_;  // global copies + shared arrays of the small-batch entry
-  bool smem_loop_ = false;    // emitting the small-batch entry
-  static bool small_entry_enabled() {
-    const char* e = std::getenv("PE_SMALL");
-    return !(e && std::atoi(e) == 0);
-  }
   bool loop_decls_ = false;
   std::vector<std::uint64_t> words_;
   std::unordered_map<std::uint32_t, std::string> pending_;  // imm_mode 4/5: second word of a pair

@@ -62,9 +62,6 @@ struct KernelImage {
   // evaluates q at -x. Both entries take two extra parameters (list, counts).
   std::uint32_t iv_partition = 0;
   std::string part_entry;
-  // small-batch entry (chain loops read a shared-memory copy of their
-  // coefficient arrays): launched instead of `entry` for small batches
-  std::string small_entry;
   std::uint32_t fix_block = 128;   // fixup kernel CTA size (.maxntid)
   std::uint32_t fix_ctas_per_sm = 4;  // fixup grid: CTAs per SM (.minnctapersm)
   // instruction counts per point (roofline bookkeeping)

@@ -67,12 +67,6 @@ void bind_functions(Artifact& a, int device) {
       a.fix_fn[device] = f;
     }
   }
-  if (!a.small_fn[device] && a.small_kernel) {
-    CUfunction f = nullptr;
-    if (driver().get_function(&f, reinterpret_cast<CUkernel>(a.small_kernel)) == CUDA_SUCCESS) {
-      a.small_fn[device] = f;
-    }
-  }
   if (!a.part_fn[device] && a.part_kernel) {
     CUfunction f = nullptr;
     if (driver().get_function(&f, reinterpret_cast<CUkernel>(a.part_kernel)) == CUDA_SUCCESS) {
@@ -161,11 +155,6 @@ void keep_pool_memory(int device) {
   }
 }
 
-std::uint64_t small_batch_max() {
-  const char* e = std::getenv("PE_SMALL_MAX");
-  return e ? static_cast<std::uint64_t>(std::atoll(e)) : std::uint64_t{1} << 20;
-}
-
 bool partition_min_batch(std::uint64_t n) {
   // below ~64K intervals the extra launches outweigh the cheaper walk
   const char* e = std::getenv("PE_IV_PART_MIN");
@@ -232,14 +221,8 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
   if (!part) {
-    // small batches of looped kernels: the entry whose chain loops read a
-    // shared-memory copy of the coefficients (no cold constant-cache miss
-    // per loop trip); large batches keep the constant-bank loop
-    const bool small = a.small_kernel && la.n <= small_batch_max();
-    launch_one(small ? a.small_kernel : a.kernel,
-               dev_ok ? (small ? a.small_fn[device] : a.fn[device]) : nullptr,
-               dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)), args.data(),
-               stream, "launch(walk)");
+    launch_one(a.kernel, dev_ok ? a.fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
+               dim3(static_cast<unsigned>(block)), args.data(), stream, "launch(walk)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   }
   if (img.interval_fast_path) {

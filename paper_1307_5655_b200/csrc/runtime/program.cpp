@@ -328,10 +328,6 @@ void ensure_loaded(Artifact& a, int device) {
       check_cuda(cudaLibraryGetKernel(&a.fix_kernel, a.library, a.image.fix_entry.c_str()),
                  "cudaLibraryGetKernel(fix)");
     }
-    if (!a.image.small_entry.empty()) {
-      check_cuda(cudaLibraryGetKernel(&a.small_kernel, a.library, a.image.small_entry.c_str()),
-                 "cudaLibraryGetKernel(small)");
-    }
     if (!a.image.part_entry.empty()) {
       check_cuda(cudaLibraryGetKernel(&a.part_kernel, a.library, a.image.part_entry.c_str()),
                  "cudaLibraryGetKernel(part)");

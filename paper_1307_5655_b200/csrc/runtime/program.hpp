@@ -33,7 +33,6 @@ struct Artifact {
   cudaKernel_t kernel = nullptr;
   cudaKernel_t fix_kernel = nullptr;  // interval fast path: strict replay of listed points
   cudaKernel_t part_kernel = nullptr; // sign-partitioned fast path: x > 0 entry
-  cudaKernel_t small_kernel = nullptr;  // small-batch entry (shared-memory chain loops)
   // sign-partitioned fast path: the mirrored program q(y) = p(-y), whose
   // kernel takes the x < 0 points (KernelImage::iv_partition == 2)
   std::unique_ptr<Artifact> mirror;
@@ -45,7 +44,6 @@ struct Artifact {
   std::array<void*, kMaxDevices> fn{};
   std::array<void*, kMaxDevices> fix_fn{};
   std::array<void*, kMaxDevices> part_fn{};
-  std::array<void*, kMaxDevices> small_fn{};
   /// The sign partition can run: this module has the x > 0 entry and the
   /// mirror module was generated with its x < 0 entry.
   bool partitioned() const {

@@ -85,13 +85,8 @@ def test_horner_chain_becomes_counted_loop(monkeypatch):
     wl = W.c1()
     prog = pe.compile(wl.poly, wl.schemes)
     ptx = prog.ptx(pe.DOMAIN_F64)
-    main, small = ptx.split(".visible .entry pe_walk_f64_s(")
-    assert main.count("bra.uni $Lrun") == 1
+    assert ptx.count("bra.uni $Lrun") == 1
     assert ".const .align 16 .b64 pe_run0[1007]" in ptx  # 999 words + 8 padding
-    # small-batch entry: the same loop over a shared-memory copy staged from
-    # a global copy of the array (one barrier before any thread leaves)
-    assert small.count("bra.uni $Lrun") == 1 and "ld.shared.v2.f64" in small
-    assert ".global .align 16 .b64 pe_rung0[1007]" in ptx and "bar.sync 0" in small
     assert prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
     assert prog.compile_only(pe.DOMAIN_F64) > 0
     monkeypatch.setenv("PE_LOOP", "0")
@@ -117,7 +112,7 @@ def test_sparse_horner_splits_runs_at_gaps():
     e = np.array([300, 299, 298] + list(range(200, -1, -1))).reshape(-1, 1)
     c = np.linspace(0.5, 1.5, len(e))
     prog = pe.compile(pe.Polynomial(e, c), pe.builtin_scheme("horner"))
-    ptx = prog.ptx(pe.DOMAIN_F64).split(".visible .entry pe_walk_f64_s(")[0]
+    ptx = prog.ptx(pe.DOMAIN_F64)
     assert ptx.count("bra.uni $Lrun") == 1  # the 200-long dense tail
     assert prog.compile_only(pe.DOMAIN_F64) > 0
 

@@ -525,31 +525,3 @@ def test_interval_sign_partition_host_buffers_and_errors(cuda_device, monkeypatc
     bad_lo[12345] = hi[0][12345] + 1.0
     with pytest.raises(ValueError):
         ev.evaluate(([bad_lo], hi))
-
-
-@pytest.mark.parametrize("n", [1, 777, 100_000])
-def test_small_batch_entry_bit_identical(n, cuda_device, monkeypatch):
-    # small batches of looped (Hörner-chain) kernels launch the entry whose
-    # loop reads a shared-memory copy of the coefficients; it runs the same
-    # FMA sequence as the constant-bank loop, so results are bit-identical
-    wl = W.c1()
-    x = [_t(a, cuda_device) for a in wl.points(n)]
-    prog = pe.compile(wl.poly, wl.schemes)
-    assert "pe_walk_f64_s" in prog.ptx(pe.DOMAIN_F64)
-    small = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(x)
-    monkeypatch.setenv("PE_SMALL_MAX", "0")
-    big = pe.Evaluator(pe.DoubleDomain(), prog).evaluate(x)
-    assert torch_equal_bits(small, big)
-    ip = pe.Polynomial(np.arange(150, -1, -1).reshape(-1, 1),
-                       np.random.default_rng(3).integers(1, 9, 151).astype(np.int64))
-    iprog = pe.compile(ip, pe.builtin_scheme("horner"))
-    xi = [_t(np.random.default_rng(4).integers(-1, 2, n).astype(np.int64), cuda_device)]
-    monkeypatch.delenv("PE_SMALL_MAX")
-    a = pe.Evaluator(pe.BigIntDomain(), iprog).evaluate(xi)
-    o = pyoracle.Oracle(ip, [pe.builtin_scheme("horner")]).eval_i64([xi[0].cpu().numpy()])
-    assert np.array_equal(a.cpu().numpy(), o)
-
-
-def torch_equal_bits(a, b):
-    import torch
-    return torch.equal(a.view(torch.int64), b.view(torch.int64))
