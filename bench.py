@@ -444,7 +444,8 @@ def run_native(args, world, rank, local):
         "frac": achieved / peak.value,
         "achieved_pipe_ops_per_s": achieved, "peak_pipe_ops_per_s": peak.value,
         "peak_source": "measured live: pe_measure_peak microbenchmark (8 independent chains/thread, "
-                       "full occupancy) on this GPU; nominal FP64 FMA pipe = "
+                       "full occupancy, immediate multiplier, best of 16 after 16 warm-up launches) "
+                       "on this GPU; nominal FP64 FMA pipe = "
                        f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes "
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "ops": f"{algo_per_pt} {unit_ops} per point (SURVEY 8d F) x {n} points per launch",
