@@ -1375,9 +1375,22 @@ class Emitter {
       fnext(dst, src, up);
       return;
     }
+    const bool outward = up == (sign > 0);  // magnitude grows
+    if (outward && out_fma_) {
+      // Outward step on the FP64 pipe, no check: RU(v + v 2^-60) for v > 0
+      // (RD for v < 0) lies strictly between v and its outer neighbour for
+      // every finite nonzero v, subnormals included, so directed rounding
+      // lands on std::nextafter (DBL_MAX -> inf, caught by the final
+      // finiteness test). It does not move a zero — but the outer endpoint
+      // of a same-sign interval is zero only if the inner one is too, and
+      // the inner endpoint's integer step turns any zero into a NaN.
+      body_ << "  fma." << (sign > 0 ? "rp" : "rm") << ".f64 " << dst << ", " << src
+            << ", 0d3C30000000000000, " << src << ";\n";
+      return;
+    }
     const std::string u = tmp_u(), r = tmp_u();
     body_ << "  mov.b64 " << u << ", " << src << ";\n"
-          << ((up == (sign > 0)) ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", 1;\n"
+          << (outward ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", 1;\n"
           << "  mov.b64 " << dst << ", " << r << ";\n";
   }
 
@@ -1710,6 +1723,10 @@ class Emitter {
   }();
   std::uint32_t nb_ = 0;
   std::uint32_t nk_ = 0;  // known-sign steps emitted (kfma_ rotation)
+  bool out_fma_ = [] {  // PE_IV_OUTFMA=0: outward known-sign steps as integer +1 too
+    const char* e = std::getenv("PE_IV_OUTFMA");
+    return !(e && std::atoi(e) == 0);
+  }();
   std::uint32_t fpcheck_ = [] {
     const char* e = std::getenv("PE_IV_FPCHECK");
     return e ? static_cast<std::uint32_t>(std::atoi(e)) : 0u;
