@@ -269,7 +269,12 @@ pe_status pe_program_limbs_needed(const pe_program* program, const uint64_t* bou
                                   uint32_t* limbs);
 
 /* Interval points [lo[v][i], hi[v][i]]; results [out_lo[i], out_hi[i]].
- * Endpoints must be non-NaN with lo <= hi (reference Interval ctor). */
+ * Endpoints must be non-NaN with lo <= hi (reference Interval ctor).
+ * Univariate batches of >= 64K intervals are split on the device by the sign
+ * of x (x < 0 runs the mirrored program p(-y) at -x; bit-identical results);
+ * the split needs 4 bytes per interval of stream-ordered scratch from the
+ * device's default memory pool, whose release threshold the library raises
+ * so the scratch stays pooled between calls. */
 pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
                            const double* const* hi, size_t n, double* out_lo,
                            double* out_hi, const pe_exec* exec);
