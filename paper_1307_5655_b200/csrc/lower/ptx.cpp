@@ -830,7 +830,6 @@ class Emitter {
         psign_[i] = p.lo == p.hi ? 1 : psign_[p.lo] * psign_[p.hi];
       }
       if (p.exponent == 1 && fast_ && gather_ && static_signs_) psign_[i] = 1;  // 0 < x (classifier)
-      if (p.exponent == 1 && fast_ && xsign_probe_) psign_[i] = xsign_probe_;  // experiment only
     }
   }
 
@@ -1333,9 +1332,7 @@ class Emitter {
       // 32-bit integer compare of the low words on the ALU pipe — a step of
       // one ulp changes the bit pattern by +-1, so the low words differ iff
       // the value moved. Mixing the two balances the FP64 and ALU pipes.
-      // PE_IV_FPCHECK=N: every N-th check on the FP64 pipe (pipe balance)
-      const bool int_check = (iv_check_ == 1 || (iv_check_ == 2 && (nb_ & 1))) &&
-                             !(fpcheck_ != 0 && (nb_ % fpcheck_) == fpcheck_ - 1);
+      const bool int_check = iv_check_ == 1 || (iv_check_ == 2 && (nb_ & 1));
       if (int_check) {
         const std::string l0 = tmp_r(), h0 = tmp_r(), l1 = tmp_r(), h1 = tmp_r();
         body_ << "  mov.b64 {" << l0 << ", " << h0 << "}, " << dst << ";\n"
@@ -1368,10 +1365,7 @@ class Emitter {
   // final finiteness test sends such points to the strict replay. Unknown
   // sign: the FP64-pipe step with its "no move" test (fnext).
   void snext(const std::string& dst, const std::string& src, bool up, int sign) {
-    // pipe balance: every kfma_-th known-sign step goes to the FP64 pipe
-    // (one DFMA + one ALU check instead of two ALU adds)
-    const bool to_fp64 = kfma_ != 0 && sign != 0 && (++nk_ % kfma_) == 0;
-    if (sign == 0 || !int_known_ || to_fp64) {
+    if (sign == 0 || !int_known_) {
       fnext(dst, src, up);
       return;
     }
@@ -1690,13 +1684,6 @@ class Emitter {
   bool medium_ = false;  // emitting the finite-case replay of the fixup entry
   std::uint32_t part_ = 0;    // KernelShape::iv_partition
   std::uint32_t gather_ = 0;  // emitting a partitioned entry: 1 front (x > 0), 2 back (x < 0)
-  // PE_IV_XSIGN=+1/-1: measurement probe only (NOT exact for other inputs):
-  // treat every coordinate as having that sign, to bound what a
-  // sign-partitioned fast path could gain
-  int xsign_probe_ = [] {
-    const char* e = std::getenv("PE_IV_XSIGN");
-    return e ? std::atoi(e) : 0;
-  }();
   bool mid_replay_ = [] {  // PE_IV_MID=0: fixup entry = bit-level replay only
     const char* e = std::getenv("PE_IV_MID");
     return !(e && std::atoi(e) == 0);
@@ -1722,18 +1709,9 @@ class Emitter {
     return e && std::string(e) == "dir";
   }();
   std::uint32_t nb_ = 0;
-  std::uint32_t nk_ = 0;  // known-sign steps emitted (kfma_ rotation)
   bool out_fma_ = [] {  // PE_IV_OUTFMA=0: outward known-sign steps as integer +1 too
     const char* e = std::getenv("PE_IV_OUTFMA");
     return !(e && std::atoi(e) == 0);
-  }();
-  std::uint32_t fpcheck_ = [] {
-    const char* e = std::getenv("PE_IV_FPCHECK");
-    return e ? static_cast<std::uint32_t>(std::atoi(e)) : 0u;
-  }();
-  std::uint32_t kfma_ = [] {  // PE_IV_KFMA=N: every N-th known-sign step on FP64 (0 = none)
-    const char* e = std::getenv("PE_IV_KFMA");
-    return e ? static_cast<std::uint32_t>(std::atoi(e)) : 0u;
   }();
   std::vector<int> rsign_, psign_;  // fast path: static signs of registers / powers
   bool static_signs_ = [] {         // PE_IV_SIGNS=0 disables (A/B measurement)
