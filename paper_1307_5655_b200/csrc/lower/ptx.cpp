@@ -22,6 +22,7 @@
 #include "lower/ptx.hpp"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -1754,8 +1755,110 @@ class Emitter {
 
 }  // namespace
 
+namespace {
+// Latency-aware reordering of a fused stream (see emit_ptx):
+// greedy list scheduling over a window of the next W unscheduled ops, taking
+// the oldest op whose producers were emitted at least D ops earlier (else the
+// oldest ready op), then renumbering coefficients by first use so paired
+// constant loads stay adjacent. The ops are SSA (one definition per
+// register), so any topological order computes the same values.
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape) {
+Stream<C> schedule_stream(const Stream<C>& in, std::size_t W, std::size_t D) {
+  const std::size_t n = in.ops.size();
+  std::unordered_map<std::uint32_t, std::size_t> def;
+  for (std::size_t i = 0; i < n; ++i) def[in.ops[i].dst] = i;
+  std::vector<std::vector<std::size_t>> preds(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    for (const Operand* o : {&in.ops[i].a, &in.ops[i].b, &in.ops[i].c}) {
+      if (o->is(Operand::Reg)) {
+        auto it = def.find(o->id);
+        if (it != def.end() && it->second < i) preds[i].push_back(it->second);
+      }
+    }
+  }
+  std::vector<std::size_t> pos(n, SIZE_MAX), order;
+  order.reserve(n);
+  std::size_t first = 0;  // lowest unscheduled original index
+  while (order.size() < n) {
+    while (first < n && pos[first] != SIZE_MAX) ++first;
+    std::size_t pick = SIZE_MAX, fallback = SIZE_MAX;
+    const std::size_t now = order.size();
+    for (std::size_t i = first; i < n && i < first + W; ++i) {
+      if (pos[i] != SIZE_MAX) continue;
+      bool ready = true, aged = true;
+      for (std::size_t p : preds[i]) {
+        if (pos[p] == SIZE_MAX) { ready = false; break; }
+        if (pos[p] + D > now) aged = false;
+      }
+      if (!ready) continue;
+      if (fallback == SIZE_MAX) fallback = i;
+      if (aged) { pick = i; break; }
+    }
+    if (pick == SIZE_MAX) pick = fallback;
+    pos[pick] = now;
+    order.push_back(pick);
+  }
+  Stream<C> out = in;
+  out.ops.clear();
+  for (std::size_t i : order) out.ops.push_back(in.ops[i]);
+  // coefficients by first use in the new order
+  std::vector<std::uint32_t> remap(in.coefs.size(), UINT32_MAX);
+  out.coefs.clear();
+  out.widen.clear();
+  out.odd.clear();
+  auto use = [&](Operand& o) {
+    if (!o.is(Operand::Coef)) return;
+    if (remap[o.id] == UINT32_MAX) {
+      remap[o.id] = static_cast<std::uint32_t>(out.coefs.size());
+      out.coefs.push_back(in.coefs[o.id]);
+      out.widen.push_back(o.id < in.widen.size() ? in.widen[o.id] : 0);
+      out.odd.push_back(o.id < in.odd.size() ? in.odd[o.id] : 0);
+    }
+    o.id = remap[o.id];
+  };
+  for (auto& op : out.ops) {
+    use(op.a);
+    use(op.b);
+    use(op.c);
+  }
+  use(out.result);
+  for (std::size_t k = 0; k < in.coefs.size(); ++k) {  // unused (should not happen)
+    if (remap[k] == UINT32_MAX) {
+      remap[k] = static_cast<std::uint32_t>(out.coefs.size());
+      out.coefs.push_back(in.coefs[k]);
+      out.widen.push_back(k < in.widen.size() ? in.widen[k] : 0);
+      out.odd.push_back(k < in.odd.size() ? in.odd[k] : 0);
+    }
+  }
+  return out;
+}
+}  // namespace
+
+template <typename C>
+KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shape) {
+  // Wide fused programs (power tables > 32 entries, one point per thread:
+  // C4's trivariate slices) get the latency-aware reordering: their warps
+  // are few (128 registers, most holding powers) and ptxas keeps the walk's
+  // order, so 68 % of FP64 ops sat within 4 instructions of their producer
+  // (profiles/r1_sched_sweep.txt: C4 3.71 -> 3.50 ms per 4e6 points; the
+  // 4-lane C2/C3 kernels have ILP from their lanes and gain nothing).
+  // PE_SCHED="W,D" overrides ("0,0" disables).
+  Stream<C> scheduled;
+  const Stream<C>* sp = &stream_in;
+  if (!stream_in.strict && (domain == Domain::F64 || domain == Domain::I64F)) {
+    std::size_t W = 0, D = 0;
+    if (const char* e = std::getenv("PE_SCHED")) {
+      if (std::sscanf(e, "%zu,%zu", &W, &D) != 2) W = D = 0;
+    } else if (stream_in.powers.size() > 32 && (shape.lanes == 0 || shape.lanes == 1)) {
+      W = 64;
+      D = 8;
+    }
+    if (W > 1) {
+      scheduled = schedule_stream(stream_in, W, D);
+      sp = &scheduled;
+    }
+  }
+  const Stream<C>& stream = *sp;
   std::unordered_map<std::uint64_t, int> distinct;
   for (const auto& c : stream.coefs) {
     std::uint64_t w;
