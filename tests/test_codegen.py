@@ -169,3 +169,23 @@ def test_interval_fixup_entry_has_finite_case_replay(monkeypatch):
     monkeypatch.setenv("PE_IV_MID", "0")
     ptx0 = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
     assert "%macc" not in ptx0
+
+
+@pytest.mark.parametrize("name", ["c2e1000", "c3", "c4"])
+def test_list_scheduler_keeps_ops_and_words(name, monkeypatch):
+    # The latency-aware reordering (on by default for wide programs like C4,
+    # PE_SCHED forces it elsewhere) only permutes SSA ops: the kernel issues
+    # the same FP64 work and reads the same coefficient words.
+    wl = CASES[name]()
+    dom = pe.DOMAIN_I64F if wl.domain == "i64" else pe.DOMAIN_F64
+    monkeypatch.setenv("PE_SCHED", "0,0")  # kernels are generated lazily, at ptx()
+    plain = pe.compile(wl.poly, wl.schemes)
+    a, fa = plain.ptx(dom), plain.kernel_stats(dom)["fp_ops"]
+    monkeypatch.setenv("PE_SCHED", "32,6")
+    sched = pe.compile(wl.poly, wl.schemes)
+    b, fb = sched.ptx(dom), sched.kernel_stats(dom)["fp_ops"]
+    assert a != b
+    assert fa == fb
+    assert _kernel_words(a) == _kernel_words(b)
+    for op in ("fma.rn.f64", "mul.rn.f64", "add.rn.f64"):
+        assert a.count(op) == b.count(op), op
