@@ -305,11 +305,13 @@ class Emitter {
       body_ << "$Lnextpt:\n";
       finish_entry();
       fix_ = false;
-      // launched with 128 threads, 4 CTAs per SM (<= 128 registers): the
-      // replay is latency-bound, so every listed point gets its own thread
-      // (PE_FIX_BLOCK / PE_FIX_CTAS override for tuning)
+      // 128-thread CTAs, .minnctapersm 6 (<= 80 registers, no spills for
+      // C5): the replay is latency-bound, so every listed point gets its own
+      // thread and occupancy helps (C5 fixup per 1e8: 612 -> 590 us at 6,
+      // 584 us at 8 but with spills; profiles/r1_c5_fix_shape.txt).
+      // PE_FIX_BLOCK / PE_FIX_CTAS override for tuning.
       img.fix_block = 128;
-      img.fix_ctas_per_sm = 4;
+      img.fix_ctas_per_sm = 6;
       if (const char* e = std::getenv("PE_FIX_BLOCK")) img.fix_block = static_cast<std::uint32_t>(std::atoi(e));
       if (const char* e = std::getenv("PE_FIX_CTAS")) img.fix_ctas_per_sm = static_cast<std::uint32_t>(std::atoi(e));
       fix_entry = entry_text(img, img.fix_entry, img.fix_block, img.fix_ctas_per_sm);
