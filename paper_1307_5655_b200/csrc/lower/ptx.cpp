@@ -1373,7 +1373,10 @@ class Emitter {
       return;
     }
     const bool outward = up == (sign > 0);  // magnitude grows
-    if (outward && out_fma_) {
+    // PE_IV_OUTFMA=N >= 2: every N-th outward step stays an integer add
+    // (FP64 / ALU balance)
+    const bool keep_int = out_fma_ >= 2 && (++n_out_ % out_fma_) == 0;
+    if (outward && out_fma_ && !keep_int) {
       // Outward step on the FP64 pipe, no check: RU(v + v 2^-60) for v > 0
       // (RD for v < 0) lies strictly between v and its outer neighbour for
       // every finite nonzero v, subnormals included, so directed rounding
@@ -1712,10 +1715,11 @@ class Emitter {
     return e && std::string(e) == "dir";
   }();
   std::uint32_t nb_ = 0;
-  bool out_fma_ = [] {  // PE_IV_OUTFMA=0: outward known-sign steps as integer +1 too
+  std::uint32_t out_fma_ = [] {  // PE_IV_OUTFMA=0: outward known-sign steps as integer +1 too
     const char* e = std::getenv("PE_IV_OUTFMA");
-    return !(e && std::atoi(e) == 0);
+    return e ? static_cast<std::uint32_t>(std::atoi(e)) : 1u;
   }();
+  std::uint32_t n_out_ = 0;
   std::vector<int> rsign_, psign_;  // fast path: static signs of registers / powers
   bool static_signs_ = [] {         // PE_IV_SIGNS=0 disables (A/B measurement)
     const char* e = std::getenv("PE_IV_SIGNS");
