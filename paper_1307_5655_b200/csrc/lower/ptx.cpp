@@ -942,13 +942,13 @@ class Emitter {
     }
     const std::uint32_t acc = s_.ops[run.head].dst;
     const Loaded none;
-    auto step = [&](std::uint32_t u) {
+    auto step = [&](std::uint32_t u, std::uint32_t si = 0) {
       for (std::uint32_t k = 0; k < P_; ++k) {
         const std::string r = reg(acc, k), m = opnd(run.mult, none, k);
         if (d_ == Domain::I64) {
-          body_ << "  mad.lo.s64 " << r << ", " << r << ", " << m << ", " << set(0) << u << ";\n";
+          body_ << "  mad.lo.s64 " << r << ", " << r << ", " << m << ", " << set(si) << u << ";\n";
         } else {
-          body_ << "  fma.rn.f64 " << r << ", " << r << ", " << m << ", " << set(0) << u << ";\n";
+          body_ << "  fma.rn.f64 " << r << ", " << r << ", " << m << ", " << set(si) << u << ";\n";
         }
       }
     };
@@ -962,7 +962,26 @@ class Emitter {
     const std::string lbl = "$Lrun" + std::to_string(idx);
     body_ << "  mov.u64 %lp, " << arr << ";\n";
     for (std::uint32_t d = 0; d < D; ++d) load8(set(d), 8 * U * d);
-    if (iters > 0) {
+    if (loop_rotate_) {
+      // rotating register sets, no moves: the loop body is R = D + 1 trips;
+      // trip j uses set j and loads set (j + D) % R for the trip D ahead
+      const std::uint32_t R = D + 1;
+      const std::size_t outer = iters / R, tail = iters % R;
+      if (outer > 0) {
+        body_ << "  mov.u32 %lc, " << outer << ";\n" << lbl << ":\n";
+        for (std::uint32_t j = 0; j < R; ++j) {
+          load8(set((j + D) % R), 8 * U * (j + D));
+          for (std::uint32_t u = 0; u < U; ++u) step(u, j);
+        }
+        body_ << "  add.u64 %lp, %lp, " << 8 * U * R << ";\n  sub.u32 %lc, %lc, 1;\n"
+              << "  setp.ne.u32 %lq, %lc, 0;\n  @%lq bra.uni " << lbl << ";\n";
+      }
+      for (std::uint32_t j = 0; j < tail; ++j) {  // remaining full trips
+        load8(set((j + D) % R), 8 * U * (j + D));
+        for (std::uint32_t u = 0; u < U; ++u) step(u, j);
+      }
+      for (std::uint32_t u = 0; u < rem; ++u) step(u, static_cast<std::uint32_t>(tail));
+    } else if (iters > 0) {
       body_ << "  mov.u32 %lc, " << iters << ";\n" << lbl << ":\n";
       load8(set(D), 8 * U * D);  // words D trips ahead (padding after the last)
       for (std::uint32_t u = 0; u < U; ++u) step(u);
@@ -974,7 +993,9 @@ class Emitter {
       body_ << "  add.u64 %lp, %lp, " << 8 * U << ";\n  sub.u32 %lc, %lc, 1;\n"
             << "  setp.ne.u32 %lq, %lc, 0;\n  @%lq bra.uni " << lbl << ";\n";
     }
-    for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in set 0
+    if (!loop_rotate_) {
+      for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in set 0
+    }
     const std::uint32_t dst = s_.ops[run.last].dst;
     if (dst != acc) {
       for (std::uint32_t k = 0; k < P_; ++k) {
@@ -1740,10 +1761,19 @@ class Emitter {
     return 1;
   }();
   static constexpr std::uint32_t kLoopU = 8;  // loop unroll (steps per trip)
-  // chain-loop prefetch distance in trips (PE_LOOP_DEPTH, 1..3)
+  // Chain-loop coefficient prefetch: D trips ahead into rotating register
+  // sets (loop body = D + 1 trips, no moves). The 1e5-point C1 kernel had 47 %
+  // of its stall samples on the move of the one-trip-ahead set (waiting on
+  // its LDCU); D = 2 rotating: C1 1e5 20.2 -> 18.6 us per call, 1e7 0.594 ->
+  // 0.577 ms (profiles/r1_c1_small_batch.txt). PE_LOOP_ROT=0 / PE_LOOP_DEPTH
+  // select the move-based variant / the distance.
+  bool loop_rotate_ = [] {
+    const char* e = std::getenv("PE_LOOP_ROT");
+    return !(e && std::atoi(e) == 0);
+  }();
   std::uint32_t loop_depth_ = [] {
     const char* e = std::getenv("PE_LOOP_DEPTH");
-    const int v = e ? std::atoi(e) : 1;
+    const int v = e ? std::atoi(e) : 2;
     return static_cast<std::uint32_t>(v < 1 ? 1 : v > 3 ? 3 : v);
   }();
   std::vector<ChainRun> runs_;

@@ -86,7 +86,7 @@ def test_horner_chain_becomes_counted_loop(monkeypatch):
     prog = pe.compile(wl.poly, wl.schemes)
     ptx = prog.ptx(pe.DOMAIN_F64)
     assert ptx.count("bra.uni $Lrun") == 1
-    assert ".const .align 16 .b64 pe_run0[1007]" in ptx  # 999 words + 8 padding
+    assert ".const .align 16 .b64 pe_run0[1015]" in ptx  # 999 words + 2 trips of padding
     assert prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
     assert prog.compile_only(pe.DOMAIN_F64) > 0
     monkeypatch.setenv("PE_LOOP", "0")
