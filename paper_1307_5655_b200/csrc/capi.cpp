@@ -1,13 +1,15 @@
 // C ABI (include/polyeval_b200.h) over the host front-end, the lowering /
 // PTX emitter, the in-process JIT and the launch runtime.
 //
-// Reference mapping: pe_program_create = build/build_multivariate +
-// compute_lazy_heights + compile (tree.cpp:159-227, eval.cpp:52-69);
+// Reference mapping: pe_program_create = canonicalize + build /
+// build_multivariate + compute_lazy_heights + compile (polynomial.cpp:13-33,
+// tree.cpp:159-227, eval.cpp:52-69), restated in front/*.hpp;
 // pe_eval_* = Evaluator<D>::evaluate over a batch (eval.hpp:74-90), one GPU
 // thread per point instead of one call per point.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <limits>
@@ -18,7 +20,10 @@
 #include <thread>
 #include <vector>
 
-#include "front/compile.hpp"
+#include "front/flat.hpp"
+#include "front/forest.hpp"
+#include "front/split.hpp"
+#include "front/terms.hpp"
 #include "lower/ptx.hpp"
 #include "lower/stream.hpp"
 #include "polyeval_b200.h"
@@ -70,88 +75,65 @@ pe_status guarded(Fn&& fn) {
   }
 }
 
-template <typename C>
-void build_program(Program& p, const std::uint32_t* exps, const C* coeffs, size_t nterms,
-                   std::uint32_t nvars, const pe_scheme_desc* schemes,
-                   std::unique_ptr<EvaluationTree<C>>& tree,
-                   std::unique_ptr<CompiledProgram<C>>& prog) {
-  std::vector<std::string> vars;
-  for (std::uint32_t v = 0; v < nvars; ++v) vars.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
-  std::vector<Term<C>> raw(nterms);
-  for (size_t t = 0; t < nterms; ++t) {
-    raw[t].coefficient = coeffs[t];
-    raw[t].exponents.assign(exps + t * nvars, exps + (t + 1) * nvars);
-  }
-  Polynomial<C> poly = Polynomial<C>::canonicalize(std::move(raw), vars);
-  std::vector<FunctionScheme> fs;
+std::vector<std::string> variable_names(std::uint32_t nvars) {
+  std::vector<std::string> out;
   for (std::uint32_t v = 0; v < nvars; ++v) {
-    fs.push_back(scheme_from_desc(SchemeDesc{schemes[v].upper, schemes[v].lower, schemes[v].cutoff}));
+    out.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
   }
-  EvaluationTree<C> t = nvars == 1 ? build(poly, fs[0], 0)
-                                   : build_multivariate(poly, std::span<const FunctionScheme>(fs));
-  compute_lazy_heights(t);
-  prog = std::make_unique<CompiledProgram<C>>(compile(t));
-  tree = std::make_unique<EvaluationTree<C>>(std::move(t));
-  p.nterms = poly.terms().size();
-  p.variables = vars;
-  p.stats = program_stats(*prog);
-  if constexpr (std::is_same_v<C, std::int64_t>) {
-    p.terms_i = poly.terms();
-  } else {
-    p.poly_f = std::make_unique<Polynomial<double>>(poly);
-  }
-  for (std::uint32_t v = 0; v < nvars; ++v) {
-    p.scheme_descs.push_back(SchemeDesc{schemes[v].upper, schemes[v].lower, schemes[v].cutoff});
-  }
+  return out;
 }
 
-// ---- pe_program_from_compiled: flat reference CompiledProgram -> Program ----
-
-// Converts programs[idx] (and, recursively, its nested programs) after
-// checking every index the walk will use; `used` marks programs already
-// referenced, so the nesting is a tree.
 template <typename C>
-std::unique_ptr<CompiledProgram<C>> convert_program(const pe_compiled_program* progs, size_t np,
-                                                    size_t idx, std::vector<char>& used,
-                                                    std::uint32_t nvars,
-                                                    const std::vector<ExponentSet>& sets) {
-  if (idx >= np) throw std::invalid_argument("nested program index out of range");
-  if (used[idx]) throw std::invalid_argument("program referenced more than once");
-  used[idx] = 1;
-  const pe_compiled_program& src = progs[idx];
+std::unique_ptr<Front<C>> build_front(Program& p, const std::uint32_t* exps, const C* coeffs,
+                                      size_t nterms, std::uint32_t nvars,
+                                      const pe_scheme_desc* schemes) {
+  auto fr = std::make_unique<Front<C>>();
+  fr->terms = front::canonical_terms(exps, coeffs, nterms, nvars);
+  std::vector<front::SplitRule> rules;
+  for (std::uint32_t v = 0; v < nvars; ++v) {
+    rules.push_back(front::SplitRule{schemes[v].upper, schemes[v].lower, schemes[v].cutoff});
+  }
+  fr->forest = std::make_unique<front::Forest<C>>(
+      front::build_forest(fr->terms, std::span<const front::SplitRule>(rules)));
+  fr->flat = front::compile_forest(*fr->forest);
+  p.nterms = fr->terms.size();
+  p.variables = variable_names(nvars);
+  p.stats = front::walk_stats(fr->flat);
+  return fr;
+}
+
+// ---- pe_program_from_compiled: flat reference CompiledProgram -> FlatProgram ----
+
+// Checks one program's register discipline (the reference's lazy-height
+// contract, tree.hpp:68-77): every non-root record accumulates into a
+// register a later record reads, every read register was accumulated into,
+// and every slot is in range.
+void check_program(const pe_compiled_program& src, std::uint32_t nvars,
+                   const std::vector<std::vector<std::uint32_t>>& sets) {
   if (src.nrecords == 0 || !src.records) throw std::invalid_argument("program without records");
   if (src.register_count == 0) throw std::invalid_argument("register_count must be >= 1");
   if (src.variable >= nvars) throw std::invalid_argument("program variable out of range");
-  auto out = std::make_unique<CompiledProgram<C>>();
-  out->register_count = src.register_count;
-  out->variable = src.variable;
   const size_t n = src.nrecords;
-  // register discipline of compiled programs (tree.hpp:68-77): every
-  // non-root record accumulates into a register that a later record reads
-  std::vector<char> read_later(src.register_count, 0);
+  std::vector<char> pending_read(src.register_count, 0);  // scanning backwards
   for (size_t i = n; i-- > 0;) {
     const pe_record& r = src.records[i];
     if (r.lazy_slot >= src.register_count) throw std::invalid_argument("lazy_slot out of range");
     if (r.reads_register != 0 && r.reads_register != 1) {
       throw std::invalid_argument("reads_register must be 0 or 1");
     }
-    if (i + 1 == n) {
-      if (r.parent_slot != -1) throw std::invalid_argument("root record has a parent_slot");
-    } else {
-      if (r.parent_slot < 0 || static_cast<std::uint32_t>(r.parent_slot) >= src.register_count) {
-        throw std::invalid_argument("parent_slot out of range");
-      }
-      if (!read_later[static_cast<std::uint32_t>(r.parent_slot)]) {
-        throw std::invalid_argument("record accumulates into a register no later record reads");
-      }
-    }
-    if (r.reads_register) read_later[r.lazy_slot] = 1;
     if (r.power_slot < -1 ||
         (r.power_slot >= 0 && static_cast<size_t>(r.power_slot) >= sets[src.variable].size())) {
       throw std::invalid_argument("power_slot out of range");
     }
+    if (i + 1 == n) {
+      if (r.parent_slot != -1) throw std::invalid_argument("root record has a parent_slot");
+    } else if (r.parent_slot < 0 || static_cast<std::uint32_t>(r.parent_slot) >= src.register_count) {
+      throw std::invalid_argument("parent_slot out of range");
+    } else if (!pending_read[static_cast<std::uint32_t>(r.parent_slot)]) {
+      throw std::invalid_argument("record accumulates into a register no later record reads");
+    }
+    if (r.reads_register) pending_read[r.lazy_slot] = 1;
   }
-  // and every register a record reads was accumulated into before
   std::vector<char> written(src.register_count, 0);
   for (size_t i = 0; i < n; ++i) {
     const pe_record& r = src.records[i];
@@ -161,26 +143,6 @@ std::unique_ptr<CompiledProgram<C>> convert_program(const pe_compiled_program* p
     }
     if (i + 1 < n) written[static_cast<std::uint32_t>(r.parent_slot)] = 1;
   }
-  out->records.resize(n);
-  for (size_t i = 0; i < n; ++i) {
-    const pe_record& r = src.records[i];
-    auto& d = out->records[i];
-    if (r.sub >= 0) {
-      if (r.sub == 0) throw std::invalid_argument("the root program cannot be nested");
-      d.sub = convert_program<C>(progs, np, static_cast<size_t>(r.sub), used, nvars, sets);
-    } else if (r.sub != -1) {
-      throw std::invalid_argument("sub must be -1 or a program index");
-    } else if constexpr (std::is_same_v<C, double>) {
-      if (!std::isfinite(r.coeff_f64)) throw std::invalid_argument("coefficient is not finite");
-      d.coeff = r.coeff_f64;
-    } else {
-      d.coeff = r.coeff_i64;
-    }
-    if (r.power_slot >= 0) d.power_slot = static_cast<std::uint32_t>(r.power_slot);
-    d.lazy_slot = r.lazy_slot;
-    if (r.parent_slot >= 0) d.parent_slot = static_cast<std::uint32_t>(r.parent_slot);
-    d.reads_register = r.reads_register != 0;
-  }
   if (src.nroot_child_ends > 0 && !src.root_child_ends) {
     throw std::invalid_argument("root_child_ends is null");
   }
@@ -189,72 +151,141 @@ std::unique_ptr<CompiledProgram<C>> convert_program(const pe_compiled_program* p
     if (e >= n || (k > 0 && e <= src.root_child_ends[k - 1])) {
       throw std::invalid_argument("root_child_ends must be ascending record indices");
     }
-    out->root_child_ends.push_back(e);
-  }
-  return out;
-}
-
-// The polynomial a compiled program evaluates, as one term per scalar
-// record ("path terms", like terms not merged): record i of a program over
-// variable v contributes coeff * v^(sum of the power exponents on its way to
-// the program root), times the exponents of the enclosing programs. Every
-// intermediate of the walk is a partial sum of these terms times a sub-product
-// of their powers, so the int64 overflow proof over them is sound.
-template <typename C>
-void expand_terms(const CompiledProgram<C>& p, const std::vector<ExponentSet>& sets,
-                  std::vector<std::uint32_t>& prefix, std::vector<Term<C>>& out) {
-  const size_t n = p.records.size();
-  std::vector<std::uint32_t> parent(n, UINT32_MAX), next_reader(p.register_count, UINT32_MAX);
-  for (size_t i = n; i-- > 0;) {
-    const auto& r = p.records[i];
-    if (r.parent_slot) parent[i] = next_reader[*r.parent_slot];
-    if (r.reads_register) next_reader[r.lazy_slot] = static_cast<std::uint32_t>(i);
-  }
-  std::vector<std::uint64_t> total(n, 0);
-  for (size_t i = n; i-- > 0;) {
-    const auto& r = p.records[i];
-    const std::uint64_t own = r.power_slot ? sets[p.variable].exponents[*r.power_slot] : 0;
-    total[i] = own + (parent[i] == UINT32_MAX ? 0 : total[parent[i]]);
-    if (total[i] > UINT32_MAX) throw std::invalid_argument("exponent overflow in compiled program");
-  }
-  for (size_t i = 0; i < n; ++i) {
-    const auto& r = p.records[i];
-    const std::uint32_t saved = prefix[p.variable];
-    const std::uint64_t e = static_cast<std::uint64_t>(saved) + total[i];
-    if (e > UINT32_MAX) throw std::invalid_argument("exponent overflow in compiled program");
-    prefix[p.variable] = static_cast<std::uint32_t>(e);
-    if (r.sub) {
-      expand_terms(*r.sub, sets, prefix, out);
-    } else if (r.coeff != C{}) {
-      out.push_back(Term<C>{r.coeff, prefix});
-    }
-    prefix[p.variable] = saved;
   }
 }
 
+// Imports the programs in the caller's numbering (programs[0] is the root;
+// each nested program referenced exactly once, all reachable from the root).
 template <typename C>
-void program_from_compiled(Program& p, const pe_compiled_program* progs, size_t np,
-                           std::uint32_t nvars, const std::vector<ExponentSet>& sets,
-                           std::unique_ptr<CompiledProgram<C>>& prog) {
-  std::vector<char> used(np, 0);
-  prog = convert_program<C>(progs, np, 0, used, nvars, sets);
+front::FlatProgram<C> import_programs(const pe_compiled_program* progs, size_t np,
+                                      std::uint32_t nvars,
+                                      std::vector<std::vector<std::uint32_t>> sets) {
+  for (size_t k = 0; k < np; ++k) check_program(progs[k], nvars, sets);
+  std::vector<int> refs(np, 0);
   for (size_t k = 0; k < np; ++k) {
-    if (!used[k]) throw std::invalid_argument("program not reachable from the root");
+    for (size_t i = 0; i < progs[k].nrecords; ++i) {
+      const std::int32_t sub = progs[k].records[i].sub;
+      if (sub == -1) continue;
+      if (sub < -1 || static_cast<size_t>(sub) >= np) {
+        throw std::invalid_argument("nested program index out of range");
+      }
+      if (sub == 0) throw std::invalid_argument("the root program cannot be nested");
+      if (++refs[static_cast<size_t>(sub)] > 1) throw std::invalid_argument("program referenced more than once");
+    }
   }
-  prog->variable_count = nvars;
-  prog->exponent_sets = sets;
-  std::vector<std::uint32_t> prefix(nvars, 0);
-  std::vector<Term<C>> terms;
-  expand_terms(*prog, sets, prefix, terms);
+  // reachability from the root (each program has at most one referrer, so
+  // an unreachable program would sit on a cycle or be unreferenced)
+  std::vector<char> seen(np, 0);
+  std::vector<size_t> todo{0};
+  seen[0] = 1;
+  while (!todo.empty()) {
+    const size_t k = todo.back();
+    todo.pop_back();
+    for (size_t i = 0; i < progs[k].nrecords; ++i) {
+      const std::int32_t sub = progs[k].records[i].sub;
+      if (sub > 0 && !seen[static_cast<size_t>(sub)]) {
+        seen[static_cast<size_t>(sub)] = 1;
+        todo.push_back(static_cast<size_t>(sub));
+      }
+    }
+  }
+  for (size_t k = 0; k < np; ++k) {
+    if (!seen[k]) throw std::invalid_argument("program not reachable from the root");
+  }
+  front::FlatProgram<C> fp;
+  fp.nvars = nvars;
+  fp.exponent_sets = std::move(sets);
+  for (size_t k = 0; k < np; ++k) {
+    const pe_compiled_program& src = progs[k];
+    typename front::FlatProgram<C>::Prog pr;
+    pr.var = src.variable;
+    pr.regs = src.register_count;
+    pr.first = static_cast<std::uint32_t>(fp.recs.size());
+    pr.count = static_cast<std::uint32_t>(src.nrecords);
+    pr.root_child_ends.assign(src.root_child_ends, src.root_child_ends + src.nroot_child_ends);
+    for (size_t i = 0; i < src.nrecords; ++i) {
+      const pe_record& r = src.records[i];
+      typename front::FlatProgram<C>::Rec d;
+      d.sub = r.sub;
+      if (r.sub < 0) {
+        if constexpr (std::is_same_v<C, double>) {
+          if (!std::isfinite(r.coeff_f64)) throw std::invalid_argument("coefficient is not finite");
+          d.coef = r.coeff_f64;
+        } else {
+          d.coef = r.coeff_i64;
+        }
+      }
+      d.power = r.power_slot;
+      d.lazy = r.lazy_slot;
+      d.parent = r.parent_slot;
+      d.reads = r.reads_register != 0;
+      fp.recs.push_back(d);
+    }
+    fp.progs.push_back(std::move(pr));
+  }
+  return fp;
+}
+
+// The polynomial an imported program evaluates, one row per scalar record
+// (like terms not merged): record i of a program over variable v contributes
+// coef * v^(sum of the powers on its way to the program's last record), times
+// the exponents of the enclosing programs. Every intermediate of the walk is
+// a partial sum of these terms times a sub-product of their powers, so the
+// int64 overflow proof over them is sound.
+template <typename C>
+front::TermTable<C> path_terms(const front::FlatProgram<C>& fp) {
+  front::TermTable<C> T;
+  T.nvars = fp.nvars;
+  struct Frame {
+    std::uint32_t prog;
+    std::vector<std::uint32_t> prefix;
+  };
+  std::vector<Frame> todo{{0, std::vector<std::uint32_t>(fp.nvars, 0)}};
+  while (!todo.empty()) {
+    Frame fr = std::move(todo.back());
+    todo.pop_back();
+    const auto& P = fp.progs[fr.prog];
+    const auto up = front::consumers(fp, fr.prog);
+    std::vector<std::uint64_t> total(P.count, 0);
+    for (std::uint32_t i = P.count; i-- > 0;) {
+      const auto& r = fp.rec(fr.prog, i);
+      const std::uint64_t own = r.power >= 0 ? fp.exponent(fr.prog, r.power) : 0;
+      total[i] = own + (up[i] == UINT32_MAX ? 0 : total[up[i]]);
+      if (total[i] + fr.prefix[P.var] > UINT32_MAX) {
+        throw std::invalid_argument("exponent overflow in compiled program");
+      }
+    }
+    for (std::uint32_t i = 0; i < P.count; ++i) {
+      const auto& r = fp.rec(fr.prog, i);
+      std::vector<std::uint32_t> row = fr.prefix;
+      row[P.var] += static_cast<std::uint32_t>(total[i]);
+      if (r.sub >= 0) {
+        todo.push_back({static_cast<std::uint32_t>(r.sub), std::move(row)});
+      } else if (r.coef != C{}) {
+        T.coefs.push_back(r.coef);
+        T.exps.insert(T.exps.end(), row.begin(), row.end());
+      }
+    }
+  }
+  return T;
+}
+
+template <typename C>
+std::unique_ptr<Front<C>> import_front(Program& p, const pe_compiled_program* progs, size_t np,
+                                       std::uint32_t nvars,
+                                       std::vector<std::vector<std::uint32_t>> sets) {
+  auto fr = std::make_unique<Front<C>>();
+  fr->flat = import_programs<C>(progs, np, nvars, std::move(sets));
+  fr->terms = path_terms(fr->flat);
   std::vector<std::vector<std::uint32_t>> keys;
-  for (const auto& t : terms) keys.push_back(t.exponents);
+  for (size_t t = 0; t < fr->terms.size(); ++t) {
+    keys.emplace_back(fr->terms.row(t), fr->terms.row(t) + nvars);
+  }
   std::sort(keys.begin(), keys.end());
   p.nterms = static_cast<std::uint64_t>(std::unique(keys.begin(), keys.end()) - keys.begin());
-  for (std::uint32_t v = 0; v < nvars; ++v) {
-    p.variables.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
-  }
-  p.stats = program_stats(*prog);
-  if constexpr (std::is_same_v<C, std::int64_t>) p.terms_i = std::move(terms);
+  p.variables = variable_names(nvars);
+  p.stats = front::walk_stats(fr->flat);
+  return fr;
 }
 
 // exec->devices: one host thread per device, each running the single-device
@@ -322,8 +353,8 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
     p.nvars = nvars;
     p.integer = coeff_type == PE_COEFF_I64;
     if (p.integer) {
-      build_program(p, exponents, static_cast<const std::int64_t*>(coeffs), nterms, nvars, schemes,
-                    p.tree_i, p.prog_i);
+      p.i = build_front(p, exponents, static_cast<const std::int64_t*>(coeffs), nterms, nvars,
+                        schemes);
       p.i64_uniform_bound = uniform_bounds(p, 63);
       p.i53_uniform_bound = uniform_bounds(p, 53);
     } else {
@@ -331,7 +362,7 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
       for (size_t t = 0; t < nterms; ++t) {
         if (!std::isfinite(c[t])) return fail(PE_EINVAL, "coefficient is not finite");
       }
-      build_program(p, exponents, c, nterms, nvars, schemes, p.tree_f, p.prog_f);
+      p.f = build_front(p, exponents, c, nterms, nvars, schemes);
     }
     *out = h.release();
     return PE_OK;
@@ -342,21 +373,22 @@ pe_status pe_program_check_registers(const pe_program* program) {
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
     const Program& p = program->impl;
-    auto clean = [](const auto& self, const auto& prog) -> bool {
-      std::vector<char> live(prog.register_count, 0);
-      const size_t n = prog.records.size();
-      for (size_t i = 0; i < n; ++i) {
-        const auto& r = prog.records[i];
-        if (r.sub && !self(self, *r.sub)) return false;
-        if (r.reads_register) live[r.lazy_slot] = 0;   // eval.hpp:225-228
-        if (i + 1 < n && r.parent_slot) live[*r.parent_slot] = 1;  // L237-238
-      }
-      for (char c : live) {
-        if (c) return false;
+    // each program's walk leaves its register file clean iff every register
+    // accumulated into is read again later (eval.hpp:225-238)
+    auto clean = [](const auto& fp) -> bool {
+      for (std::uint32_t k = 0; k < fp.progs.size(); ++k) {
+        const auto& P = fp.progs[k];
+        std::vector<char> live(P.regs, 0);
+        for (std::uint32_t i = 0; i < P.count; ++i) {
+          const auto& r = fp.rec(k, i);
+          if (r.reads) live[r.lazy] = 0;
+          if (i + 1 < P.count && r.parent >= 0) live[static_cast<std::uint32_t>(r.parent)] = 1;
+        }
+        if (std::find(live.begin(), live.end(), 1) != live.end()) return false;
       }
       return true;
     };
-    const bool ok = p.integer ? clean(clean, *p.prog_i) : clean(clean, *p.prog_f);
+    const bool ok = p.integer ? clean(p.i->flat) : clean(p.f->flat);
     if (!ok) return fail(PE_ELOGIC, "register file not clean after walk");
     return PE_OK;
   });
@@ -375,7 +407,7 @@ pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t n
     if (coeff_type != PE_COEFF_F64 && coeff_type != PE_COEFF_I64) {
       return fail(PE_EINVAL, "unknown coefficient type");
     }
-    std::vector<ExponentSet> sets(nvars);
+    std::vector<std::vector<std::uint32_t>> sets(nvars);
     for (uint32_t v = 0; v < nvars; ++v) {
       const size_t k = exponent_set_sizes[v];
       if (k > 0 && !exponent_sets[v]) return fail(PE_EINVAL, "exponent set is null");
@@ -384,7 +416,7 @@ pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t n
         if (e == 0 || (i > 0 && e <= exponent_sets[v][i - 1])) {
           return fail(PE_EINVAL, "exponent sets must be ascending, distinct and >= 1");
         }
-        sets[v].exponents.push_back(e);
+        sets[v].push_back(e);
       }
     }
     auto h = std::make_unique<pe_program>();
@@ -392,30 +424,18 @@ pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t n
     p.nvars = nvars;
     p.integer = coeff_type == PE_COEFF_I64;
     if (p.integer) {
-      program_from_compiled(p, programs, nprograms, nvars, sets, p.prog_i);
+      p.i = import_front<std::int64_t>(p, programs, nprograms, nvars, std::move(sets));
       p.i64_uniform_bound = uniform_bounds(p, 63);
       p.i53_uniform_bound = uniform_bounds(p, 53);
     } else {
-      program_from_compiled(p, programs, nprograms, nvars, sets, p.prog_f);
+      p.f = import_front<double>(p, programs, nprograms, nvars, std::move(sets));
     }
     *out = h.release();
     return PE_OK;
   });
 }
 
-void pe_program_destroy(pe_program* program) {
-  if (!program) return;
-  auto release = [](Artifact* a) {
-    if (!a) return;
-    for (auto& [dev, ptr] : a->global_coefs) {
-      if (cudaSetDevice(dev) == cudaSuccess) cudaFree(ptr);
-    }
-    if (a->library) cudaLibraryUnload(a->library);
-  };
-  for (auto& a : program->impl.artifacts) release(a.get());
-  for (auto& a : program->impl.slice_arts) release(a.get());
-  delete program;
-}
+void pe_program_destroy(pe_program* program) { delete program; }
 
 pe_status pe_program_info(const pe_program* program, pe_program_info_t* info) {
   return guarded([&]() -> pe_status {
@@ -430,14 +450,14 @@ pe_status pe_program_info(const pe_program* program, pe_program_info_t* info) {
     info->walk_muls = p.stats.walk_muls;
     info->power_muls = p.stats.power_muls;
     info->terms = p.nterms;
-    auto fill = [&](const auto& prog) {
-      info->register_count = prog.register_count;
-      info->root_children = static_cast<uint32_t>(prog.root_child_ends.size());
-      for (size_t v = 0; v < prog.exponent_sets.size() && v < 8; ++v) {
-        info->exponent_set_sizes[v] = static_cast<uint32_t>(prog.exponent_sets[v].size());
+    auto fill = [&](const auto& fp) {
+      info->register_count = fp.progs[0].regs;
+      info->root_children = static_cast<uint32_t>(fp.progs[0].root_child_ends.size());
+      for (size_t v = 0; v < fp.exponent_sets.size() && v < 8; ++v) {
+        info->exponent_set_sizes[v] = static_cast<uint32_t>(fp.exponent_sets[v].size());
       }
     };
-    if (p.integer) fill(*p.prog_i); else fill(*p.prog_f);
+    if (p.integer) fill(p.i->flat); else fill(p.f->flat);
     return PE_OK;
   });
 }
@@ -447,9 +467,9 @@ pe_status pe_program_exponents(const pe_program* program, uint32_t v, uint32_t* 
   return guarded([&]() -> pe_status {
     if (!program || !count) return fail(PE_EINVAL, "null argument");
     const Program& p = program->impl;
-    const auto& sets = p.integer ? p.prog_i->exponent_sets : p.prog_f->exponent_sets;
-    if (v >= sets.size()) return fail(PE_EINVAL, "variable index out of range");
-    const auto& e = sets[v].exponents;
+    const auto& sets = p.integer ? p.i->flat.exponent_sets : p.f->flat.exponent_sets;
+    if (v >= sets.size() || v >= p.nvars) return fail(PE_EINVAL, "variable index out of range");
+    const auto& e = sets[v];
     *count = e.size();
     for (size_t i = 0; i < e.size() && i < cap && out; ++i) out[i] = e[i];
     return PE_OK;
@@ -460,18 +480,19 @@ pe_status pe_program_records(const pe_program* program, int32_t* out, size_t cap
   return guarded([&]() -> pe_status {
     if (!program || !count) return fail(PE_EINVAL, "null argument");
     const Program& p = program->impl;
-    auto dump = [&](const auto& prog) {
-      *count = prog.records.size();
-      for (size_t i = 0; i < prog.records.size() && (i + 1) * 5 <= cap && out; ++i) {
-        const auto& r = prog.records[i];
-        out[5 * i + 0] = r.power_slot ? static_cast<int32_t>(*r.power_slot) : -1;
-        out[5 * i + 1] = static_cast<int32_t>(r.lazy_slot);
-        out[5 * i + 2] = r.parent_slot ? static_cast<int32_t>(*r.parent_slot) : -1;
-        out[5 * i + 3] = r.reads_register ? 1 : 0;
-        out[5 * i + 4] = r.sub ? 1 : 0;
+    auto dump = [&](const auto& fp) {
+      const std::uint32_t n = fp.progs[0].count;
+      *count = n;
+      for (size_t i = 0; i < n && (i + 1) * 5 <= cap && out; ++i) {
+        const auto& r = fp.rec(0, static_cast<std::uint32_t>(i));
+        out[5 * i + 0] = r.power;
+        out[5 * i + 1] = static_cast<int32_t>(r.lazy);
+        out[5 * i + 2] = r.parent;
+        out[5 * i + 3] = r.reads ? 1 : 0;
+        out[5 * i + 4] = r.sub >= 0 ? 1 : 0;
       }
     };
-    if (p.integer) dump(*p.prog_i); else dump(*p.prog_f);
+    if (p.integer) dump(p.i->flat); else dump(p.f->flat);
     return PE_OK;
   });
 }
@@ -480,10 +501,12 @@ pe_status pe_program_dot(const pe_program* program, char* out, size_t cap, size_
   return guarded([&]() -> pe_status {
     if (!program || !len) return fail(PE_EINVAL, "null argument");
     const Program& p = program->impl;
-    if (p.integer ? !p.tree_i : !p.tree_f) {
+    if (p.integer ? !p.i->forest : !p.f->forest) {
       return fail(PE_EINVAL, "program was created from a compiled program and has no tree");
     }
-    const std::string dot = p.integer ? to_dot(*p.tree_i) : to_dot(*p.tree_f);
+    const std::span<const std::string> names(p.variables);
+    const std::string dot = p.integer ? front::forest_dot(*p.i->forest, names)
+                                      : front::forest_dot(*p.f->forest, names);
     *len = dot.size();
     if (out && cap) {
       const size_t k = std::min(cap - 1, dot.size());
@@ -548,7 +571,7 @@ pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63, ui
 pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices) {
   return guarded([&]() -> pe_status {
     if (!program || !slices) return fail(PE_EINVAL, "null argument");
-    *slices = static_cast<uint32_t>(program->impl.slice_count());
+    *slices = 1;
     return PE_OK;
   });
 }
@@ -630,9 +653,8 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     MemKind kind;
     const int dev = resolve_device(exec, out, &kind);
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
-    const std::vector<const Artifact*> arts =
-        strict ? std::vector<const Artifact*>{&p.loaded(lower::Domain::F64Strict, dev)}
-               : p.f64_kernels(dev);
+    const std::vector<const Artifact*> arts{
+        &p.loaded(strict ? lower::Domain::F64Strict : lower::Domain::F64, dev)};
     std::vector<const void*> ins(coords, coords + p.nvars);
     std::vector<void*> outs{out};
     LaunchArgs la;
@@ -672,10 +694,8 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
     std::vector<const Artifact*> arts;
     std::vector<size_t> base;
     for (size_t j = 0; j < k; ++j) {
-      for (const Artifact* a : programs[j]->impl.f64_kernels(dev)) {
-        arts.push_back(a);
-        base.push_back(j);
-      }
+      arts.push_back(&programs[j]->impl.loaded(lower::Domain::F64, dev));
+      base.push_back(j);
     }
     std::vector<const void*> ins(coords, coords + nv);
     std::vector<void*> o(outs, outs + k);

@@ -1,4 +1,4 @@
-// Lowering of a CompiledProgram into a straight-line register stream.
+// Lowering of a FlatProgram into a straight-line register stream.
 // See stream.hpp for the contract; reference walk: eval.hpp:208-249,
 // power tables: powers.hpp:50-72.
 #include "lower/stream.hpp"
@@ -14,11 +14,11 @@ namespace {
 // recursion order (ensure(e) -> ensure(e/2), ensure(e - e/2), then multiply;
 // powers.hpp:58-66), and returns [var][slot] -> power id.
 template <typename C>
-std::vector<std::vector<std::uint32_t>> build_powers(const CompiledProgram<C>& prog,
+std::vector<std::vector<std::uint32_t>> build_powers(const front::FlatProgram<C>& prog,
                                                      Stream<C>& s) {
   std::vector<std::vector<std::uint32_t>> slot_to_power(prog.exponent_sets.size());
   for (std::size_t v = 0; v < prog.exponent_sets.size(); ++v) {
-    const ExponentSet& set = prog.exponent_sets[v];
+    const std::vector<std::uint32_t>& set = prog.exponent_sets[v];
     if (set.empty()) continue;
     std::map<std::uint32_t, std::uint32_t> memo;
     memo[1] = static_cast<std::uint32_t>(s.powers.size());
@@ -53,7 +53,7 @@ std::vector<std::vector<std::uint32_t>> build_powers(const CompiledProgram<C>& p
         st.pop_back();
       }
     };
-    for (std::uint32_t e : set.exponents) {
+    for (std::uint32_t e : set) {
       ensure(e);
       slot_to_power[v].push_back(memo.at(e));
     }
@@ -61,26 +61,11 @@ std::vector<std::vector<std::uint32_t>> build_powers(const CompiledProgram<C>& p
   return slot_to_power;
 }
 
-// For record i, the index of its parent record: the first later record that
-// reads the register i accumulates into (register discipline of the lazy
-// heights, reference tree.hpp:68-77).
-template <typename C>
-std::vector<std::uint32_t> parent_records(const CompiledProgram<C>& p) {
-  const std::size_t n = p.records.size();
-  std::vector<std::uint32_t> parent(n, UINT32_MAX);
-  std::vector<std::uint32_t> next_reader(p.register_count, UINT32_MAX);
-  for (std::size_t i = n; i-- > 0;) {
-    const auto& r = p.records[i];
-    if (r.parent_slot) parent[i] = next_reader[*r.parent_slot];
-    if (r.reads_register) next_reader[r.lazy_slot] = static_cast<std::uint32_t>(i);
-  }
-  return parent;
-}
-
 template <typename C>
 struct Lowerer {
   Stream<C>& s;
   const std::vector<std::vector<std::uint32_t>>& pow_of;
+  const front::FlatProgram<C>& fp;
 
   std::uint8_t cur_odd = 0;  // strict: parity of the record being lowered
 
@@ -91,8 +76,8 @@ struct Lowerer {
     s.odd.push_back(cur_odd);
     return Operand::coef(static_cast<std::uint32_t>(s.coefs.size() - 1));
   }
-  Operand power(const CompiledProgram<C>& p, std::uint32_t slot) {
-    return Operand::pow(pow_of.at(p.variable).at(slot));
+  Operand power(std::uint32_t prog, std::int32_t slot) {
+    return Operand::pow(pow_of.at(fp.progs[prog].var).at(static_cast<std::uint32_t>(slot)));
   }
   Operand emit(OpKind k, Operand a, Operand b, Operand c = {}) {
     if (s.strict && k == OpKind::Add && a.is(Operand::Zero) && b.is(Operand::Coef)) {
@@ -121,35 +106,35 @@ struct Lowerer {
   }
 
   // ---- strict: the reference walk verbatim (eval.hpp:218-239) ----
-  Operand strict(const CompiledProgram<C>& p) {
-    std::vector<Operand> m(p.register_count, Operand::zero());
-    const std::size_t last = p.records.size() - 1;
+  Operand strict(std::uint32_t prog) {
+    const auto& P = fp.progs[prog];
+    std::vector<Operand> m(P.regs, Operand::zero());
+    const std::uint32_t last = P.count - 1;
     // parity of each record's absolute exponent: its own power plus its
-    // ancestors' (a record's value is added into the register its parent
-    // reads and multiplies by the parent's power)
-    std::vector<std::uint8_t> par(p.records.size(), 0);
-    if (s.mirrorable && !p.records.empty()) {  // univariate only
-      const auto parent = parent_records(p);
-      for (std::size_t i = p.records.size(); i-- > 0;) {
-        const auto& rec = p.records[i];
-        std::uint32_t d = 0;
-        if (rec.power_slot) d = p.exponent_sets.at(p.variable).exponents.at(*rec.power_slot);
-        const std::uint8_t up = parent[i] == UINT32_MAX ? 0 : par[parent[i]];
-        par[i] = static_cast<std::uint8_t>((d + up) & 1u);
-        if (rec.sub) s.mirrorable = false;
+    // consumer's (a record's value is added into the register its consumer
+    // reads and multiplies by the consumer's power)
+    std::vector<std::uint8_t> par(P.count, 0);
+    if (s.mirrorable) {  // univariate only
+      const auto up = front::consumers(fp, prog);
+      for (std::uint32_t i = P.count; i-- > 0;) {
+        const auto& rec = fp.rec(prog, i);
+        const std::uint32_t d = rec.power >= 0 ? fp.exponent(prog, rec.power) : 0;
+        const std::uint8_t above = up[i] == UINT32_MAX ? 0 : par[up[i]];
+        par[i] = static_cast<std::uint8_t>((d + above) & 1u);
+        if (rec.sub >= 0) s.mirrorable = false;
       }
     }
-    for (std::size_t i = 0; i <= last; ++i) {
-      const auto& rec = p.records[i];
+    for (std::uint32_t i = 0; i <= last; ++i) {
+      const auto& rec = fp.rec(prog, i);
       cur_odd = par[i];
-      Operand v = rec.sub ? strict(*rec.sub) : coef(rec.coeff);  // L224
-      if (rec.reads_register) {                                   // L225-228
-        v = emit(OpKind::Add, m[rec.lazy_slot], v);
-        m[rec.lazy_slot] = Operand::zero();
+      Operand v = own(prog, i, true);                          // L224
+      if (rec.reads) {                                         // L225-228
+        v = emit(OpKind::Add, m[rec.lazy], v);
+        m[rec.lazy] = Operand::zero();
       }
-      if (rec.power_slot) v = emit(OpKind::Mul, v, power(p, *rec.power_slot));  // L229-232
-      if (i == last) return v;                                    // L233-236
-      Operand& slot = m[*rec.parent_slot];                        // L237-238
+      if (rec.power >= 0) v = emit(OpKind::Mul, v, power(prog, rec.power));  // L229-232
+      if (i == last) return v;                                 // L233-236
+      Operand& slot = m[static_cast<std::uint32_t>(rec.parent)];  // L237-238
       slot = emit(OpKind::Add, slot, v);
     }
     return Operand::zero();
@@ -159,52 +144,55 @@ struct Lowerer {
   // A record's "own" value is its scalar coefficient or its nested program's
   // result; it enters exactly once, either as the addend that makes the
   // record's register live or as a final add when the record is visited.
-  Operand own(const CompiledProgram<C>& p, std::size_t i) {
-    const auto& rec = p.records[i];
-    return rec.sub ? fused(*rec.sub) : coef(rec.coeff);
+  Operand own(std::uint32_t prog, std::uint32_t i, bool strict_walk = false) {
+    const auto& rec = fp.rec(prog, i);
+    if (rec.sub < 0) return coef(rec.coef);
+    const auto sub = static_cast<std::uint32_t>(rec.sub);
+    return strict_walk ? strict(sub) : fused(sub);
   }
 
-  Operand fused(const CompiledProgram<C>& p) {
-    const std::size_t n = p.records.size();
-    const auto parent = parent_records(p);
-    std::vector<Operand> m(p.register_count);  // None == not live
+  Operand fused(std::uint32_t prog) {
+    const auto& P = fp.progs[prog];
+    const std::uint32_t n = P.count;
+    const auto parent = front::consumers(fp, prog);
+    std::vector<Operand> m(P.regs);  // None == not live
     std::vector<char> folded(n, 0);
-    for (std::size_t i = 0; i < n; ++i) {
-      const auto& rec = p.records[i];
+    for (std::uint32_t i = 0; i < n; ++i) {
+      const auto& rec = fp.rec(prog, i);
       Operand val;
-      if (rec.reads_register) {
-        Operand acc = m[rec.lazy_slot];
-        m[rec.lazy_slot] = Operand{};
+      if (rec.reads) {
+        Operand acc = m[rec.lazy];
+        m[rec.lazy] = Operand{};
         if (acc.is(Operand::None)) throw std::logic_error("fused lowering: dead register read");
-        val = folded[i] ? acc : emit(OpKind::Add, acc, own(p, i));
+        val = folded[i] ? acc : emit(OpKind::Add, acc, own(prog, i));
       } else {
-        val = own(p, i);
+        val = own(prog, i);
       }
       if (i + 1 == n) {
-        if (rec.power_slot) return emit(OpKind::Mul, val, power(p, *rec.power_slot));
+        if (rec.power >= 0) return emit(OpKind::Mul, val, power(prog, rec.power));
         return val;
       }
       const std::uint32_t j = parent[i];
       if (j == UINT32_MAX) throw std::logic_error("fused lowering: record without parent");
-      Operand& cur = m[*rec.parent_slot];
-      if (rec.power_slot) {
-        const Operand P = power(p, *rec.power_slot);
+      Operand& cur = m[static_cast<std::uint32_t>(rec.parent)];
+      if (rec.power >= 0) {
+        const Operand Pw = power(prog, rec.power);
         if (cur.is(Operand::None)) {
           if (!folded[j]) {
             folded[j] = 1;
-            const Operand addend = own(p, j);
-            cur = emit(OpKind::Fma, val, P, addend);
+            const Operand addend = own(prog, j);
+            cur = emit(OpKind::Fma, val, Pw, addend);
           } else {
-            cur = emit(OpKind::Mul, val, P);
+            cur = emit(OpKind::Mul, val, Pw);
           }
         } else {
-          cur = emit(OpKind::Fma, val, P, cur);
+          cur = emit(OpKind::Fma, val, Pw, cur);
         }
       } else {
         if (cur.is(Operand::None)) {
           if (!folded[j]) {
             folded[j] = 1;
-            const Operand addend = own(p, j);
+            const Operand addend = own(prog, j);
             if (val.is(Operand::Coef) && addend.is(Operand::Coef)) {
               // constant + constant: fold on the host (same IEEE/int result
               // the device add would produce)
@@ -235,14 +223,14 @@ struct Lowerer {
 }  // namespace
 
 template <typename C>
-Stream<C> lower_strict(const CompiledProgram<C>& program) {
+Stream<C> lower_strict(const front::FlatProgram<C>& program) {
   Stream<C> s;
   s.strict = true;
-  s.nvars = static_cast<std::uint32_t>(program.variable_count);
+  s.nvars = program.nvars;
   s.mirrorable = s.nvars == 1;
   const auto pow_of = build_powers(program, s);
-  Lowerer<C> L{s, pow_of};
-  s.result = L.strict(program);
+  Lowerer<C> L{s, pow_of, program};
+  s.result = L.strict(0);
   return s;
 }
 
@@ -264,19 +252,19 @@ template bool mirror_stream(const Stream<double>&, Stream<double>*);
 template bool mirror_stream(const Stream<std::int64_t>&, Stream<std::int64_t>*);
 
 template <typename C>
-Stream<C> lower_fused(const CompiledProgram<C>& program) {
+Stream<C> lower_fused(const front::FlatProgram<C>& program) {
   Stream<C> s;
   s.strict = false;
-  s.nvars = static_cast<std::uint32_t>(program.variable_count);
+  s.nvars = program.nvars;
   const auto pow_of = build_powers(program, s);
-  Lowerer<C> L{s, pow_of};
-  s.result = L.fused(program);
+  Lowerer<C> L{s, pow_of, program};
+  s.result = L.fused(0);
   return s;
 }
 
-template Stream<double> lower_strict(const CompiledProgram<double>&);
-template Stream<std::int64_t> lower_strict(const CompiledProgram<std::int64_t>&);
-template Stream<double> lower_fused(const CompiledProgram<double>&);
-template Stream<std::int64_t> lower_fused(const CompiledProgram<std::int64_t>&);
+template Stream<double> lower_strict(const front::FlatProgram<double>&);
+template Stream<std::int64_t> lower_strict(const front::FlatProgram<std::int64_t>&);
+template Stream<double> lower_fused(const front::FlatProgram<double>&);
+template Stream<std::int64_t> lower_fused(const front::FlatProgram<std::int64_t>&);
 
 }  // namespace polyeval::lower

@@ -1,4 +1,4 @@
-// Lowering: CompiledProgram -> register-scheduled instruction stream.
+// Lowering: FlatProgram -> register-scheduled instruction stream.
 //
 // The reference interprets its flat record list per point through a heap
 // register file indexed at run time (eval.hpp:218-249, run_nested 208-213,
@@ -28,7 +28,7 @@
 #include <string>
 #include <vector>
 
-#include "front/compile.hpp"
+#include "front/flat.hpp"
 
 namespace polyeval::lower {
 
@@ -93,10 +93,10 @@ struct Stream {
 };
 
 template <typename C>
-Stream<C> lower_strict(const CompiledProgram<C>& program);
+Stream<C> lower_strict(const front::FlatProgram<C>& program);
 
 template <typename C>
-Stream<C> lower_fused(const CompiledProgram<C>& program);
+Stream<C> lower_fused(const front::FlatProgram<C>& program);
 
 /// The strict stream of q(y) = p(-y): the same walk with the coefficients of
 /// odd-exponent terms negated. Every primitive of the interval walk (RN

@@ -54,13 +54,14 @@ bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bi
   for (std::uint32_t v = 0; v < p.nvars; ++v) base[v] = std::max<u128>(1, bounds[v]);
   u128 m = 0;
   std::vector<std::uint32_t> max_e(p.nvars, 0);
-  for (const auto& t : p.terms_i) {
-    const u128 c = t.coefficient < 0 ? static_cast<u128>(-(t.coefficient + 1)) + 1
-                                     : static_cast<u128>(t.coefficient);
+  const auto& T = p.i->terms;
+  for (std::size_t t = 0; t < T.size(); ++t) {
+    const std::int64_t cf = T.coefs[t];
+    const u128 c = cf < 0 ? static_cast<u128>(-(cf + 1)) + 1 : static_cast<u128>(cf);
     u128 term = c;
     for (std::uint32_t v = 0; v < p.nvars; ++v) {
-      term = sat_mul(term, sat_pow(base[v], t.exponents[v]));
-      max_e[v] = std::max(max_e[v], t.exponents[v]);
+      term = sat_mul(term, sat_pow(base[v], T.exp(t, v)));
+      max_e[v] = std::max(max_e[v], T.exp(t, v));
     }
     m = std::min<u128>(m + term, kSat);
   }
@@ -76,8 +77,9 @@ bool i64_proof_holds(const Program& p, const std::uint64_t* bounds, int limit_bi
 std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits) {
   std::vector<std::uint64_t> out(p.nvars, UINT64_MAX);
   std::vector<bool> present(p.nvars, false);
-  for (const auto& t : p.terms_i) {
-    for (std::uint32_t v = 0; v < p.nvars; ++v) present[v] = present[v] || t.exponents[v] > 0;
+  const auto& T = p.i->terms;
+  for (std::size_t t = 0; t < T.size(); ++t) {
+    for (std::uint32_t v = 0; v < p.nvars; ++v) present[v] = present[v] || T.exp(t, v) > 0;
   }
   // the exact-FP64 path converts coordinates to double: they must be < 2^53
   // even for variables absent from the polynomial
@@ -112,7 +114,7 @@ bool partition_enabled() {
 // Interval domain: the program's kernel (+ the mirror module when the sign
 // partition applies, see lower/ptx.cpp and lower::mirror_stream).
 template <typename C>
-void emit_interval(const CompiledProgram<C>& prog, std::uint32_t nvars, Artifact& a) {
+void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, Artifact& a) {
   lower::KernelShape shape;
   if (nvars == 1 && partition_enabled()) shape.iv_partition = 1;
   const auto s = lower::lower_strict(prog);
@@ -137,18 +139,18 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
       // univariate programs get the sign-partitioned fast path: this module
       // gains an x > 0 entry, a mirror module evaluates q(y) = p(-y) at -x
       if (integer) {
-        emit_interval(*prog_i, nvars, *a);
+        emit_interval(i->flat, nvars, *a);
       } else {
-        emit_interval(*prog_f, nvars, *a);
+        emit_interval(f->flat, nvars, *a);
       }
     } else if (integer) {
-      auto s = strict ? lower::lower_strict(*prog_i) : lower::lower_fused(*prog_i);
+      auto s = strict ? lower::lower_strict(i->flat) : lower::lower_fused(i->flat);
       a->image = lower::emit_ptx(s, d);
     } else {
       if (d == lower::Domain::I64 || d == lower::Domain::I64F) {
         throw std::invalid_argument("pe_eval_i64 needs a program with int64 coefficients");
       }
-      auto s = strict ? lower::lower_strict(*prog_f) : lower::lower_fused(*prog_f);
+      auto s = strict ? lower::lower_strict(f->flat) : lower::lower_fused(f->flat);
       a->image = lower::emit_ptx(s, d);
     }
     slot = std::move(a);
@@ -190,7 +192,7 @@ Artifact& Program::limb_artifact(std::uint32_t limbs, bool need_cubin) const {
     slot = std::make_unique<Artifact>();
     lower::KernelShape shape;
     shape.limbs = limbs;
-    slot->image = lower::emit_ptx(lower::lower_fused(*prog_i), lower::Domain::I64K, shape);
+    slot->image = lower::emit_ptx(lower::lower_fused(i->flat), lower::Domain::I64K, shape);
   }
   if (need_cubin && slot->cubin.empty()) {
     CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);
@@ -209,23 +211,24 @@ Artifact& Program::loaded_limbs(std::uint32_t limbs, int device) const {
 }
 
 std::uint32_t limbs_needed(const Program& p, const std::uint64_t* bounds) {
-  if (p.terms_i.empty()) return 1;
+  const auto& T = p.i->terms;
+  if (T.empty()) return 1;
   std::vector<double> lx(p.nvars);
   for (std::uint32_t v = 0; v < p.nvars; ++v) {
     lx[v] = std::log2(std::max<double>(1.0, static_cast<double>(bounds[v])));
   }
   double worst = 0.0, max_pow = 0.0;
-  for (const auto& t : p.terms_i) {
-    const double c = std::fabs(static_cast<double>(t.coefficient));
+  for (std::size_t t = 0; t < T.size(); ++t) {
+    const double c = std::fabs(static_cast<double>(T.coefs[t]));
     double bits = c > 0 ? std::log2(c) : 0.0;
     for (std::uint32_t v = 0; v < p.nvars; ++v) {
-      bits += t.exponents[v] * lx[v];
-      max_pow = std::max(max_pow, t.exponents[v] * lx[v]);
+      bits += T.exp(t, v) * lx[v];
+      max_pow = std::max(max_pow, T.exp(t, v) * lx[v]);
     }
     worst = std::max(worst, bits);
   }
   // M <= T * max term; 1e-6 relative + 1 bit of slack for log2 rounding
-  const double need = std::max(worst + std::log2(static_cast<double>(p.terms_i.size())), max_pow) *
+  const double need = std::max(worst + std::log2(static_cast<double>(T.size())), max_pow) *
                           (1 + 1e-6) + 1.0;
   for (std::uint32_t k = 1; k <= 8; ++k) {
     if (need < 64.0 * k - 1.0) return k;
@@ -233,86 +236,17 @@ std::uint32_t limbs_needed(const Program& p, const std::uint64_t* bounds) {
   return 0;
 }
 
-std::size_t Program::slice_count() const {
-  if (integer || !poly_f) return 1;  // no terms/schemes (pe_program_from_compiled): unsliced
-  std::size_t k = 0;
-  if (const char* e = std::getenv("PE_SLICES")) k = static_cast<std::size_t>(std::atoi(e));
-  if (k == 0) {
-    // measured on C4 (profiles/r1_slices_c4.txt, r1_imm6_sweep.txt):
-    // straight-line kernels beyond a few thousand records pay for
-    // instruction fetch and register pressure (power tables); ~3k records
-    // per slice with paired coefficient loads (2k before them)
-    k = stats.records >= 8192 ? std::clamp<std::size_t>(stats.records / 3000, 2, 256) : 1;
+Artifact::~Artifact() {
+  for (auto& [dev, ptr] : global_coefs) {
+    if (cudaSetDevice(dev) == cudaSuccess) cudaFree(ptr);
   }
-  return std::min<std::size_t>(std::max<std::size_t>(1, k), std::max<std::size_t>(1, nterms));
+  if (library) cudaLibraryUnload(library);
 }
 
-std::vector<const Artifact*> Program::f64_kernels(int device) const {
-  const std::size_t k = slice_count();
-  if (k <= 1) return {&loaded(lower::Domain::F64, device)};
+void Program::release() const {
   std::lock_guard<std::mutex> lock(mu);
-  if (!slices_planned) {
-    // terms are in decreasing lexicographic order: equal outer exponents are
-    // contiguous; cut at outer-exponent boundaries near multiples of T/k
-    const auto& terms = poly_f->terms();
-    const std::size_t T = terms.size();
-    std::vector<std::size_t> cuts{0};
-    for (std::size_t i = 1; i < T && cuts.size() < k; ++i) {
-      if (terms[i].exponents[0] != terms[i - 1].exponents[0] && i * k >= cuts.size() * T) {
-        cuts.push_back(i);
-      }
-    }
-    cuts.push_back(T);
-    std::vector<FunctionScheme> fs;
-    for (const auto& d : scheme_descs) fs.push_back(scheme_from_desc(d));
-    for (std::size_t s = 0; s + 1 < cuts.size(); ++s) {
-      std::vector<Term<double>> part(terms.begin() + static_cast<std::ptrdiff_t>(cuts[s]),
-                                     terms.begin() + static_cast<std::ptrdiff_t>(cuts[s + 1]));
-      Polynomial<double> sp = Polynomial<double>::canonicalize(std::move(part), variables);
-      EvaluationTree<double> t = nvars == 1 ? build(sp, fs[0], 0)
-                                            : build_multivariate(sp, std::span<const FunctionScheme>(fs));
-      compute_lazy_heights(t);
-      slice_progs.push_back(std::make_unique<CompiledProgram<double>>(compile(t)));
-      auto a = std::make_unique<Artifact>();
-      lower::KernelShape shape;
-      shape.accumulate = s > 0;
-      a->image = lower::emit_ptx(lower::lower_fused(*slice_progs.back()), lower::Domain::F64, shape);
-      slice_arts.push_back(std::move(a));
-    }
-    // ptxas the slices concurrently (independent modules; nvPTXCompiler
-    // handles are independent)
-    std::vector<std::future<CompileResult>> jobs;
-    const std::size_t width = std::max(1u, std::thread::hardware_concurrency());
-    for (std::size_t s = 0; s < slice_arts.size(); ++s) {
-      if (jobs.size() == width) {
-        // bounded fan-out: finish the oldest before starting another
-        CompileResult r = jobs.front().get();
-        jobs.erase(jobs.begin());
-        if (!r.ok) throw std::logic_error(r.log);
-        auto& done = slice_arts[s - width];
-        done->cubin = std::move(r.cubin);
-        done->compile_seconds = r.seconds;
-      }
-      const Artifact* a = slice_arts[s].get();
-      jobs.push_back(std::async(std::launch::async, [a] {
-        return compile_ptx_cached(a->image.ptx, a->image.entry);
-      }));
-    }
-    for (std::size_t i = 0; i < jobs.size(); ++i) {
-      CompileResult r = jobs[i].get();
-      if (!r.ok) throw std::logic_error(r.log);
-      auto& done = slice_arts[slice_arts.size() - jobs.size() + i];
-      done->cubin = std::move(r.cubin);
-      done->compile_seconds = r.seconds;
-    }
-    slices_planned = true;
-  }
-  std::vector<const Artifact*> out;
-  for (auto& a : slice_arts) {
-    ensure_loaded(*a, device);
-    out.push_back(a.get());
-  }
-  return out;
+  for (auto& a : artifacts) a.reset();
+  limb_arts.clear();
 }
 
 namespace {

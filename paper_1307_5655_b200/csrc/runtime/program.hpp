@@ -13,7 +13,10 @@
 #include <string>
 #include <vector>
 
-#include "front/compile.hpp"
+#include "front/flat.hpp"
+#include "front/forest.hpp"
+#include "front/split.hpp"
+#include "front/terms.hpp"
 #include "lower/ptx.hpp"
 
 namespace polyeval::rt {
@@ -49,10 +52,26 @@ struct Artifact {
   bool partitioned() const {
     return image.iv_partition == 1 && mirror && mirror->image.iv_partition == 2;
   }
+  Artifact() = default;
+  Artifact(const Artifact&) = delete;
+  Artifact& operator=(const Artifact&) = delete;
+  /// Frees the per-device coefficient copies and unloads the library (the
+  /// mirror module goes with its owner).
+  ~Artifact();
 };
 
 /// Resolves a.fn / a.fix_fn for `device` (current device = `device`).
 void bind_functions(Artifact& a, int device);
+
+/// Host front-end state of one coefficient type: the canonical terms, the
+/// evaluation trees (absent for pe_program_from_compiled) and the compiled
+/// walk the kernels are generated from.
+template <typename C>
+struct Front {
+  front::TermTable<C> terms;         // canonical (create) or one row per scalar record (import)
+  std::unique_ptr<front::Forest<C>> forest;
+  front::FlatProgram<C> flat;
+};
 
 struct Program {
   std::uint32_t nvars = 0;
@@ -60,21 +79,10 @@ struct Program {
   std::uint64_t nterms = 0;
   std::vector<std::string> variables;
 
-  std::unique_ptr<EvaluationTree<double>> tree_f;
-  std::unique_ptr<CompiledProgram<double>> prog_f;
-  // fp64 slicing of wide multivariate programs: terms split at outer-variable
-  // exponent boundaries into K sub-polynomials, each compiled with the same
-  // schemes; slice 0 stores, slices 1..K-1 accumulate (fused fp64 only).
-  std::unique_ptr<Polynomial<double>> poly_f;
-  std::vector<SchemeDesc> scheme_descs;
-  mutable std::vector<std::unique_ptr<CompiledProgram<double>>> slice_progs;
-  mutable std::vector<std::unique_ptr<Artifact>> slice_arts;
-  mutable bool slices_planned = false;
-  std::unique_ptr<EvaluationTree<std::int64_t>> tree_i;
-  std::unique_ptr<CompiledProgram<std::int64_t>> prog_i;
-  std::vector<Term<std::int64_t>> terms_i;  // canonical terms (int64 proof)
+  std::unique_ptr<Front<double>> f;         // fp64 coefficients
+  std::unique_ptr<Front<std::int64_t>> i;   // int64 coefficients
 
-  ProgramStats stats;
+  front::WalkStats stats;
   // int64: largest B such that all |x_v| <= B is provably wrap-free;
   // variables absent from the polynomial get UINT64_MAX.
   std::vector<std::uint64_t> i64_uniform_bound;
@@ -89,14 +97,13 @@ struct Program {
   Artifact& artifact(lower::Domain d, bool need_cubin) const;
   /// Loaded kernel handle + global-tier coefficients on `device`.
   Artifact& loaded(lower::Domain d, int device) const;
-  /// Kernels pe_eval_f64 (fused) launches in order: the whole program, or
-  /// its slices for wide programs.
-  std::vector<const Artifact*> f64_kernels(int device) const;
-  std::size_t slice_count() const;
   /// K-limb exact integer kernel (Domain::I64K): generated (+ compiled), or
   /// loaded on `device`.
   Artifact& limb_artifact(std::uint32_t limbs, bool need_cubin) const;
   Artifact& loaded_limbs(std::uint32_t limbs, int device) const;
+  /// Unloads every kernel library and frees the device coefficient copies.
+  void release() const;
+  ~Program() { release(); }
 };
 
 /// Smallest K (1..8) with every intermediate provably below 2^(64K-1) for

@@ -231,3 +231,33 @@ def test_scheme_range_violation_is_invalid_argument():
                 rec, rc = pyoracle.Oracle(p, [s]).records()
                 prog = pe.compile(p, [s])
                 assert np.array_equal(prog.records(), rec) and prog.info()["register_count"] == rc
+
+
+@pytest.mark.skipif(not pyoracle.ref_available(), reason="reference library not built here")
+def test_multivariate_dot_matches_reference():
+    # nested-coefficient labels render the inner polynomial over the suffix
+    # variables (reference tree.cpp:290-309 + parser.cpp render)
+    rng = np.random.default_rng(41)
+    for nv in (2, 3):
+        for trial in range(6):
+            t = int(rng.integers(1, 40))
+            ex = rng.integers(0, 6, size=(t, nv))
+            c = rng.integers(-9, 10, size=t).astype(np.int64)
+            c[c == 0] = 1
+            p = pe.Polynomial(ex, c)
+            for s in SCHEMES:
+                sch = [pe.builtin_scheme(s)] * nv
+                prog = pe.compile(p, sch)
+                assert prog.dot() == pyoracle.Reference(p, sch).dot(), (nv, trial, s)
+                rr, rc = pyoracle.Reference(p, sch).records()
+                assert np.array_equal(prog.records(), rr) and prog.info()["register_count"] == rc
+
+
+def test_deep_horner_builds_without_recursion():
+    # the builder is iterative: a 200k-term Horner chain (tree depth 200k)
+    # needs no deep stack
+    n = 200_000
+    p = pe.Polynomial(np.arange(n).reshape(-1, 1), np.ones(n, dtype=np.int64))
+    prog = pe.compile(p, pe.builtin_scheme("horner"))
+    inf = prog.info()
+    assert inf["records"] == n and inf["register_count"] == 1 and inf["walk_muls"] == n - 1
