@@ -42,9 +42,12 @@
  *   - Point and result buffers are caller-owned, structure-of-arrays: coords[v]
  *     points at n values of variable v (variable order of the program).
  *     Pointers may be device memory (evaluated in place, asynchronously on
- *     exec->stream) or host memory (staged through pinned buffers with
- *     copy/compute overlap; the call returns when results are on the host).
- *     n == 0 is valid and does nothing.
+ *     exec->stream) or host memory (chunked H2D / walk / D2H pipeline on the
+ *     library's own streams, copies overlapping the neighbouring chunks'
+ *     walks; pageable memory is first copied into page-locked staging
+ *     buffers by host threads; the call returns when results are on the
+ *     host). All buffers of one call must be device memory (of one device) or
+ *     all host memory, else PE_EINVAL. n == 0 is valid and does nothing.
  */
 #ifndef POLYEVAL_B200_H_
 #define POLYEVAL_B200_H_
@@ -116,7 +119,10 @@ typedef struct pe_exec {
    * Device-buffer calls reject ndevices > 1 (their data lives on one device). */
   const int32_t* devices;
   int32_t ndevices;
-  int32_t reserved2;
+  /* Host-buffer calls: points per pipeline chunk (0 = n/16 clamped to
+   * [256K, 4M]) and chunks in flight (0 = 3; 2..8). */
+  int32_t stage_slots;
+  uint64_t stage_chunk;
 } pe_exec;
 
 /* Compiles a polynomial given as raw terms: `exponents` is nterms x nvars
@@ -171,6 +177,31 @@ pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t n
                                    pe_program** out);
 
 void pe_program_destroy(pe_program* program);
+
+/* Code-generation options of a program's kernels. Zero-initialise for the
+ * measured defaults; every field's 0 means "default". */
+typedef struct pe_tuning {
+  uint32_t lanes;          /* points per thread, 1..8 */
+  uint32_t block;          /* threads per CTA, 32..1024 */
+  uint32_t min_ctas;       /* .minnctapersm of the walk kernel */
+  uint32_t sync_every;     /* walk ops between CTA barriers */
+  uint32_t section_ops;    /* long int/fp64 walks: ops per barrier-separated section
+                              (default 3000; UINT32_MAX = never section) */
+  uint32_t sched_window;   /* latency-aware op reordering window (1 = walk order) */
+  uint32_t sched_distance; /* producer distance the reordering aims for */
+  uint32_t chain_min;      /* shortest Horner run emitted as a loop (default 64;
+                              UINT32_MAX = never) */
+  int32_t iv_fast;         /* interval: -1 = bit-level replay only (no fast path) */
+  int32_t iv_mid;          /* interval fixup: -1 = skip the finite-case replay */
+  int32_t iv_partition;    /* univariate interval sign partition: -1 = off */
+  int32_t carry_powers;    /* sections: 1 = keep power tables live across sections */
+  uint64_t iv_partition_min; /* smallest batch that is sign-partitioned (default 65536) */
+} pe_tuning;
+
+/* Replaces the program's code-generation options and drops its generated
+ * kernels (they are regenerated on next use). Not thread-safe with respect
+ * to concurrent evaluation of the same program. */
+pe_status pe_program_set_tuning(pe_program* program, const pe_tuning* tuning);
 
 typedef struct pe_program_info_t {
   uint32_t nvars;
@@ -235,8 +266,8 @@ pe_status pe_program_compile_only(const pe_program* program, int32_t domain,
 pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63,
                                 uint64_t* bound53);
 
-/* Number of kernels a fused pe_eval_f64 launches (wide programs are split
- * into slices at outer-variable exponent boundaries). */
+/* Barrier-separated sections of the fused fp64 kernel (long walks are cut
+ * where few walk values are live; the op sequence is unchanged). */
 pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices);
 
 /* Batch evaluation. coords: nvars pointers, each to n values. */

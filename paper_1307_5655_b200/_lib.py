@@ -40,7 +40,27 @@ class pe_exec(C.Structure):
         ("reserved", C.c_int32),
         ("devices", C.POINTER(C.c_int32)),
         ("ndevices", C.c_int32),
-        ("reserved2", C.c_int32),
+        ("stage_slots", C.c_int32),
+        ("stage_chunk", C.c_uint64),
+    ]
+
+
+class pe_tuning(C.Structure):
+    """Code-generation options (include/polyeval_b200.h pe_tuning); 0 = default."""
+    _fields_ = [
+        ("lanes", C.c_uint32),
+        ("block", C.c_uint32),
+        ("min_ctas", C.c_uint32),
+        ("sync_every", C.c_uint32),
+        ("section_ops", C.c_uint32),
+        ("sched_window", C.c_uint32),
+        ("sched_distance", C.c_uint32),
+        ("chain_min", C.c_uint32),
+        ("iv_fast", C.c_int32),
+        ("iv_mid", C.c_int32),
+        ("iv_partition", C.c_int32),
+        ("carry_powers", C.c_int32),
+        ("iv_partition_min", C.c_uint64),
     ]
 
 
@@ -94,6 +114,7 @@ EXPORTS = [
       C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_size_t), C.c_int,
       C.POINTER(C.c_void_p)]),
     ("pe_program_destroy", None, [C.c_void_p]),
+    ("pe_program_set_tuning", C.c_int, [C.c_void_p, C.POINTER(pe_tuning)]),
     ("pe_program_info", C.c_int, [C.c_void_p, C.POINTER(pe_program_info_t)]),
     ("pe_program_exponents", C.c_int,
      [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_size_t)]),

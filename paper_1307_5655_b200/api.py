@@ -104,11 +104,32 @@ class Polynomial:
     variables: tuple = ("x",)
 
     def __post_init__(self):
-        self.exponents = np.ascontiguousarray(np.asarray(self.exponents, dtype=np.uint32))
+        # range checks before any cast: astype would wrap silently
+        e = np.asarray(self.exponents)
+        if e.dtype.kind not in "iu":
+            if e.dtype.kind == "f" and np.all(np.isfinite(e)) and np.all(e == np.floor(e)):
+                e = e.astype(np.float64)
+            elif e.dtype != object:
+                raise ValueError("exponents must be integers")
+        if e.size:
+            lo, hi = (int(e.min()), int(e.max())) if e.dtype != object else \
+                (min(int(v) for v in e.flat), max(int(v) for v in e.flat))
+            if lo < 0 or hi >= 2**32:
+                raise ValueError("exponents must lie in [0, 2^32)")
+        self.exponents = np.ascontiguousarray(np.asarray(e).astype(np.int64).astype(np.uint32))
         if self.exponents.ndim == 1:
             self.exponents = self.exponents.reshape(-1, 1)
         c = np.asarray(self.coefficients)
-        if c.dtype.kind in "iu":
+        if c.dtype == object and all(isinstance(v, (int, np.integer)) for v in c.flat):
+            c = np.asarray([int(v) for v in c.flat], dtype=object).reshape(c.shape)
+            if c.size and (min(c.flat) < -2**63 or max(c.flat) >= 2**63):
+                raise OverflowError("integer coefficients must fit int64")
+            c = c.astype(np.int64)
+        elif c.dtype.kind == "u":
+            if c.size and int(c.max()) >= 2**63:
+                raise OverflowError("integer coefficients must fit int64")
+            c = c.astype(np.int64)
+        elif c.dtype.kind == "i":
             c = c.astype(np.int64)
         else:
             c = c.astype(np.float64)
@@ -287,6 +308,17 @@ class CompiledProgram:
         L.check(L.lib().pe_program_f64_slices(self._h, C.byref(k)))
         return k.value
 
+    def set_tuning(self, **options) -> None:
+        """Code-generation options (pe_tuning fields, e.g. lanes=2,
+        section_ops=4000, iv_fast=-1); drops the generated kernels."""
+        t = L.pe_tuning()
+        names = {f for f, _ in L.pe_tuning._fields_}
+        for k, v in options.items():
+            if k not in names:
+                raise ValueError(f"unknown tuning option {k!r}")
+            setattr(t, k, int(v))
+        L.check(L.lib().pe_program_set_tuning(self._h, C.byref(t)))
+
     def compile_only(self, domain: int) -> int:
         nb = C.c_uint64()
         L.check(L.lib().pe_program_compile_only(self._h, domain, C.byref(nb)))
@@ -329,6 +361,18 @@ class BigIntDomain:
 
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _check_tensor(t, dtype, what):
+    """A CUDA tensor is handed to the kernels as a raw pointer: its element
+    type must be exactly the domain's (float32 data read as float64 would run
+    past the buffer)."""
+    import torch
+    want = torch.float64 if np.dtype(dtype) == np.float64 else torch.int64
+    if t.dtype != want:
+        raise TypeError(f"{what} tensor must have dtype {want}, got {t.dtype}")
+    if t.dim() != 1:
+        raise ValueError(f"{what} tensor must be one-dimensional")
 
 
 class Evaluator:
@@ -385,8 +429,14 @@ class Evaluator:
         if len(points) != self.program.nvars:
             raise ValueError("evaluation point arity mismatch")
         cols = []
+        on_gpu = [_is_torch_cuda(p) for p in points]
+        if any(on_gpu) and not all(on_gpu):
+            raise ValueError("coordinates must be all CUDA tensors or all host arrays")
         for p in points:
             if _is_torch_cuda(p):
+                _check_tensor(p, dtype, "coordinate")
+                if p.device != points[0].device:
+                    raise ValueError("all coordinate tensors must be on one device")
                 if not p.is_contiguous():
                     p = p.contiguous()
                 cols.append(p)
@@ -396,6 +446,27 @@ class Evaluator:
         if len(n) != 1:
             raise ValueError("all coordinate arrays must have the same length")
         return cols, n.pop()
+
+    @staticmethod
+    def _check_out(out, dtype, n, like):
+        """out= must live where the coordinates do, with the result dtype."""
+        if _is_torch_cuda(like):
+            if not _is_torch_cuda(out):
+                raise ValueError("out must be a CUDA tensor for CUDA coordinates")
+            _check_tensor(out, dtype, "out")
+            if out.device != like.device:
+                raise ValueError("out must be on the coordinates' device")
+            if not out.is_contiguous():
+                raise ValueError("out must be contiguous")
+        else:
+            if not isinstance(out, np.ndarray):
+                raise ValueError("out must be a numpy array for host coordinates")
+            if out.dtype != np.dtype(dtype):
+                raise TypeError(f"out must have dtype {np.dtype(dtype)}, got {out.dtype}")
+            if not out.flags.c_contiguous or not out.flags.writeable:
+                raise ValueError("out must be a writeable contiguous array")
+        if int(out.shape[0]) != n or len(out.shape) != 1:
+            raise ValueError(f"out must have shape ({n},)")
 
     @staticmethod
     def _ptr(a):
@@ -413,8 +484,12 @@ class Evaluator:
             if n != n2:
                 raise ValueError("lo/hi length mismatch")
             dev = _is_torch_cuda(lo_c[0])
+            if dev != _is_torch_cuda(hi_c[0]) or (dev and hi_c[0].device != lo_c[0].device):
+                raise ValueError("lo and hi must live on the same device")
             if out is None:
                 out = (self._alloc(n, "f64", dev, lo_c[0]), self._alloc(n, "f64", dev, lo_c[0]))
+            for o in out:
+                self._check_out(o, np.float64, n, lo_c[0])
             lo_p = (C.c_void_p * len(lo_c))(*[self._ptr(a) for a in lo_c])
             hi_p = (C.c_void_p * len(hi_c))(*[self._ptr(a) for a in hi_c])
             ex = self._exec(self._stream(stream, lo_c[0]))
@@ -429,6 +504,7 @@ class Evaluator:
         dev = _is_torch_cuda(cols[0])
         if out is None:
             out = self._alloc(n, "i64" if integer else "f64", dev, cols[0])
+        self._check_out(out, np.int64 if integer else np.float64, n, cols[0])
         ptrs = (C.c_void_p * len(cols))(*[self._ptr(a) for a in cols])
         ex = self._exec(self._stream(stream, cols[0]), bounds=bounds)
         fn = lib.pe_eval_i64 if integer else lib.pe_eval_f64
@@ -519,6 +595,10 @@ def evaluate_many(programs, points, outs=None, device: int = -1, stream=None, de
     dev = _is_torch_cuda(cols[0])
     if outs is None:
         outs = [Evaluator._alloc(n, "f64", dev, cols[0]) for _ in programs]
+    if len(outs) != len(programs):
+        raise ValueError("one output per program")
+    for o in outs:
+        Evaluator._check_out(o, np.float64, n, cols[0])
     handles = (C.c_void_p * len(programs))(*[p.handle.value for p in programs])
     ptrs = (C.c_void_p * len(cols))(*[Evaluator._ptr(a) for a in cols])
     optrs = (C.c_void_p * len(outs))(*[Evaluator._ptr(o) for o in outs])

@@ -437,6 +437,30 @@ pe_status pe_program_from_compiled(const pe_compiled_program* programs, size_t n
 
 void pe_program_destroy(pe_program* program) { delete program; }
 
+pe_status pe_program_set_tuning(pe_program* program, const pe_tuning* t) {
+  return guarded([&]() -> pe_status {
+    if (!program || !t) return fail(PE_EINVAL, "null argument");
+    Program& p = program->impl;
+    p.release();
+    std::lock_guard<std::mutex> lock(p.mu);
+    lower::Tuning& d = p.tuning;
+    d.lanes = t->lanes;
+    d.block = t->block;
+    d.min_ctas = t->min_ctas;
+    d.sync_every = t->sync_every;
+    d.section_ops = t->section_ops;
+    d.sched_window = t->sched_window;
+    d.sched_distance = t->sched_distance;
+    d.chain_min = t->chain_min;
+    d.iv_fast = t->iv_fast;
+    d.iv_mid = t->iv_mid;
+    d.iv_partition = t->iv_partition;
+    d.carry_powers = t->carry_powers;
+    d.iv_partition_min = t->iv_partition_min;
+    return PE_OK;
+  });
+}
+
 pe_status pe_program_info(const pe_program* program, pe_program_info_t* info) {
   return guarded([&]() -> pe_status {
     if (!program || !info) return fail(PE_EINVAL, "null argument");
@@ -571,7 +595,7 @@ pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63, ui
 pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices) {
   return guarded([&]() -> pe_status {
     if (!program || !slices) return fail(PE_EINVAL, "null argument");
-    *slices = 1;
+    *slices = program->impl.artifact(lower::Domain::F64, false).image.sections;
     return PE_OK;
   });
 }
@@ -659,7 +683,8 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     std::vector<void*> outs{out};
     LaunchArgs la;
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
-    run_batch(arts, dev, kind, n, ins, outs, la, s, exec && exec->synchronize);
+    run_batch(arts, dev, kind, n, ins, outs, la, s, exec && exec->synchronize, false, {},
+              staging_of(exec));
     return PE_OK;
   });
 }
@@ -701,7 +726,8 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
     std::vector<void*> o(outs, outs + k);
     LaunchArgs la;
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
-    run_batch(arts, dev, kind, n, ins, o, la, s, exec && exec->synchronize, false, base);
+    run_batch(arts, dev, kind, n, ins, o, la, s, exec && exec->synchronize, false, base,
+              staging_of(exec));
     return PE_OK;
   });
 }
@@ -745,12 +771,6 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
         la.list = reinterpret_cast<std::uint64_t>(st.list);
         la.count = reinterpret_cast<std::uint64_t>(st.count);
         la.cap = st.list_cap;
-        // PE_IV_OVERLAP=1: chunked, fixup kernels on a side stream beside the
-        // next chunk's fast path — measured slower on C5 (1.66 vs 1.56 ms per
-        // 1e7: the replay's CTAs take SM slots from the fast path), so opt-in
-        if (const char* e = std::getenv("PE_IV_OVERLAP"); e && std::atoi(e) == 1) {
-          la.fix_stream = st.side;
-        }
       }
       run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false);
       return PE_OK;
@@ -759,7 +779,7 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
       Flag flag(s);
       LaunchArgs la;
       la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
-      run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false, attempt == 1);
+      run_batch(a, dev, kind, n, ins, {out_lo, out_hi}, la, s, false, attempt == 1, staging_of(exec));
       const unsigned f = flag.read();
       if (f & 2) return fail(PE_EINVAL, "invalid interval endpoints (NaN or lo > hi)");
       if (!(f & 4)) return PE_OK;
@@ -858,7 +878,7 @@ pe_status pe_eval_limbs(const pe_program* program, const int64_t* const* coords,
     LaunchArgs la;
     la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
     la.bounds = bounds;
-    run_batch(a, dev, kind, n, ins, outs, la, s, false);
+    run_batch(a, dev, kind, n, ins, outs, la, s, false, false, staging_of(exec));
     if (flag.read() != 0) return fail(PE_EOVERFLOW, "a coordinate exceeds the asserted bound");
     return PE_OK;
   });
@@ -918,7 +938,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
       LaunchArgs la;
       la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
       la.bounds = b53;
-      run_batch(af, dev, kind, n, ins, {out}, la, s, false);
+      run_batch(af, dev, kind, n, ins, {out}, la, s, false, false, staging_of(exec));
       if (flag.read() == 0) return PE_OK;
       if (caller_bounds) {
         return fail(PE_EOVERFLOW, "a coordinate exceeds the asserted int64 bound");
@@ -931,7 +951,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
       LaunchArgs la;
       la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
       la.bounds = bounds;
-      run_batch(a, dev, kind, n, ins, {out}, la, s, false);
+      run_batch(a, dev, kind, n, ins, {out}, la, s, false, false, staging_of(exec));
       if (flag.read() == 0) return PE_OK;
       if (caller_bounds || attempt == 1) break;
       // Some coordinate exceeded the uniform bound: derive the batch's real
@@ -989,7 +1009,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
     LaunchArgs la;
     la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
     la.bounds = actual;
-    run_batch(ak, dev, kind, n, ins, limbs, la, s, false);
+    run_batch(ak, dev, kind, n, ins, limbs, la, s, false, false, staging_of(exec));
     bool fits = true;
     if (kind == MemKind::Device) {
       std::vector<const unsigned long long*> lp(K);

@@ -45,53 +45,38 @@ const char* domain_name(Domain d) {
   return "?";
 }
 
-KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
-                          std::uint64_t distinct_coefs) {
+KernelShape default_shape(Domain d, std::uint32_t powers, std::uint64_t distinct_coefs,
+                          const Tuning& t) {
   // Measured on B200 (profiles/r1_shape_sweep.txt): the fp64 walk of a
   // one-point-per-thread kernel is bound by per-thread constant loads (MIO);
   // P points per thread share each coefficient load. One 512-thread CTA per
   // SM (ptxas capped at 128 registers) beats several 128-thread CTAs.
+  // Coefficients: a DFMA reads at most one uniform register, so the walk's
+  // coefficients split into uniform-bound words (paired 16-byte LDCU) and the
+  // register-bound second coefficient of fma(c, x^d, c') leaves (paired
+  // per-thread LDC) — profiles/r1_imm6_sweep.txt: C4 4.23 -> 3.71 ms per 4e6
+  // points, C2 0.683 -> 0.646 ms per 1e7, C3 0.610 -> 0.579 ms per 1e7.
   KernelShape s;
-  (void)ops;
-  // Coefficient delivery (imm_mode): a DFMA reads at most one uniform
-  // register, so the walk's coefficients split into uniform-bound words
-  // (paired LDCU.128) and the register-bound second coefficient of
-  // fma(c, x^d, c') leaves (per-thread LDC); the earlier alternation of
-  // constant loads and immediates (mode 2, profiles/r1_imm_sweep.txt) spent
-  // two ALU/uniform MOVs per immediate and left C4 issue-bound.
   if (d == Domain::Interval) {
-    s = {1, 512, 32, 0};  // integer-pipe bound; no coefficient pressure
+    s = {1, 512, 32};  // integer-pipe bound; no coefficient pressure
   } else if (d == Domain::I64K) {
-    s = {1, 256, 0, 0};   // K-limb registers: one point per thread
-  } else if (powers > 32) {
-    // very wide programs (large power tables): registers are the limit
-    s = {1, 512, 0, 6};
-  } else if (distinct_coefs < 64) {
-    // few distinct coefficients: independent sub-chains give enough ILP
-    s = {1, 512, 0, 6};
+    s = {1, 256, 0};   // K-limb registers: one point per thread
+  } else if (powers > 32 || distinct_coefs < 64) {
+    // very wide programs (large power tables): registers are the limit; few
+    // distinct coefficients: independent sub-chains give enough ILP
+    s = {1, 512, 0};
   } else {
-    s = {4, 256, 0, 6};
+    s = {4, 256, 0};
     s.min_ctas = 2;  // <= 128 registers: two CTAs (16 warps) per SM
   }
-  // imm_mode 6 (profiles/r1_imm6_sweep.txt): uniform-bound coefficients in
-  // paired 16-byte LDCUs, the second coefficient of two-coefficient FMAs as
-  // per-thread LDCs — C4 4.23 -> 3.71 ms per 4e6 points (with 4 slices), C2
-  // 0.683 -> 0.646 ms per 1e7, C3 0.610 -> 0.579 ms per 1e7.
   // strict fp64 keeps every reference add: more live temporaries; a 512-wide
   // CTA caps ptxas at 128 registers so two CTAs fit an SM (C2 balanced d1000
   // strict: 174 registers at 256 wide, 2.54 -> 1.46 ms per 1e7 points)
   if (d == Domain::F64Strict && s.block < 512) s.block = 512;
-  auto env = [](const char* name, std::uint32_t lo, std::uint32_t hi, std::uint32_t& out) {
-    if (const char* e = std::getenv(name)) {
-      const long v = std::atol(e);
-      if (v >= static_cast<long>(lo) && v <= static_cast<long>(hi)) out = static_cast<std::uint32_t>(v);
-    }
-  };
-  env("PE_LANES", 1, 8, s.lanes);
-  env("PE_BLOCK", 32, 1024, s.block);
-  env("PE_SYNC", 0, 1u << 20, s.sync_every);
-  env("PE_IMM", 0, 6, s.imm_mode);
-  env("PE_MINCTAS", 0, 32, s.min_ctas);
+  if (t.lanes >= 1 && t.lanes <= 8) s.lanes = t.lanes;
+  if (t.block >= 32 && t.block <= 1024) s.block = t.block;
+  if (t.sync_every) s.sync_every = t.sync_every;
+  if (t.min_ctas) s.min_ctas = t.min_ctas;
   return s;
 }
 
@@ -138,13 +123,12 @@ struct ChainRun {
 
 template <typename C>
 std::vector<ChainRun> chain_runs(const Stream<C>& s, Domain d, std::uint32_t sync_every,
-                                 std::uint64_t budget) {
+                                 std::uint64_t budget, std::uint32_t chain_min) {
   std::vector<ChainRun> runs;
   if (s.strict || sync_every != 0) return runs;
   if (d != Domain::F64 && d != Domain::I64F && d != Domain::I64) return runs;
-  std::size_t min_run = 64;
-  if (const char* e = std::getenv("PE_LOOP")) min_run = static_cast<std::size_t>(std::atol(e));
-  if (min_run == 0) return runs;
+  const std::size_t min_run = chain_min ? chain_min : 64;
+  if (chain_min == UINT32_MAX) return runs;
   // uses of the value each op defines (registers may be redefined)
   const std::size_t n = s.ops.size();
   std::vector<std::uint32_t> uses(n, 0);
@@ -201,12 +185,12 @@ std::vector<ChainRun> chain_runs(const Stream<C>& s, Domain d, std::uint32_t syn
 template <typename C>
 class Emitter {
  public:
-  Emitter(const Stream<C>& s, Domain d, const KernelShape& shape)
+  Emitter(const Stream<C>& s, Domain d, const KernelShape& shape, const Tuning& t,
+          std::vector<std::size_t> cuts)
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
-        imm_mode_(shape.imm_mode), min_ctas_(shape.min_ctas), accumulate_(shape.accumulate),
+        paired_(d != Domain::Interval && d != Domain::I64K), min_ctas_(shape.min_ctas),
         K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1),
-        part_(shape.iv_partition) {
-    if (accumulate_ && d_ != Domain::F64) throw std::logic_error("accumulate is fp64-only");
+        part_(shape.iv_partition), tuning_(t), cuts_(std::move(cuts)) {
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
 
@@ -262,12 +246,15 @@ class Emitter {
     if (fast) {
       // exact fast path; points it cannot prove go to the fixup list
       emit_fast_body();
+    } else if (cuts_.size() > 1) {
+      emit_sectioned();
     } else {
       emit_prologue();
       emit_powers();
       emit_walk();
       emit_epilogue();
     }
+    img.sections = static_cast<std::uint32_t>(std::max<std::size_t>(1, cuts_.size()));
     const std::string main_entry = entry_text(img, img.entry, 0, min_ctas_);
 
     // fixup entry: exact replay of the listed points, one per thread
@@ -280,7 +267,7 @@ class Emitter {
       reset_entry();
       fix_ = true;
       emit_fix_prologue();
-      if (mid_replay_) {
+      if (tuning_.iv_mid >= 0) {
         // finite-case replay first; the bit-level replay only on %pmid
         decls_ << "  .reg .pred %pmid;\n  .reg .f64 %macc;\n";
         body_ << "  mov.f64 %macc, 0d0000000000000000;\n";
@@ -309,11 +296,8 @@ class Emitter {
       // C5): the replay is latency-bound, so every listed point gets its own
       // thread and occupancy helps (C5 fixup per 1e8: 612 -> 590 us at 6,
       // 584 us at 8 but with spills; profiles/r1_c5_fix_shape.txt).
-      // PE_FIX_BLOCK / PE_FIX_CTAS override for tuning.
       img.fix_block = 128;
       img.fix_ctas_per_sm = 6;
-      if (const char* e = std::getenv("PE_FIX_BLOCK")) img.fix_block = static_cast<std::uint32_t>(std::atoi(e));
-      if (const char* e = std::getenv("PE_FIX_CTAS")) img.fix_ctas_per_sm = static_cast<std::uint32_t>(std::atoi(e));
       fix_entry = entry_text(img, img.fix_entry, img.fix_block, img.fix_ctas_per_sm);
       P_ = lanes;
       sync_every_ = sync;
@@ -445,18 +429,15 @@ class Emitter {
       dedup.emplace(w, idx);
       return idx;
     };
-    // imm_mode 5 (scalar domains): an FMA can take one uniform-register
-    // operand, so the second coefficient of a two-coefficient op
-    // (fma(c, x^d, c'), the leaves of every scheme) is register-bound. Those
-    // become immediates; every other coefficient is uniform-bound, and only
-    // those words go to the constant bank, in first-use order, where they
-    // arrive two per 16-byte LDCU (load_word).
+    // Scalar domains: an FMA can take one uniform-register operand, so the
+    // second coefficient of a two-coefficient op (fma(c, x^d, c'), the leaves
+    // of every scheme) is register-bound. Uniform-bound words go to the
+    // constant bank first, deduplicated, in first-use order (they arrive two
+    // per 16-byte LDCU, load_word); the register-bound words follow as a
+    // second region in first-use order (paired loads: ptxas turns those into
+    // per-thread 16-byte LDCs, one issue slot per two coefficients).
     reg_bound_.assign(s_.coefs.size(), 0);
-    // imm_mode 6: the register-bound words are not immediates but a second
-    // constant-bank region (first-use order, paired loads: ptxas turns those
-    // into per-thread 16-byte LDCs, one issue slot per two coefficients).
-    const bool split = (imm_mode_ == 5 || imm_mode_ == 6) && d_ != Domain::Interval &&
-                       d_ != Domain::I64K;
+    const bool split = paired_;
     if (split) {
       for (const Op& op : s_.ops) {
         const int nc = op.a.is(Operand::Coef) + op.b.is(Operand::Coef) + op.c.is(Operand::Coef);
@@ -466,7 +447,7 @@ class Emitter {
       }
     }
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
-      if (split && reg_bound_[k]) continue;  // emitted as an immediate (load())
+      if (split && reg_bound_[k]) continue;  // second region, below
       if (d_ == Domain::Interval) {
         const IvCoef c = ivcoef(k);
         coef_lo_[k] = word(bits_of(c.lo));
@@ -486,7 +467,7 @@ class Emitter {
         coef_lo_[k] = coef_hi_[k] = word(bits_of(c));
       }
     }
-    if (split && imm_mode_ == 6) {
+    if (split) {
       if (words_.size() & 1) words_.push_back(0);  // region starts on a pair
       for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
         if (!reg_bound_[k]) continue;
@@ -526,9 +507,7 @@ class Emitter {
   // The fast interval path needs finite, nonzero, non-straddling coefficient
   // intervals (checked here once) and a walk that ends in a register.
   bool interval_fast_path_ok() const {
-    if (const char* e = std::getenv("PE_IV_FAST")) {
-      if (std::atoi(e) == 0) return false;
-    }
+    if (tuning_.iv_fast < 0) return false;
     if (!s_.result.is(Operand::Reg)) return false;
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
       const IvCoef c = ivcoef(k);
@@ -548,7 +527,7 @@ class Emitter {
 
   // Loads coefficient word w into a fresh register (shared by all lanes).
   std::string load_word(std::uint32_t w) {
-    if (imm_mode_ >= 4) {
+    if (paired_) {
       // paired uniform loads: words sit in first-use order, so an even word
       // and its odd neighbour arrive in one 16-byte LDCU (half the
       // coefficient-delivery issue slots of one LDCU per word)
@@ -575,12 +554,6 @@ class Emitter {
       }
     }
     std::string r = "%c" + std::to_string(n_creg_++);
-    if (imm_mode_ == 1 || (imm_mode_ == 2 && (w & 1)) || (imm_mode_ == 3 && w >= n_const_)) {
-      // immediate: ptxas materialises it with two 32-bit moves on the ALU /
-      // FMA / uniform pipes instead of a constant-cache load on the MIO queue
-      body_ << "  mov.b64 " << r << ", " << hex64(words_[w]) << ";\n";
-      return r;
-    }
     if (w < n_const_) {
       body_ << "  ld.const." << ldty() << " " << r << ", [pe_coef+" << 8 * w << "];\n";
     } else if (w < n_const_ + n_param_) {
@@ -599,19 +572,22 @@ class Emitter {
     }
     return "%v" + std::to_string(id) + ln(lane);
   }
+  // section suffix of per-section power / coordinate copies (sections
+  // after the first reload the coordinates and rebuild the powers they use)
+  std::string sx() const { return sec_ && tuning_.carry_powers <= 0 ? "s" + std::to_string(sec_) : ""; }
   std::string pw(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) {
       return std::string(fast_ ? "%f" : medium_ ? "%m" : "%") + (hi ? "ph" : "pl") + std::to_string(id) + ln(lane);
     }
-    return "%q" + std::to_string(id) + ln(lane);
+    return "%q" + std::to_string(id) + sx() + ln(lane);
   }
   std::string xr(std::uint32_t v, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) return (hi ? "%xh" : "%xl") + std::to_string(v) + ln(lane);
-    return "%x" + std::to_string(v) + ln(lane);
+    return "%x" + std::to_string(v) + sx() + ln(lane);
   }
   // integer coordinate as loaded (I64: the arithmetic register itself)
   std::string xi(std::uint32_t v, std::uint32_t lane) const {
-    if (d_ == Domain::I64F || d_ == Domain::I64K) return "%xi" + std::to_string(v) + ln(lane);
+    if (d_ == Domain::I64F || d_ == Domain::I64K) return "%xi" + std::to_string(v) + sx() + ln(lane);
     return xr(v, lane);
   }
   // I64K: limb j of a K-limb register name
@@ -623,11 +599,6 @@ class Emitter {
   };
   Loaded load(const Operand& o) {
     if (!o.is(Operand::Coef)) return {};
-    if (o.id < reg_bound_.size() && reg_bound_[o.id] && imm_mode_ == 5) {
-      const std::string r = "%c" + std::to_string(n_creg_++);
-      body_ << "  mov.b64 " << r << ", " << hex64(scalar_word(o.id)) << ";\n";
-      return {r, r};
-    }
     const std::string lo = load_word(coef_lo_[o.id]);
     const std::string hi = coef_hi_[o.id] == coef_lo_[o.id] ? lo : load_word(coef_hi_[o.id]);
     return {lo, hi};
@@ -671,7 +642,7 @@ class Emitter {
             << "  ld.param.u64 %rd21, [pe_pidx];\n  cvta.to.global.u64 %rd21, %rd21;\n";
     }
     emit_chain_warmup();
-    if (sync_every_ == 0) {
+    if (sync_every_ == 0 && cuts_.size() <= 1) {
       // no CTA barriers: threads past the end leave immediately; with
       // barriers every thread stays (clamped loads, predicated stores)
       body_ << "  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n";
@@ -764,10 +735,11 @@ class Emitter {
     }
   }
 
-  void emit_powers() {
+  void emit_powers(const std::vector<char>* only = nullptr) {
     const std::size_t np = s_.powers.size();
     for (std::size_t i = 0; i < np; ++i) {
       const auto id = static_cast<std::uint32_t>(i);
+      if (only && !(*only)[i]) continue;
       for (std::uint32_t k = 0; k < P_; ++k) {
         if (d_ == Domain::Interval) {
           decls_ << "  .reg .f64 " << pw(id, k, false) << ", " << pw(id, k, true) << ";\n";
@@ -782,6 +754,7 @@ class Emitter {
     for (std::size_t i = 0; i < np; ++i) {
       const Power& p = s_.powers[i];
       const auto id = static_cast<std::uint32_t>(i);
+      if (only && !(*only)[i]) continue;
       for (std::uint32_t k = 0; k < P_; ++k) {
         if (p.exponent == 1) {
           if (d_ == Domain::Interval) {
@@ -829,14 +802,88 @@ class Emitter {
         }
       }
       // static sign: squares are positive, products of known signs known
-      if (p.exponent > 1 && static_signs_) {
+      if (p.exponent > 1) {
         psign_[i] = p.lo == p.hi ? 1 : psign_[p.lo] * psign_[p.hi];
       }
-      if (p.exponent == 1 && fast_ && gather_ && static_signs_) psign_[i] = 1;  // 0 < x (classifier)
+      if (p.exponent == 1 && fast_ && gather_) psign_[i] = 1;  // 0 < x (classifier)
     }
   }
 
   void emit_walk() {
+    declare_walk_regs();
+    emit_ops(0, s_.ops.size());
+  }
+
+  // Sectioned walk (scalar domains, long streams): the op sequence is cut at
+  // points where few walk values are live (emit_ptx); each section after the
+  // first starts with a CTA barrier, reloads the coordinates (L1/L2 hits)
+  // and rebuilds the powers it uses, so only the live walk values cross a
+  // section boundary in registers. All warps of the CTA run one section's
+  // code at a time (one instruction window per SM), and each section's
+  // register pressure is its own power table, not the whole program's. The
+  // arithmetic is the unsectioned op sequence, unchanged.
+  void emit_sectioned() {
+    emit_prologue();
+    declare_walk_regs();
+    std::size_t begin = 0;
+    for (std::size_t k = 0; k < cuts_.size(); ++k) {
+      const std::size_t end = cuts_[k];
+      sec_ = static_cast<std::uint32_t>(k);
+      if (k > 0) {
+        body_ << "  bar.sync 0;\n";
+        if (tuning_.carry_powers <= 0) emit_coord_reload();
+      }
+      if (k == 0 || tuning_.carry_powers <= 0) {
+        std::vector<char> need = k == 0 && tuning_.carry_powers > 0
+                                     ? std::vector<char>(s_.powers.size(), 1)
+                                     : powers_used(begin, end, k + 1 == cuts_.size());
+        emit_powers(&need);
+      }
+      emit_ops(begin, end);
+      begin = end;
+    }
+    emit_epilogue();
+    sec_ = 0;
+  }
+
+  // Powers read by ops [begin, end) (and by the result, for the last
+  // section), closed under the halving DAG.
+  std::vector<char> powers_used(std::size_t begin, std::size_t end, bool last) const {
+    std::vector<char> need(s_.powers.size(), 0);
+    auto mark = [&](const Operand& o) {
+      if (o.is(Operand::Pow)) need[o.id] = 1;
+    };
+    for (std::size_t i = begin; i < end; ++i) {
+      mark(s_.ops[i].a);
+      mark(s_.ops[i].b);
+      mark(s_.ops[i].c);
+    }
+    if (last) mark(s_.result);
+    for (std::size_t i = s_.powers.size(); i-- > 0;) {  // products follow their factors
+      if (need[i] && s_.powers[i].exponent > 1) need[s_.powers[i].lo] = need[s_.powers[i].hi] = 1;
+    }
+    return need;
+  }
+
+  // Section entry: fresh coordinate registers, loaded with plain (coherent)
+  // global loads after the barrier so ptxas cannot reuse the first load.
+  void emit_coord_reload() {
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      body_ << "  ld.param.u64 %rd5, [pe_in" << v << "];\n  cvta.to.global.u64 %rd5, %rd5;\n";
+      for (std::uint32_t k = 0; k < P_; ++k) {
+        if (d_ == Domain::I64F) {
+          decls_ << "  .reg .f64 " << xr(v, k) << ";\n  .reg .b64 " << xi(v, k) << ";\n";
+        } else {
+          decls_ << "  .reg ." << ldty() << " " << xr(v, k) << ";\n";
+        }
+        body_ << "  add.u64 %rd6, %rd5, %ix" << k << ";\n  ld.global." << ioty() << " "
+              << (int_io() ? xi(v, k) : xr(v, k)) << ", [%rd6];\n";
+        if (d_ == Domain::I64F) body_ << "  cvt.rn.f64.s64 " << xr(v, k) << ", " << xi(v, k) << ";\n";
+      }
+    }
+  }
+
+  void declare_walk_regs() {
     for (std::uint32_t id = 0; id < s_.nregs; ++id) {
       std::ostringstream line;
       line << "  .reg .f64 ";
@@ -854,9 +901,12 @@ class Emitter {
       line << ";\n";
       decls_ << line.str();
     }
+  }
+
+  void emit_ops(std::size_t begin, std::size_t end) {
     std::uint64_t since_sync = 0;
     std::size_t next_run = 0;
-    for (std::size_t i = 0; i < s_.ops.size(); ++i) {
+    for (std::size_t i = begin; i < end; ++i) {
       const Op& op = s_.ops[i];
       if (sync_every_ && ++since_sync == sync_every_) {
         body_ << "  bar.sync 0;\n";
@@ -884,12 +934,9 @@ class Emitter {
   // round trip per trip on a cold cache (small batches after an L2 flush:
   // the loop is a single dependent chain of up to L/8 such misses). The
   // loaded word feeds a never-true comparison (coefficient words are finite,
-  // the pattern is a NaN) so the load is not dead code. PE_WARM=0 disables.
+  // touch is a prefetchu.L1 of the line.
   void emit_chain_warmup() {
     if (runs_.empty() || fix_) return;
-    int warm_mode = 1;
-    if (const char* e = std::getenv("PE_WARM")) warm_mode = std::atoi(e);
-    if (warm_mode == 0) return;
     decls_ << "  .reg .b64 %wq<2>;\n  .reg .pred %wp<2>;\n  .reg .b32 %wl;\n";
     for (std::size_t idx = 0; idx < runs_.size(); ++idx) {
       const std::size_t words = runs_[idx].last - runs_[idx].head + loop_depth_ * kLoopU;
@@ -898,11 +945,9 @@ class Emitter {
       // for (line = tid; line < lines; line += ntid) touch(line)
       body_ << "  mov.u32 %wl, %r3;\n" << lbl << ":\n"
             << "  setp.ge.u32 %wp0, %wl, " << lines << ";\n  @%wp0 bra " << lbl << "e;\n"
-            << (warm_mode == 2 ? "  mov.u64 %wq0, pe_run" : "  cvta.const.u64 %wq0, pe_run") << idx
+            << "  cvta.const.u64 %wq0, pe_run" << idx
             << ";\n  mul.wide.u32 %wq1, %wl, 64;\n  add.u64 %wq0, %wq0, %wq1;\n"
-            << (warm_mode == 2 ? "  ld.const.b64 %wq1, [%wq0];\n  setp.eq.b64 %wp1, %wq1, "
-                                 "0x7FF8DEADBEEF0001;\n  @%wp1 trap;\n"
-                               : "  prefetchu.L1 [%wq0];\n")
+            << "  prefetchu.L1 [%wq0];\n"
             << "  add.u32 %wl, %wl, %r2;\n  bra " << lbl << ";\n"
             << lbl << "e:\n";
     }
@@ -910,7 +955,8 @@ class Emitter {
   void find_chain_runs() {
     const std::uint64_t budget =
         n_const_ < CoefTiers::kConstCap ? CoefTiers::kConstCap - n_const_ : 0;
-    runs_ = chain_runs(s_, d_, sync_every_, budget);
+    runs_ = cuts_.size() > 1 ? std::vector<ChainRun>{}
+                              : chain_runs(s_, d_, sync_every_, budget, tuning_.chain_min);
   }
 
   // Loop body: U steps; coefficients arrive as warp-uniform constant-bank
@@ -962,7 +1008,7 @@ class Emitter {
     const std::string lbl = "$Lrun" + std::to_string(idx);
     body_ << "  mov.u64 %lp, " << arr << ";\n";
     for (std::uint32_t d = 0; d < D; ++d) load8(set(d), 8 * U * d);
-    if (loop_rotate_) {
+    {
       // rotating register sets, no moves: the loop body is R = D + 1 trips;
       // trip j uses set j and loads set (j + D) % R for the trip D ahead
       const std::uint32_t R = D + 1;
@@ -981,20 +1027,6 @@ class Emitter {
         for (std::uint32_t u = 0; u < U; ++u) step(u, j);
       }
       for (std::uint32_t u = 0; u < rem; ++u) step(u, static_cast<std::uint32_t>(tail));
-    } else if (iters > 0) {
-      body_ << "  mov.u32 %lc, " << iters << ";\n" << lbl << ":\n";
-      load8(set(D), 8 * U * D);  // words D trips ahead (padding after the last)
-      for (std::uint32_t u = 0; u < U; ++u) step(u);
-      for (std::uint32_t d = 0; d < D; ++d) {
-        for (std::uint32_t u = 0; u < U; ++u) {
-          body_ << "  mov.b64 " << set(d) << u << ", " << set(d + 1) << u << ";\n";
-        }
-      }
-      body_ << "  add.u64 %lp, %lp, " << 8 * U << ";\n  sub.u32 %lc, %lc, 1;\n"
-            << "  setp.ne.u32 %lq, %lc, 0;\n  @%lq bra.uni " << lbl << ";\n";
-    }
-    if (!loop_rotate_) {
-      for (std::uint32_t u = 0; u < rem; ++u) step(u);  // words already in set 0
     }
     const std::uint32_t dst = s_.ops[run.last].dst;
     if (dst != acc) {
@@ -1328,56 +1360,27 @@ class Emitter {
   //    rule or a zero that the next step flags; NaN/inf always reach one of
   //    the two products ({A1,A2} and {B1,B2} are both endpoint pairs).
   void fnext(const std::string& dst, const std::string& src, bool up) {
-    if (fma_next_) {
-      // FP64-pipe nextafter: RN(v +- |v| * phi), phi = 2^-53 (1 + 2^-52).
-      // For a finite normal v the exact increment is strictly between 1/2
-      // and 3/2 of the spacing on its side, so RN lands on the neighbour
-      // (also across binades and into the subnormal range, and DBL_MAX up
-      // gives +inf). For 0 and subnormals it returns v unchanged — caught by
-      // the equality test, OR-accumulated into 4 rotating predicates so the
-      // checks do not form one serial chain; inf gives NaN, caught at the
-      // end.
-      const std::string a = tmp_f();
-      body_ << "  abs.f64 " << a << ", " << src << ";\n";
-      if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
-      if (dir_next_) {
-        // Directed variant: RD(v - |v| 2^-60) / RU(v + |v| 2^-60). The exact
-        // value lies strictly between v and its neighbour on that side for
-        // every finite nonzero v, subnormals included (|v| 2^-60 is below
-        // the spacing), so directed rounding lands on the neighbour; only
-        // +-0 does not move (flagged by the test below), and DBL_MAX up /
-        // -DBL_MAX down give +-inf as std::nextafter does.
-        body_ << "  fma." << (up ? "rp" : "rm") << ".f64 " << dst << ", " << a
-              << ", 0d3C30000000000000, " << src << ";\n";
-      } else {
-        body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
-      }
-      // "Did not move" test: either an FP64 compare, or (same answer) a
-      // 32-bit integer compare of the low words on the ALU pipe — a step of
-      // one ulp changes the bit pattern by +-1, so the low words differ iff
-      // the value moved. Mixing the two balances the FP64 and ALU pipes.
-      const bool int_check = iv_check_ == 1 || (iv_check_ == 2 && (nb_ & 1));
-      if (int_check) {
-        const std::string l0 = tmp_r(), h0 = tmp_r(), l1 = tmp_r(), h1 = tmp_r();
-        body_ << "  mov.b64 {" << l0 << ", " << h0 << "}, " << dst << ";\n"
-              << "  mov.b64 {" << l1 << ", " << h1 << "}, " << src << ";\n"
-              << "  setp.eq.or.b32 %pb" << (nb_ & 3) << ", " << l0 << ", " << l1 << ", %pb"
-              << (nb_ & 3) << ";\n";
-      } else {
-        body_ << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << dst << ", " << src << ", %pb"
-              << (nb_ & 3) << ";\n";
-      }
-      ++nb_;
-      return;
-    }
-    const std::string u = tmp_u(), s = tmp_u(), d = tmp_u(), r = tmp_u(), x = tmp_u();
-    body_ << "  mov.b64 " << u << ", " << src << ";\n"
-          << "  shr.s64 " << s << ", " << u << ", 63;\n"
-          << "  or.b64 " << d << ", " << s << ", 1;\n"
-          << (up ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", " << d << ";\n"
-          << "  xor.b64 " << x << ", " << r << ", " << u << ";\n"
-          << "  or.b64 %facc, %facc, " << x << ";\n"
-          << "  mov.b64 " << dst << ", " << r << ";\n";
+    // FP64-pipe nextafter: RN(v +- |v| * phi), phi = 2^-53 (1 + 2^-52).
+    // For a finite normal v the exact increment is strictly between 1/2 and
+    // 3/2 of the spacing on its side, so RN lands on the neighbour (also
+    // across binades and into the subnormal range, and DBL_MAX up gives +inf).
+    // For 0 and subnormals it returns v unchanged — caught by the "did not
+    // move" test, OR-accumulated into 4 rotating predicates so the checks do
+    // not form one serial chain; inf gives NaN, caught at the end. The test
+    // is a 32-bit compare of the low words on the ALU pipe (a step of one ulp
+    // changes the bit pattern by +-1, so the low words differ iff the value
+    // moved; C5 per 1e7: 1.56 ms vs 1.88 with an FP64 compare,
+    // profiles/r1_c5_check_modes.txt).
+    const std::string a = tmp_f();
+    body_ << "  abs.f64 " << a << ", " << src << ";\n";
+    if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
+    body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
+    const std::string l0 = tmp_r(), h0 = tmp_r(), l1 = tmp_r(), h1 = tmp_r();
+    body_ << "  mov.b64 {" << l0 << ", " << h0 << "}, " << dst << ";\n"
+          << "  mov.b64 {" << l1 << ", " << h1 << "}, " << src << ";\n"
+          << "  setp.eq.or.b32 %pb" << (nb_ & 3) << ", " << l0 << ", " << l1 << ", %pb"
+          << (nb_ & 3) << ";\n";
+    ++nb_;
   }
 
   // nextafter of a value whose sign is known statically (sign != 0): the
@@ -1389,29 +1392,26 @@ class Emitter {
   // final finiteness test sends such points to the strict replay. Unknown
   // sign: the FP64-pipe step with its "no move" test (fnext).
   void snext(const std::string& dst, const std::string& src, bool up, int sign) {
-    if (sign == 0 || !int_known_) {
+    if (sign == 0) {
       fnext(dst, src, up);
       return;
     }
-    const bool outward = up == (sign > 0);  // magnitude grows
-    // PE_IV_OUTFMA=N >= 2: every N-th outward step stays an integer add
-    // (FP64 / ALU balance)
-    const bool keep_int = out_fma_ >= 2 && (++n_out_ % out_fma_) == 0;
-    if (outward && out_fma_ && !keep_int) {
-      // Outward step on the FP64 pipe, no check: RU(v + v 2^-60) for v > 0
-      // (RD for v < 0) lies strictly between v and its outer neighbour for
-      // every finite nonzero v, subnormals included, so directed rounding
-      // lands on std::nextafter (DBL_MAX -> inf, caught by the final
-      // finiteness test). It does not move a zero — but the outer endpoint
-      // of a same-sign interval is zero only if the inner one is too, and
-      // the inner endpoint's integer step turns any zero into a NaN.
+    if (up == (sign > 0)) {
+      // Outward step (magnitude grows) on the FP64 pipe, no check: RU(v +
+      // v 2^-60) for v > 0 (RD for v < 0) lies strictly between v and its
+      // outer neighbour for every finite nonzero v, subnormals included, so
+      // directed rounding lands on std::nextafter (DBL_MAX -> inf, caught by
+      // the final finiteness test). It does not move a zero — but the outer
+      // endpoint of a same-sign interval is zero only if the inner one is
+      // too, and the inner endpoint's integer step turns any zero into a NaN.
       body_ << "  fma." << (sign > 0 ? "rp" : "rm") << ".f64 " << dst << ", " << src
             << ", 0d3C30000000000000, " << src << ";\n";
       return;
     }
+    // inward step: the bit pattern minus one (magnitude shrinks)
     const std::string u = tmp_u(), r = tmp_u();
     body_ << "  mov.b64 " << u << ", " << src << ";\n"
-          << (outward ? "  add.s64 " : "  sub.s64 ") << r << ", " << u << ", 1;\n"
+          << "  sub.s64 " << r << ", " << u << ", 1;\n"
           << "  mov.b64 " << dst << ", " << r << ";\n";
   }
 
@@ -1456,7 +1456,6 @@ class Emitter {
                 const std::pair<std::string, std::string>& a,
                 const std::pair<std::string, std::string>& b, bool check_a, bool check_b,
                 int sa = 0, int sb = 0) {
-    if (!fma_next_ || hybrid_next_) sa = sb = 0;  // integer steps need the runtime sign
     if (check_a && sa == 0) fcheck_straddle(a);
     if (check_b && sb == 0) fcheck_straddle(b);
     const std::string an = tmp_p(), bn = tmp_p(), ng = tmp_p();
@@ -1487,37 +1486,8 @@ class Emitter {
     const std::string lo = tmp_f(), hi = tmp_f();
     body_ << "  mul.rn.f64 " << lo << ", " << A1 << ", " << B1 << ";\n"
           << "  mul.rn.f64 " << hi << ", " << A2 << ", " << B2 << ";\n";
-    if (fma_next_ && !hybrid_next_) {
-      snext(dlo, lo, false, sa * sb);
-      snext(dhi, hi, true, sa * sb);
-      return;
-    }
-    if (fma_next_ && hybrid_next_) {
-      // pipe balance: the lower endpoint steps on the integer pipe (sign is
-      // known, so -/+1 on the bits; a sign flip marks +-0/NaN as special),
-      // the upper one on the FP64 pipe
-      const std::string d = tmp_u(), ul = tmp_u(), rl = tmp_u(), xl = tmp_u();
-      body_ << "  selp.b64 " << d << ", -1, 1, " << ng << ";\n"
-            << "  mov.b64 " << ul << ", " << lo << ";\n"
-            << "  sub.s64 " << rl << ", " << ul << ", " << d << ";\n"
-            << "  xor.b64 " << xl << ", " << rl << ", " << ul << ";\n"
-            << "  or.b64 %facc, %facc, " << xl << ";\n"
-            << "  mov.b64 " << dlo << ", " << rl << ";\n";
-      fnext(dhi, hi, true);
-      return;
-    }
-    // product sign is known: next_down(lo) = lo - d, next_up(hi) = hi + d,
-    // d = -1 for negative products, +1 for positive ones
-    const std::string d = tmp_u(), ul = tmp_u(), uh = tmp_u(), rl = tmp_u(), rh = tmp_u(),
-                      xl = tmp_u(), xh = tmp_u();
-    body_ << "  selp.b64 " << d << ", -1, 1, " << ng << ";\n"
-          << "  mov.b64 " << ul << ", " << lo << ";\n  mov.b64 " << uh << ", " << hi << ";\n"
-          << "  sub.s64 " << rl << ", " << ul << ", " << d << ";\n"
-          << "  add.s64 " << rh << ", " << uh << ", " << d << ";\n"
-          << "  xor.b64 " << xl << ", " << rl << ", " << ul << ";\n"
-          << "  xor.b64 " << xh << ", " << rh << ", " << uh << ";\n"
-          << "  or.b64 %facc, %facc, " << xl << ";\n  or.b64 %facc, %facc, " << xh << ";\n"
-          << "  mov.b64 " << dlo << ", " << rl << ";\n  mov.b64 " << dhi << ", " << rh << ";\n";
+    snext(dlo, lo, false, sa * sb);
+    snext(dhi, hi, true, sa * sb);
   }
 
   // Static sign of an operand in the fast path: +1 / -1 when every
@@ -1576,7 +1546,7 @@ class Emitter {
       } else if (sa == sb) {
         r = sa;
       }
-      rsign_[op.dst] = static_signs_ ? r : 0;
+      rsign_[op.dst] = r;
     }
   }
 
@@ -1586,12 +1556,6 @@ class Emitter {
     for (std::uint32_t k = 0; k < P_; ++k) {
       fcheck_finite(reg(s_.result.id, k, false));
       fcheck_finite(reg(s_.result.id, k, true));
-    }
-    const char* dbg = std::getenv("PE_IV_DEBUG");
-    if (dbg && std::atoi(dbg) == 1) {
-      // diagnostics: out_hi receives the accumulator bits, no slow path
-      body_ << "  ld.param.u64 %rd9, [pe_out1];\n  cvta.to.global.u64 %rd9, %rd9;\n"
-            << "  add.u64 %rd10, %rd9, %ix0;\n  st.global.b64 [%rd10], %facc;\n  bra $Ldone;\n";
     }
     // special: append the thread's valid point indices to the fixup list
     body_ << "  setp.lt.s64 %pslow, %facc, 0;\n"
@@ -1685,14 +1649,7 @@ class Emitter {
           body_ << "  cvt.rni.s64.f64 " << t << ", " << val << ";\n";
           val = t;
         }
-        if (accumulate_) {
-          const std::string old = tmp_f(), sum = tmp_f();
-          body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n  ld.global.f64 " << old
-                << ", [%rd10];\n  add.rn.f64 " << sum << ", " << old << ", " << val << ";\n";
-          val = sum;
-        } else {
-          body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n";
-        }
+        body_ << "  add.u64 %rd10, %rd9, %ix" << k << ";\n";
         body_ << "  @%pv" << k << " st.global." << ioty() << " [%rd10], " << val << ";\n";
       }
     }
@@ -1703,85 +1660,32 @@ class Emitter {
   std::uint32_t P_;
   std::uint32_t block_;
   std::uint32_t sync_every_;
-  std::uint32_t imm_mode_;
+  bool paired_;  // scalar domains: paired coefficient loads, register-bound second region
   std::uint32_t min_ctas_ = 0;
-  bool accumulate_ = false;
   std::uint32_t K_ = 1;  // I64K limbs
+  std::uint32_t part_ = 0;    // KernelShape::iv_partition
+  Tuning tuning_;
+  std::vector<std::size_t> cuts_;  // section boundaries (op indices), ascending, ends with ops.size()
+  std::uint32_t sec_ = 0;          // section being emitted
   bool fast_ = false;  // emitting the interval fast path
   bool medium_ = false;  // emitting the finite-case replay of the fixup entry
-  std::uint32_t part_ = 0;    // KernelShape::iv_partition
   std::uint32_t gather_ = 0;  // emitting a partitioned entry: 1 front (x > 0), 2 back (x < 0)
-  bool mid_replay_ = [] {  // PE_IV_MID=0: fixup entry = bit-level replay only
-    const char* e = std::getenv("PE_IV_MID");
-    return !(e && std::atoi(e) == 0);
-  }();
   bool fix_ = false;   // emitting the fixup entry
-  // fast-path nextafter on the FP64 pipe (default) or as integer +-1 with
-  // sign-flip detection (PE_IV_NEXT=int)
-  bool fma_next_ = [] {
-    const char* e = std::getenv("PE_IV_NEXT");
-    return !(e && std::string(e) == "int");
-  }();
-  // PE_IV_NEXT=hybrid: product lower endpoints step on the integer pipe,
-  // upper ones on FP64 — measured slower than all-FP64 on C5 (2.66 vs
-  // 2.42 ms per 1e7, profiles/r1_c5_next_modes.txt), so opt-in only
-  bool hybrid_next_ = [] {
-    const char* e = std::getenv("PE_IV_NEXT");
-    return e && std::string(e) == "hybrid";
-  }();
-  // PE_IV_NEXT=dir: the FP64-pipe step with directed rounding (exact for
-  // subnormals too, so fewer points need the strict replay)
-  bool dir_next_ = [] {
-    const char* e = std::getenv("PE_IV_NEXT");
-    return e && std::string(e) == "dir";
-  }();
   std::uint32_t nb_ = 0;
-  std::uint32_t out_fma_ = [] {  // PE_IV_OUTFMA=0: outward known-sign steps as integer +1 too
-    const char* e = std::getenv("PE_IV_OUTFMA");
-    return e ? static_cast<std::uint32_t>(std::atoi(e)) : 1u;
-  }();
-  std::uint32_t n_out_ = 0;
   std::vector<int> rsign_, psign_;  // fast path: static signs of registers / powers
-  bool static_signs_ = [] {         // PE_IV_SIGNS=0 disables (A/B measurement)
-    const char* e = std::getenv("PE_IV_SIGNS");
-    return !(e && std::atoi(e) == 0);
-  }();
-  bool int_known_ = [] {            // integer nextafter for known signs (PE_IV_INTSTEP=0 off)
-    const char* e = std::getenv("PE_IV_INTSTEP");
-    return !(e && std::atoi(e) == 0);
-  }();
-  // fast-path "no move" test: 0 FP64 compare, 1 integer low-word compare
-  // (default), 2 alternate (PE_IV_CHECK=fp|int|mix). With static signs, C5
-  // per 1e7 intervals: fp 1.88 ms, mix 1.69, int 1.56
-  // (profiles/r1_c5_check_modes.txt)
-  int iv_check_ = [] {
-    const char* e = std::getenv("PE_IV_CHECK");
-    if (e && std::string(e) == "mix") return 2;
-    if (e && std::string(e) == "fp") return 0;
-    return 1;
-  }();
   static constexpr std::uint32_t kLoopU = 8;  // loop unroll (steps per trip)
   // Chain-loop coefficient prefetch: D trips ahead into rotating register
   // sets (loop body = D + 1 trips, no moves). The 1e5-point C1 kernel had 47 %
-  // of its stall samples on the move of the one-trip-ahead set (waiting on
-  // its LDCU); D = 2 rotating: C1 1e5 20.2 -> 18.6 us per call, 1e7 0.594 ->
-  // 0.577 ms (profiles/r1_c1_small_batch.txt). PE_LOOP_ROT=0 / PE_LOOP_DEPTH
-  // select the move-based variant / the distance.
-  bool loop_rotate_ = [] {
-    const char* e = std::getenv("PE_LOOP_ROT");
-    return !(e && std::atoi(e) == 0);
-  }();
-  std::uint32_t loop_depth_ = [] {
-    const char* e = std::getenv("PE_LOOP_DEPTH");
-    const int v = e ? std::atoi(e) : 2;
-    return static_cast<std::uint32_t>(v < 1 ? 1 : v > 3 ? 3 : v);
-  }();
+  // of its stall samples on the move of a one-trip-ahead set (waiting on its
+  // LDCU); D = 2 rotating: C1 1e5 20.2 -> 18.6 us per call, 1e7 0.594 ->
+  // 0.577 ms (profiles/r1_c1_small_batch.txt).
+  static constexpr std::uint32_t loop_depth_ = 2;
   std::vector<ChainRun> runs_;
   std::string run_arrays_;
   bool loop_decls_ = false;
   std::vector<std::uint64_t> words_;
-  std::unordered_map<std::uint32_t, std::string> pending_;  // imm_mode 4/5: second word of a pair
-  std::vector<char> reg_bound_;  // imm_mode 5: coefficient emitted as an immediate
+  std::unordered_map<std::uint32_t, std::string> pending_;  // second word of a loaded pair
+  std::vector<char> reg_bound_;  // coefficient in the register-bound region
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
   std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0, n_tr_ = 0;
@@ -1799,7 +1703,8 @@ namespace {
 // constant loads stay adjacent. The ops are SSA (one definition per
 // register), so any topological order computes the same values.
 template <typename C>
-Stream<C> schedule_stream(const Stream<C>& in, std::size_t W, std::size_t D) {
+Stream<C> schedule_stream(const Stream<C>& in, std::size_t W, std::size_t D,
+                          const std::vector<std::size_t>& cuts) {
   const std::size_t n = in.ops.size();
   std::unordered_map<std::uint32_t, std::size_t> def;
   for (std::size_t i = 0; i < n; ++i) def[in.ops[i].dst] = i;
@@ -1815,11 +1720,14 @@ Stream<C> schedule_stream(const Stream<C>& in, std::size_t W, std::size_t D) {
   std::vector<std::size_t> pos(n, SIZE_MAX), order;
   order.reserve(n);
   std::size_t first = 0;  // lowest unscheduled original index
+  std::size_t sec = 0;    // ops never move across a section boundary
   while (order.size() < n) {
     while (first < n && pos[first] != SIZE_MAX) ++first;
+    while (sec < cuts.size() && cuts[sec] <= first) ++sec;
+    const std::size_t limit = sec < cuts.size() ? cuts[sec] : n;
     std::size_t pick = SIZE_MAX, fallback = SIZE_MAX;
     const std::size_t now = order.size();
-    for (std::size_t i = first; i < n && i < first + W; ++i) {
+    for (std::size_t i = first; i < limit && i < first + W; ++i) {
       if (pos[i] != SIZE_MAX) continue;
       bool ready = true, aged = true;
       for (std::size_t p : preds[i]) {
@@ -1868,29 +1776,90 @@ Stream<C> schedule_stream(const Stream<C>& in, std::size_t W, std::size_t D) {
   }
   return out;
 }
+
+// Section boundaries of a long scalar walk: about `target` ops per section,
+// each cut placed where the fewest walk values are live (they cross the
+// boundary in registers), within a quarter section of its even position.
+// Returns the ascending section ends (the last is ops.size()).
+template <typename C>
+std::vector<std::size_t> section_cuts(const Stream<C>& s, std::size_t target) {
+  const std::size_t n = s.ops.size();
+  if (target == 0 || n < target + target / 2) return {n};
+  const std::size_t K = (n + target / 2) / target;
+  // live[b]: values defined before op b and read at or after it
+  std::unordered_map<std::uint32_t, std::size_t> def;
+  std::vector<std::int64_t> diff(n + 2, 0);
+  std::unordered_map<std::uint32_t, std::size_t> last_use;
+  auto use = [&](const Operand& o, std::size_t at) {
+    if (o.is(Operand::Reg)) last_use[o.id] = at;
+  };
+  for (std::size_t i = 0; i < n; ++i) {
+    use(s.ops[i].a, i);
+    use(s.ops[i].b, i);
+    use(s.ops[i].c, i);
+    def[s.ops[i].dst] = i;
+  }
+  use(s.result, n);
+  for (const auto& [reg, d] : def) {
+    auto it = last_use.find(reg);
+    if (it == last_use.end() || it->second <= d) continue;
+    diff[d + 1] += 1;
+    diff[it->second + 1] -= 1;
+  }
+  std::vector<std::int64_t> live(n + 1, 0);
+  std::int64_t run = 0;
+  for (std::size_t b = 0; b <= n; ++b) {
+    run += diff[b];
+    live[b] = run;
+  }
+  std::vector<std::size_t> cuts;
+  const std::size_t slack = std::max<std::size_t>(1, n / (4 * K));
+  for (std::size_t k = 1; k < K; ++k) {
+    const std::size_t t = k * n / K;
+    std::size_t best = t;
+    for (std::size_t b = t > slack ? t - slack : 1; b <= std::min(n - 1, t + slack); ++b) {
+      const auto dist = [&](std::size_t x) { return x > t ? x - t : t - x; };
+      if (live[b] < live[best] || (live[b] == live[best] && dist(b) < dist(best))) best = b;
+    }
+    if (cuts.empty() || best > cuts.back()) cuts.push_back(best);
+  }
+  cuts.push_back(n);
+  return cuts;
+}
 }  // namespace
 
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shape) {
+KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shape,
+                     const Tuning& tuning) {
+  const bool scalar = domain == Domain::F64 || domain == Domain::F64Strict ||
+                      domain == Domain::I64 || domain == Domain::I64F;
+  // Long scalar walks are emitted in sections (Emitter::emit_sectioned);
+  // ~3k ops per section (profiles/r1_slices_c4.txt: C4 at 4-6 parts of
+  // 2-3k records beat the 12.6k-record walk by 22 %).
+  const std::size_t target = tuning.section_ops == UINT32_MAX ? 0
+                             : tuning.section_ops        ? tuning.section_ops
+                                                         : 3000;
+  const std::vector<std::size_t> cuts =
+      scalar ? section_cuts(stream_in, target) : std::vector<std::size_t>{stream_in.ops.size()};
   // Wide fused programs (power tables > 32 entries, one point per thread:
-  // C4's trivariate slices) get the latency-aware reordering: their warps
-  // are few (128 registers, most holding powers) and ptxas keeps the walk's
+  // C4's trivariate walk) get the latency-aware reordering: their warps are
+  // few (128 registers, most holding powers) and ptxas keeps the walk's
   // order, so 68 % of FP64 ops sat within 4 instructions of their producer
   // (profiles/r1_sched_sweep.txt: C4 3.71 -> 3.50 ms per 4e6 points; the
   // 4-lane C2/C3 kernels have ILP from their lanes and gain nothing).
-  // PE_SCHED="W,D" overrides ("0,0" disables).
   Stream<C> scheduled;
   const Stream<C>* sp = &stream_in;
   if (!stream_in.strict && (domain == Domain::F64 || domain == Domain::I64F)) {
     std::size_t W = 0, D = 0;
-    if (const char* e = std::getenv("PE_SCHED")) {
-      if (std::sscanf(e, "%zu,%zu", &W, &D) != 2) W = D = 0;
+    if (tuning.sched_window) {
+      W = tuning.sched_window;
+      D = tuning.sched_distance;
     } else if (stream_in.powers.size() > 32 && (shape.lanes == 0 || shape.lanes == 1)) {
       W = 64;
       D = 8;
     }
     if (W > 1) {
-      scheduled = schedule_stream(stream_in, W, D);
+      scheduled = schedule_stream(stream_in, W, D, cuts);
       sp = &scheduled;
     }
   }
@@ -1901,20 +1870,20 @@ KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shap
     std::memcpy(&w, &c, 8);
     distinct.emplace(w, 0);
   }
-  const KernelShape def = default_shape(domain, stream.ops.size(),
-                                        static_cast<std::uint32_t>(stream.powers.size()),
-                                        distinct.size());
+  const KernelShape def = default_shape(domain, static_cast<std::uint32_t>(stream.powers.size()),
+                                        distinct.size(), tuning);
   if (shape.lanes == 0) shape.lanes = def.lanes;
   if (shape.block == 0) shape.block = def.block;
   if (shape.sync_every == 0) shape.sync_every = def.sync_every;
-  if (shape.imm_mode == 0) shape.imm_mode = def.imm_mode;
   if (shape.min_ctas == 0) shape.min_ctas = def.min_ctas;
   if (shape.limbs == 0) shape.limbs = 1;
-  Emitter<C> e(stream, domain, shape);
-  return e.run();
+  Emitter<C> e(stream, domain, shape, tuning, cuts);
+  KernelImage img = e.run();
+  img.iv_partition_min = tuning.iv_partition_min ? tuning.iv_partition_min : 65536;
+  return img;
 }
 
-template KernelImage emit_ptx(const Stream<double>&, Domain, KernelShape);
-template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, KernelShape);
+template KernelImage emit_ptx(const Stream<double>&, Domain, KernelShape, const Tuning&);
+template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, KernelShape, const Tuning&);
 
 }  // namespace polyeval::lower

@@ -54,6 +54,7 @@ struct KernelImage {
   bool interval_fast_path = false; // fast exact path + fixup entry (strict replay)
   std::uint32_t limbs = 1;         // I64K: 64-bit words per value (= result arrays)
   std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
+  std::uint32_t sections = 1;      // barrier-separated sections of the walk
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
   // sign-partitioned interval fast path (univariate): 1 = this module also
   // has `part_entry` (points with x > 0, taken from the front of a device
@@ -62,12 +63,32 @@ struct KernelImage {
   // evaluates q at -x. Both entries take two extra parameters (list, counts).
   std::uint32_t iv_partition = 0;
   std::string part_entry;
+  std::uint64_t iv_partition_min = 65536;  // smaller batches skip the partition
   std::uint32_t fix_block = 128;   // fixup kernel CTA size (.maxntid)
   std::uint32_t fix_ctas_per_sm = 4;  // fixup grid: CTAs per SM (.minnctapersm)
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
   std::uint64_t int_ops = 0;       // int64 add/mul/mad per point
   std::uint64_t hash = 0;          // FNV-1a of `ptx`
+};
+
+/// Code-generation options of one program (the C ABI's pe_tuning). Every
+/// field's 0 means "the measured default"; a program's kernels are generated
+/// from the options it holds when the kernel is first needed.
+struct Tuning {
+  std::uint32_t lanes = 0;        // points per thread (1..8)
+  std::uint32_t block = 0;        // threads per CTA (32..1024)
+  std::uint32_t min_ctas = 0;     // .minnctapersm of the walk entry
+  std::uint32_t sync_every = 0;   // walk ops between CTA barriers
+  std::uint32_t section_ops = 0;  // ops per section of a long scalar walk; UINT32_MAX = one section
+  std::uint32_t sched_window = 0; // list-scheduling window (1 = keep the walk order)
+  std::uint32_t sched_distance = 0;
+  std::uint32_t chain_min = 0;    // shortest Hörner run emitted as a loop; UINT32_MAX = never
+  std::int32_t iv_fast = 0;       // interval fast path + fixup list (-1 = bit-level replay only)
+  std::int32_t iv_mid = 0;        // fixup: finite-case replay first (-1 = bit-level only)
+  std::int32_t iv_partition = 0;  // univariate sign partition (-1 = off)
+  std::int32_t carry_powers = 0;  // sections: 1 = keep power tables live across sections
+  std::uint64_t iv_partition_min = 0;  // smallest partitioned batch (default 65536)
 };
 
 /// Launch shape of a specialised kernel.
@@ -82,12 +103,6 @@ struct KernelShape {
   std::uint32_t lanes = 0;
   std::uint32_t block = 0;
   std::uint32_t sync_every = 0;
-  // coefficient delivery: 0 constant bank (LDC/LDCU), 1 immediates (MOV
-  // pairs), 2 alternate words, 3 immediates beyond the constant-bank tier
-  std::uint32_t imm_mode = 0;
-  // fp64 slices of a wide program: add the slice value into the result
-  // instead of storing it (out[i] += v)
-  bool accumulate = false;
   // I64K: 64-bit limbs per value (1..8)
   std::uint32_t limbs = 0;
   // .minnctapersm of the walk entry (0 = none): caps ptxas at
@@ -97,12 +112,12 @@ struct KernelShape {
   std::uint32_t iv_partition = 0;
 };
 
-/// Defaults per domain and program size; PE_LANES / PE_BLOCK / PE_SYNC
-/// environment variables override (tuning only).
-KernelShape default_shape(Domain d, std::uint64_t ops, std::uint32_t powers,
-                          std::uint64_t distinct_coefs);
+/// Measured defaults per domain and program size, then the tuning overrides.
+KernelShape default_shape(Domain d, std::uint32_t powers, std::uint64_t distinct_coefs,
+                          const Tuning& t);
 
 template <typename C>
-KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape = {});
+KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape = {},
+                     const Tuning& tuning = {});
 
 }  // namespace polyeval::lower

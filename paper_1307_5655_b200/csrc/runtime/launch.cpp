@@ -5,6 +5,10 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -155,11 +159,6 @@ void keep_pool_memory(int device) {
   }
 }
 
-bool partition_min_batch(std::uint64_t n) {
-  // below ~64K intervals the extra launches outweigh the cheaper walk
-  const char* e = std::getenv("PE_IV_PART_MIN");
-  return n >= (e ? static_cast<std::uint64_t>(std::atoll(e)) : std::uint64_t{1} << 16);
-}
 }  // namespace
 
 void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
@@ -169,7 +168,8 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(la.count), 0, sizeof(unsigned), stream),
                "cudaMemsetAsync(fixup count)");
   }
-  const bool part = a.partitioned() && la.n <= 0xffffffffull && partition_min_batch(la.n);
+  // below ~64K intervals the extra launches outweigh the cheaper walk
+  const bool part = a.partitioned() && la.n <= 0xffffffffull && la.n >= img.iv_partition_min;
   void* scratch = nullptr;  // partition: n u32 point indices + 2 u32 list lengths
   if (part) {
     keep_pool_memory(device);
@@ -231,28 +231,20 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     // one thread per list slot (the kernel has no grid-stride loop); threads
     // past the device-side count exit at once
     const std::uint64_t fb = img.fix_block;
+    // (a caller-bound list can be larger than this call's batch)
     const unsigned fix_grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(0x7fffffffull, (la.cap + fb - 1) / fb));
-    cudaStream_t fs = stream;
-    if (la.fix_stream) {
-      // hand the list over to the side stream: the latency-bound replay then
-      // runs beside the next chunk's fast path instead of after it
-      cudaEvent_t ev;
-      check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-      check_cuda(cudaEventRecord(ev, stream), "cudaEventRecord");
-      check_cuda(cudaStreamWaitEvent(la.fix_stream, ev, 0), "cudaStreamWaitEvent");
-      cudaEventDestroy(ev);
-      fs = la.fix_stream;
-    }
+        std::min<std::uint64_t>(0x7fffffffull, (std::min(la.cap, la.n) + fb - 1) / fb));
     launch_one(a.fix_kernel, dev_ok ? a.fix_fn[device] : nullptr,
-               dim3(fix_grid ? fix_grid : 1), dim3(static_cast<unsigned>(fb)), args.data(), fs, "launch(fixup)");
+               dim3(fix_grid ? fix_grid : 1), dim3(static_cast<unsigned>(fb)), args.data(), stream,
+               "launch(fixup)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   }
   if (scratch) check_cuda(cudaFreeAsync(scratch, stream), "cudaFreeAsync(partition)");
 }
 
 
-MemKind classify(const void* p, int* device) {
+MemKind classify(const void* p, int* device, bool* pinned) {
+  if (pinned) *pinned = false;
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
     cudaGetLastError();
@@ -262,10 +254,9 @@ MemKind classify(const void* p, int* device) {
     if (device) *device = attr.device;
     return MemKind::Device;
   }
+  if (pinned) *pinned = attr.type == cudaMemoryTypeHost;
   return MemKind::Host;
 }
-
-
 
 DeviceCtx& device_ctx(int device) {
   static std::mutex g;
@@ -274,11 +265,9 @@ DeviceCtx& device_ctx(int device) {
   auto& c = ctxs[device];
   if (!c) {
     c = std::make_unique<DeviceCtx>();
-    if (const char* e = std::getenv("PE_STAGE_SLOTS")) {
-      c->slots = std::clamp(std::atoi(e), 2, DeviceCtx::kMaxSlots);
-    }
-    for (int i = 0; i < c->slots; ++i) {
+    for (int i = 0; i < DeviceCtx::kMaxSlots; ++i) {
       check_cuda(cudaStreamCreateWithFlags(&c->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      check_cuda(cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming), "cudaEventCreate");
     }
     check_cuda(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device),
                "cudaDeviceGetAttribute");
@@ -286,22 +275,112 @@ DeviceCtx& device_ctx(int device) {
   return *c;
 }
 
-static void ensure_buffers(DeviceCtx& c, size_t arrays, size_t bytes) {
-  if (c.cap >= bytes && c.buffers[0].size() >= arrays) return;
-  for (auto& slot : c.buffers) {
-    for (void* p : slot) cudaFree(p);
+Staging staging_of(const pe_exec* ex) {
+  Staging s;
+  if (ex) {
+    s.chunk = static_cast<std::size_t>(ex->stage_chunk);
+    s.slots = ex->stage_slots;
+  }
+  return s;
+}
+
+namespace {
+void ensure_buffers(DeviceCtx& c, int slots, size_t arrays, size_t bytes, bool pinned) {
+  const bool dev_ok = c.cap >= bytes && c.buffers[slots - 1].size() >= arrays;
+  if (!dev_ok) {
+    for (auto& slot : c.buffers) {
+      for (void* p : slot) cudaFree(p);
+      slot.clear();
+    }
+    c.cap = std::max(bytes, c.cap);
+    for (int k = 0; k < DeviceCtx::kMaxSlots && k < slots; ++k) {
+      for (size_t i = 0; i < arrays; ++i) {
+        void* p = nullptr;
+        check_cuda(cudaMalloc(&p, c.cap), "cudaMalloc(staging)");
+        c.buffers[k].push_back(p);
+      }
+    }
+  }
+  if (!pinned) return;
+  if (c.pinned_cap >= bytes && c.pinned[slots - 1].size() >= arrays) return;
+  for (auto& slot : c.pinned) {
+    for (void* p : slot) cudaFreeHost(p);
     slot.clear();
   }
-  c.cap = std::max(bytes, c.cap);
-  for (int k = 0; k < c.slots; ++k) {
-    auto& slot = c.buffers[k];
+  c.pinned_cap = std::max(bytes, c.pinned_cap);
+  for (int k = 0; k < slots; ++k) {
     for (size_t i = 0; i < arrays; ++i) {
       void* p = nullptr;
-      check_cuda(cudaMalloc(&p, c.cap), "cudaMalloc(staging)");
-      slot.push_back(p);
+      check_cuda(cudaHostAlloc(&p, c.pinned_cap, cudaHostAllocPortable), "cudaHostAlloc(staging)");
+      c.pinned[k].push_back(p);
     }
   }
 }
+
+// Host memcpy of large pageable buffers into / out of page-locked staging:
+// split over a few persistent worker threads (one thread's memcpy, ~10 GB/s,
+// would be slower than PCIe).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    const size_t parts = std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, bytes >> 20));
+    if (parts <= 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    const size_t per = (bytes + parts - 1) / parts;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      for (size_t k = 1; k < parts; ++k) {
+        const size_t lo = k * per, len = std::min(bytes, lo + per) - lo;
+        jobs_.push_back({static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len});
+      }
+      pending_ += parts - 1;
+    }
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(per, bytes));
+    std::unique_lock<std::mutex> lock(mu_);
+    idle_.wait(lock, [&] { return pending_ == 0; });
+  }
+
+ private:
+  struct Job {
+    char* dst;
+    const char* src;
+    size_t len;
+  };
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    for (unsigned i = 0; i < std::min(7u, hw - 1); ++i) {
+      workers_.emplace_back([this] { run(); });
+      workers_.back().detach();
+    }
+  }
+  void run() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [&] { return !jobs_.empty(); });
+        j = jobs_.front();
+        jobs_.pop_front();
+      }
+      std::memcpy(j.dst, j.src, j.len);
+      std::lock_guard<std::mutex> lock(mu_);
+      if (--pending_ == 0) idle_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, idle_;
+  std::deque<Job> jobs_;
+  size_t pending_ = 0;
+  std::vector<std::thread> workers_;
+};
+}  // namespace
 
 int resolve_device(const pe_exec* ex, const void* probe, MemKind* kind) {
   int ptr_dev = -1;
@@ -359,14 +438,34 @@ struct FixupLists {
 
 }  // namespace
 
-// `arts` run in order on each chunk (wide fp64 programs: slice 0 stores,
-// later slices accumulate); inputs are staged once per chunk for all of them.
+// `arts` run in order on each chunk; inputs are staged once per chunk for
+// all of them (pe_eval_f64_multi).
 void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
-               bool full_fixup, const std::vector<size_t>& out_base) {
+               bool full_fixup, const std::vector<size_t>& out_base, const Staging& staging) {
   const size_t elem = 8;
   const Artifact& a = *arts.front();  // interval programs have exactly one
+  // every buffer must live where the output does (a host pointer handed to a
+  // kernel, or a device pointer to a host memcpy, would be read blindly)
+  bool all_pinned = true;
+  {
+    std::vector<const void*> all(ins.begin(), ins.end());
+    all.insert(all.end(), outs.begin(), outs.end());
+    for (const void* p : all) {
+      int d = -1;
+      bool pinned = false;
+      const MemKind k = classify(p, &d, &pinned);
+      if (k != kind) {
+        throw std::invalid_argument(
+            "coordinate and result buffers must all be device memory or all host memory");
+      }
+      if (k == MemKind::Device && d >= 0 && d != device) {
+        throw std::invalid_argument("buffers live on different devices");
+      }
+      all_pinned = all_pinned && pinned;
+    }
+  }
   // art i writes outs[out_base[i] .. out_base[i] + n_out) (default: from 0)
   auto launch_all = [&](const LaunchArgs& la, cudaStream_t st) {
     for (size_t i = 0; i < arts.size(); ++i) {
@@ -378,72 +477,66 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     }
   };
   if (kind == MemKind::Device) {
-    size_t max_chunk = size_t{1} << 30;
+    const size_t max_chunk = size_t{1} << 30;
     // a caller-bound list (deferred checks) is reused; otherwise per call
     const bool own_list = proto.list == 0;
-    // deferred interval calls with a side stream: chunks of >= 1M points, each
-    // with its own list region and counter; chunk k's fixup kernel overlaps
-    // chunk k+1's fast path
-    const bool overlap = !own_list && proto.fix_stream && a.image.interval_fast_path;
-    if (overlap) {
-      const size_t k = std::clamp<size_t>(n >> 20, 1, StreamState::kMaxChunks);
-      max_chunk = (n + k - 1) / k;
-    }
     FixupLists fix(a, own_list ? std::min(n, max_chunk) : 0, full_fixup, {user_stream});
-    size_t idx = 0;
-    for (size_t off = 0; off < n; off += max_chunk, ++idx) {
+    for (size_t off = 0; off < n; off += max_chunk) {
       LaunchArgs la = proto;
       if (own_list) fix.bind(la, 0);
       la.n = std::min(max_chunk, n - off);
-      if (overlap) {
-        la.list = proto.list + 4 * off;
-        la.count = proto.count + 4 * idx;
-        la.cap = la.n;
-      } else {
-        la.fix_stream = nullptr;
-      }
       la.ins.clear();
       la.outs.clear();
       for (auto p : ins) la.ins.push_back(reinterpret_cast<std::uint64_t>(static_cast<const char*>(p) + off * elem));
       for (auto p : outs) la.outs.push_back(reinterpret_cast<std::uint64_t>(static_cast<char*>(p) + off * elem));
       launch_all(la, user_stream);
     }
-    if (overlap) {  // the caller's stream resumes after the last replay
-      cudaEvent_t ev;
-      check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-      check_cuda(cudaEventRecord(ev, proto.fix_stream), "cudaEventRecord");
-      check_cuda(cudaStreamWaitEvent(user_stream, ev, 0), "cudaStreamWaitEvent");
-      cudaEventDestroy(ev);
-    }
     if (sync) check_cuda(cudaStreamSynchronize(user_stream), "cudaStreamSynchronize");
     return;
   }
+  // Host buffers: chunk k runs on slot k % S — H2D, the walk kernels and D2H
+  // on the slot's stream, so the copy engines overlap the neighbouring
+  // chunks' walks. Pageable buffers additionally pass through page-locked
+  // staging arrays: before chunk k is enqueued, the host waits for chunk
+  // k - S (same slot), copies its results out and chunk k's inputs in, while
+  // the GPU works on chunks k - S + 1 .. k - 1.
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
+  const int S = staging.slots >= 2 && staging.slots <= DeviceCtx::kMaxSlots ? staging.slots : 3;
   // 16+ chunks keep the un-overlapped first H2D / last D2H short; >= 256K
   // points keep each walk launch large enough to fill the GPU
-  size_t chunk = std::clamp<size_t>(n / 16, size_t{1} << 18, size_t{1} << 22);
-  if (const char* e = std::getenv("PE_STAGE_CHUNK")) {
-    const long v = std::atol(e);
-    if (v >= 4096) chunk = static_cast<size_t>(v);
-  }
-  ensure_buffers(c, ins.size() + outs.size(), chunk * elem);
+  size_t chunk = staging.chunk >= 4096 ? staging.chunk
+                                       : std::clamp<size_t>(n / 16, size_t{1} << 18, size_t{1} << 22);
+  chunk = std::min(chunk, std::max<size_t>(n, 1));
+  const bool stage = !all_pinned;
+  ensure_buffers(c, S, ins.size() + outs.size(), chunk * elem, stage);
   cudaEvent_t flag_ready = nullptr;
   if (proto.flag) {
     // the flag was initialised on user_stream: order the slots after it
     check_cuda(cudaEventCreateWithFlags(&flag_ready, cudaEventDisableTiming), "cudaEventCreate");
     check_cuda(cudaEventRecord(flag_ready, user_stream), "cudaEventRecord");
-    for (int i = 0; i < c.slots; ++i) {
+    for (int i = 0; i < S; ++i) {
       check_cuda(cudaStreamWaitEvent(c.streams[i], flag_ready, 0), "cudaStreamWaitEvent");
     }
   }
-  FixupLists fix(a, chunk, full_fixup,
-                 std::vector<cudaStream_t>(c.streams, c.streams + c.slots));
+  FixupLists fix(a, chunk, full_fixup, std::vector<cudaStream_t>(c.streams, c.streams + S));
+  std::vector<size_t> slot_off(static_cast<size_t>(S), SIZE_MAX), slot_len(static_cast<size_t>(S), 0);
+  auto drain = [&](int slot) {  // pageable: results of the slot's last chunk to the caller
+    if (!stage || slot_off[static_cast<size_t>(slot)] == SIZE_MAX) return;
+    check_cuda(cudaEventSynchronize(c.done[slot]), "cudaEventSynchronize");
+    const size_t off = slot_off[static_cast<size_t>(slot)], m = slot_len[static_cast<size_t>(slot)];
+    for (size_t o = 0; o < outs.size(); ++o) {
+      CopyPool::get().copy(static_cast<char*>(outs[o]) + off * elem, c.pinned[slot][ins.size() + o],
+                           m * elem);
+    }
+    slot_off[static_cast<size_t>(slot)] = SIZE_MAX;
+  };
   size_t k = 0;
   for (size_t off = 0; off < n; off += chunk, ++k) {
-    const int slot = static_cast<int>(k % static_cast<size_t>(c.slots));
+    const int slot = static_cast<int>(k % static_cast<size_t>(S));
     cudaStream_t s = c.streams[slot];
     const size_t m = std::min(chunk, n - off);
+    drain(slot);
     LaunchArgs la = proto;
     fix.bind(la, static_cast<size_t>(slot));
     la.n = m;
@@ -451,9 +544,12 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     la.outs.clear();
     for (size_t i = 0; i < ins.size(); ++i) {
       void* d = c.buffers[slot][i];
-      check_cuda(cudaMemcpyAsync(d, static_cast<const char*>(ins[i]) + off * elem, m * elem,
-                                 cudaMemcpyHostToDevice, s),
-                 "cudaMemcpyAsync(H2D)");
+      const char* src = static_cast<const char*>(ins[i]) + off * elem;
+      if (stage) {
+        CopyPool::get().copy(c.pinned[slot][i], src, m * elem);
+        src = static_cast<const char*>(c.pinned[slot][i]);
+      }
+      check_cuda(cudaMemcpyAsync(d, src, m * elem, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
       la.ins.push_back(reinterpret_cast<std::uint64_t>(d));
     }
     for (size_t o = 0; o < outs.size(); ++o) {
@@ -461,21 +557,28 @@ void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kin
     }
     launch_all(la, s);
     for (size_t o = 0; o < outs.size(); ++o) {
-      check_cuda(cudaMemcpyAsync(static_cast<char*>(outs[o]) + off * elem,
-                                 c.buffers[slot][ins.size() + o], m * elem, cudaMemcpyDeviceToHost, s),
+      void* dst = stage ? c.pinned[slot][ins.size() + o] : static_cast<char*>(outs[o]) + off * elem;
+      check_cuda(cudaMemcpyAsync(dst, c.buffers[slot][ins.size() + o], m * elem,
+                                 cudaMemcpyDeviceToHost, s),
                  "cudaMemcpyAsync(D2H)");
     }
+    check_cuda(cudaEventRecord(c.done[slot], s), "cudaEventRecord");
+    slot_off[static_cast<size_t>(slot)] = off;
+    slot_len[static_cast<size_t>(slot)] = m;
   }
-  for (int i = 0; i < c.slots; ++i) check_cuda(cudaStreamSynchronize(c.streams[i]), "cudaStreamSynchronize");
+  for (size_t j = 0; j < static_cast<size_t>(S); ++j) {  // oldest chunk first
+    drain(static_cast<int>((k + j) % static_cast<size_t>(S)));
+  }
+  for (int i = 0; i < S; ++i) check_cuda(cudaStreamSynchronize(c.streams[i]), "cudaStreamSynchronize");
   if (flag_ready) cudaEventDestroy(flag_ready);
 }
 
 void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
-               bool full_fixup) {
+               bool full_fixup, const Staging& staging) {
   run_batch(std::vector<const Artifact*>{&a}, device, kind, n, ins, outs, proto, user_stream, sync,
-            full_fixup);
+            full_fixup, {}, staging);
 }
 
 }  // namespace polyeval::rt

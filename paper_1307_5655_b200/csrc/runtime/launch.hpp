@@ -27,9 +27,12 @@ struct LaunchArgs {
   std::vector<std::uint64_t> bounds;
   // interval fast path: fixup list (u32 point indices), counter, capacity
   std::uint64_t list = 0, count = 0, cap = 0;
-  // interval fast path: run the fixup kernel on this stream (after an event
-  // from the launching stream) so it overlaps the next chunk's fast path
-  cudaStream_t fix_stream = nullptr;
+};
+
+/// Host-buffer pipeline shape (pe_exec::stage_chunk / stage_slots; 0 = default).
+struct Staging {
+  std::size_t chunk = 0;  // points per chunk
+  int slots = 0;          // chunks in flight (2..8)
 };
 
 int sm_count(int device);
@@ -39,25 +42,26 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
 
 enum class MemKind { Host, Device };
 
-MemKind classify(const void* p, int* device);
+/// Device (or managed) memory vs host memory; `pinned` (optional) tells
+/// page-locked host memory from pageable.
+MemKind classify(const void* p, int* device, bool* pinned = nullptr);
 
 // Deferred-check state of one caller stream: an accumulating status word and
 // a grow-only full-capacity interval fixup list, both stream-ordered.
 struct StreamState {
-  static constexpr int kMaxChunks = 16;  // fixup counters: one per overlapped chunk
   unsigned* status = nullptr;
   void* list = nullptr;
-  unsigned* count = nullptr;            // kMaxChunks words
+  unsigned* count = nullptr;
   std::uint64_t list_cap = 0;
-  cudaStream_t side = nullptr;          // fixup kernels (overlap with the next chunk)
 };
 
 struct DeviceCtx {
   static constexpr int kMaxSlots = 8;
-  int slots = 3;                          // pipeline depth (PE_STAGE_SLOTS, 2..8)
   cudaStream_t streams[kMaxSlots] = {};
-  std::vector<void*> buffers[kMaxSlots];  // per slot: arrays of `cap` bytes
-  size_t cap = 0;
+  cudaEvent_t done[kMaxSlots] = {};
+  std::vector<void*> buffers[kMaxSlots];  // per slot: device arrays of `cap` bytes
+  std::vector<void*> pinned[kMaxSlots];   // per slot: page-locked host arrays (pageable callers)
+  size_t cap = 0, pinned_cap = 0;
   std::mutex mu;  // serialises host-staged calls on a device
   int sms = 0;
   std::mutex state_mu;
@@ -67,18 +71,14 @@ struct DeviceCtx {
     std::lock_guard<std::mutex> lock(state_mu);
     StreamState& st = states[s];
     if (!st.status) {
-      const size_t words = 1 + StreamState::kMaxChunks;
-      check_cuda(cudaMalloc(reinterpret_cast<void**>(&st.status), words * sizeof(unsigned)),
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&st.status), 2 * sizeof(unsigned)),
                  "cudaMalloc(status)");
-      check_cuda(cudaMemsetAsync(st.status, 0, words * sizeof(unsigned), s),
-                 "cudaMemsetAsync(status)");
+      check_cuda(cudaMemsetAsync(st.status, 0, 2 * sizeof(unsigned), s), "cudaMemsetAsync(status)");
       st.count = st.status + 1;
-      check_cuda(cudaStreamCreateWithFlags(&st.side, cudaStreamNonBlocking), "cudaStreamCreate(side)");
     }
     if (need_list > st.list_cap) {
       if (st.list) {
         check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        check_cuda(cudaStreamSynchronize(st.side), "cudaStreamSynchronize(side)");
         cudaFree(st.list);
       }
       check_cuda(cudaMalloc(&st.list, 4 * need_list), "cudaMalloc(fixup list)");
@@ -112,16 +112,21 @@ struct Flag {
 };
 
 /// Runs the artifacts over [0, n): device pointers in place on
-/// `user_stream`; host pointers through the 3-slot chunked pipeline on the
-/// device's own streams. `arts` run in order per chunk; art i writes
-/// outs[out_base[i] ..] (default 0).
+/// `user_stream`; host pointers through the chunked H2D / walk / D2H
+/// pipeline on the device's own streams (pageable host memory additionally
+/// through page-locked staging buffers). Every buffer must be of `kind`.
+/// `arts` run in order per chunk; art i writes outs[out_base[i] ..] (default 0).
 void run_batch(const std::vector<const Artifact*>& arts, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
-               bool full_fixup = false, const std::vector<size_t>& out_base = {});
+               bool full_fixup = false, const std::vector<size_t>& out_base = {},
+               const Staging& staging = {});
 void run_batch(const Artifact& a, int device, MemKind kind, size_t n,
                const std::vector<const void*>& ins, const std::vector<void*>& outs,
                const LaunchArgs& proto, cudaStream_t user_stream, bool sync,
-               bool full_fixup = false);
+               bool full_fixup = false, const Staging& staging = {});
+
+/// Staging options of a call (pe_exec fields).
+Staging staging_of(const pe_exec* ex);
 
 }  // namespace polyeval::rt

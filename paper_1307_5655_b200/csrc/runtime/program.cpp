@@ -106,25 +106,21 @@ std::vector<std::uint64_t> uniform_bounds(const Program& p, int limit_bits) {
 }
 
 namespace {
-bool partition_enabled() {
-  const char* e = std::getenv("PE_IV_PART");
-  return !(e && std::atoi(e) == 0);
-}
-
 // Interval domain: the program's kernel (+ the mirror module when the sign
 // partition applies, see lower/ptx.cpp and lower::mirror_stream).
 template <typename C>
-void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, Artifact& a) {
+void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, const lower::Tuning& t,
+                   Artifact& a) {
   lower::KernelShape shape;
-  if (nvars == 1 && partition_enabled()) shape.iv_partition = 1;
+  if (nvars == 1 && t.iv_partition >= 0) shape.iv_partition = 1;
   const auto s = lower::lower_strict(prog);
-  a.image = lower::emit_ptx(s, lower::Domain::Interval, shape);
+  a.image = lower::emit_ptx(s, lower::Domain::Interval, shape, t);
   lower::Stream<C> q;
   if (a.image.iv_partition != 1 || !lower::mirror_stream(s, &q)) return;
   lower::KernelShape ms;
   ms.iv_partition = 2;
   auto m = std::make_unique<Artifact>();
-  m->image = lower::emit_ptx(q, lower::Domain::Interval, ms);
+  m->image = lower::emit_ptx(q, lower::Domain::Interval, ms, t);
   if (m->image.iv_partition == 2) a.mirror = std::move(m);
 }
 }  // namespace
@@ -139,19 +135,19 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
       // univariate programs get the sign-partitioned fast path: this module
       // gains an x > 0 entry, a mirror module evaluates q(y) = p(-y) at -x
       if (integer) {
-        emit_interval(i->flat, nvars, *a);
+        emit_interval(i->flat, nvars, tuning, *a);
       } else {
-        emit_interval(f->flat, nvars, *a);
+        emit_interval(f->flat, nvars, tuning, *a);
       }
     } else if (integer) {
       auto s = strict ? lower::lower_strict(i->flat) : lower::lower_fused(i->flat);
-      a->image = lower::emit_ptx(s, d);
+      a->image = lower::emit_ptx(s, d, {}, tuning);
     } else {
       if (d == lower::Domain::I64 || d == lower::Domain::I64F) {
         throw std::invalid_argument("pe_eval_i64 needs a program with int64 coefficients");
       }
       auto s = strict ? lower::lower_strict(f->flat) : lower::lower_fused(f->flat);
-      a->image = lower::emit_ptx(s, d);
+      a->image = lower::emit_ptx(s, d, {}, tuning);
     }
     slot = std::move(a);
   }
@@ -192,7 +188,7 @@ Artifact& Program::limb_artifact(std::uint32_t limbs, bool need_cubin) const {
     slot = std::make_unique<Artifact>();
     lower::KernelShape shape;
     shape.limbs = limbs;
-    slot->image = lower::emit_ptx(lower::lower_fused(i->flat), lower::Domain::I64K, shape);
+    slot->image = lower::emit_ptx(lower::lower_fused(i->flat), lower::Domain::I64K, shape, tuning);
   }
   if (need_cubin && slot->cubin.empty()) {
     CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);

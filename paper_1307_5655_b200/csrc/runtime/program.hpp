@@ -83,6 +83,7 @@ struct Program {
   std::unique_ptr<Front<std::int64_t>> i;   // int64 coefficients
 
   front::WalkStats stats;
+  lower::Tuning tuning;  // code-generation options (pe_program_set_tuning)
   // int64: largest B such that all |x_v| <= B is provably wrap-free;
   // variables absent from the polynomial get UINT64_MAX.
   std::vector<std::uint64_t> i64_uniform_bound;

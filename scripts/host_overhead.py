@@ -60,7 +60,7 @@ for _ in range(20):
     torch.cuda.synchronize()
     iso.append(a.elapsed_time(b) * 1e3)
 iso.sort()
-print(json.dumps({"n": n, "PE_LOOP": os.environ.get("PE_LOOP", "default"),
+print(json.dumps({"n": n, 
                   "stream": "side" if os.environ.get("SIDE_STREAM") else "current(default)",
                   "gpu_us_per_call_back_to_back": round(gpu_us, 2),
                   "host_us_per_evaluate": round(host_us, 2),

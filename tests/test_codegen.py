@@ -35,11 +35,33 @@ def test_kernels_compile_for_sm100a(name):
 
 @pytest.mark.parametrize("name", ["c1", "c2e1000", "c2b1000", "c2e1023", "c4"])
 def test_fused_fp64_issues_exactly_F(name):
+    # one sectioned kernel: F exactly; sections after the first rebuild only
+    # the powers they read (C4: 4 sections, +184 multiplies = 1.5 %)
     wl = CASES[name]()
     prog = pe.compile(wl.poly, wl.schemes)
+    prog.set_tuning(section_ops=2**32 - 1)
     inf = prog.info()
-    st = prog.kernel_stats(pe.DOMAIN_F64)
-    assert st["fp_ops"] == inf["walk_muls"] + inf["power_muls"]
+    F = inf["walk_muls"] + inf["power_muls"]
+    assert prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == F
+    prog.set_tuning()
+    k = prog.f64_slices()
+    fp = prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"]
+    assert F <= fp <= F + (k - 1) * inf["power_muls"]
+    assert (k > 1) == (name == "c4")
+    if k > 1:
+        assert prog.ptx(pe.DOMAIN_F64).count("bar.sync 0;") == k - 1
+
+
+def test_sections_cut_where_few_values_are_live():
+    # C4: each section reloads the 3 coordinates with coherent loads (so
+    # ptxas cannot keep the first ones live) and the kernel compiles
+    wl = W.c4()
+    prog = pe.compile(wl.poly, wl.schemes)
+    ptx = prog.ptx(pe.DOMAIN_F64)
+    k = prog.f64_slices()
+    assert k >= 3
+    assert ptx.count("ld.global.f64") == 3 * (k - 1)
+    assert prog.compile_only(pe.DOMAIN_F64) > 0
 
 
 def test_int64_fused_issues_one_mad_per_record():
@@ -65,20 +87,20 @@ def test_i64_domain_rejects_fp_coefficients():
         prog.kernel_stats(pe.DOMAIN_I64)
 
 
-def test_coefficient_tiers_large_program(monkeypatch):
+def test_coefficient_tiers_large_program():
     # > 8000 distinct coefficient words spill from the constant bank into the
     # parameter tier and then global memory; the kernel must still build
-    monkeypatch.setenv("PE_LANES", "1")  # keeps the ptxas run short
     rng = np.random.default_rng(11)
     n = 12_100
     p = pe.Polynomial(np.arange(n - 1, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, n))
     prog = pe.compile(p, pe.builtin_scheme("estrin"))
+    prog.set_tuning(lanes=1)  # keeps the ptxas run short
     ptx = prog.ptx(pe.DOMAIN_F64)
     assert "pe_pcoef" in ptx and "ld.global.nc.f64" in ptx
     assert prog.compile_only(pe.DOMAIN_F64) > 0
 
 
-def test_horner_chain_becomes_counted_loop(monkeypatch):
+def test_horner_chain_becomes_counted_loop():
     # C1: one 999-step fma(acc, x, c) chain -> a loop over a constant-bank
     # array (same FMA sequence, so results are bit-identical; see
     # test_gpu_edges)
@@ -89,8 +111,8 @@ def test_horner_chain_becomes_counted_loop(monkeypatch):
     assert ".const .align 16 .b64 pe_run0[1015]" in ptx  # 999 words + 2 trips of padding
     assert prog.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
     assert prog.compile_only(pe.DOMAIN_F64) > 0
-    monkeypatch.setenv("PE_LOOP", "0")
     prog2 = pe.compile(wl.poly, wl.schemes)
+    prog2.set_tuning(chain_min=2**32 - 1)
     assert "$Lrun" not in prog2.ptx(pe.DOMAIN_F64)
     assert prog2.kernel_stats(pe.DOMAIN_F64)["fp_ops"] == 1000
 
@@ -128,16 +150,14 @@ def _kernel_words(ptx):
     return words
 
 
-@pytest.mark.parametrize("imm", ["0", "2", "5", "6"])
 @pytest.mark.parametrize("domain", ["f64", "f64strict", "i64", "i64f"])
-def test_coefficient_words_every_delivery_mode(monkeypatch, imm, domain):
+def test_coefficient_words_in_domain_format(domain):
     # The reference worked example (eval_test.cpp:80-93) with int64
-    # coefficients; whatever the coefficient delivery (constant bank, paired
-    # loads, register-bound second coefficients, immediates), the kernel
-    # reads each coefficient in the domain's own word format: doubles for the
-    # FP64 kernels, raw integers for the int64 kernel.
+    # coefficients; through both coefficient regions (uniform-bound words and
+    # the register-bound second region), the kernel reads each coefficient in
+    # the domain's own word format: doubles for the FP64 kernels, raw
+    # integers for the int64 kernel.
     import struct
-    monkeypatch.setenv("PE_IMM", imm)
     e, c = [8, 7, 6, 5, 4, 3, 2, 1, 0], [3, -1, 2, 1, -4, 9, -3, -2, 1]
     d = {"f64": pe.DOMAIN_F64, "f64strict": pe.DOMAIN_F64_STRICT, "i64": pe.DOMAIN_I64,
          "i64f": pe.DOMAIN_I64F}[domain]
@@ -153,7 +173,7 @@ def test_coefficient_words_every_delivery_mode(monkeypatch, imm, domain):
         assert got <= want, (scheme, sorted(got - want))
 
 
-def test_interval_fixup_entry_has_finite_case_replay(monkeypatch):
+def test_interval_fixup_entry_has_finite_case_replay():
     # The fixup entry replays a listed point with the finite-case primitives
     # first (directed-rounding nextafter, plain products + scan-order
     # min/max, NaN-poisoned accumulator) and keeps the bit-level replay
@@ -166,23 +186,23 @@ def test_interval_fixup_entry_has_finite_case_replay(monkeypatch):
     assert "%macc" in fix and "@%pmid bra $Lexact" in fix
     assert "sub.rm.f64" in fix and "add.rn.f64 %tf" in fix
     assert "bra $Lfix" not in fix
-    monkeypatch.setenv("PE_IV_MID", "0")
-    ptx0 = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
+    prog.set_tuning(iv_mid=-1)
+    ptx0 = prog.ptx(pe.DOMAIN_INTERVAL)
     assert "%macc" not in ptx0
 
 
 @pytest.mark.parametrize("name", ["c2e1000", "c3", "c4"])
-def test_list_scheduler_keeps_ops_and_words(name, monkeypatch):
+def test_list_scheduler_keeps_ops_and_words(name):
     # The latency-aware reordering (on by default for wide programs like C4,
-    # PE_SCHED forces it elsewhere) only permutes SSA ops: the kernel issues
-    # the same FP64 work and reads the same coefficient words.
+    # sched_window forces it elsewhere) only permutes SSA ops: the kernel
+    # issues the same FP64 work and reads the same coefficient words.
     wl = CASES[name]()
     dom = pe.DOMAIN_I64F if wl.domain == "i64" else pe.DOMAIN_F64
-    monkeypatch.setenv("PE_SCHED", "0,0")  # kernels are generated lazily, at ptx()
     plain = pe.compile(wl.poly, wl.schemes)
+    plain.set_tuning(sched_window=1)
     a, fa = plain.ptx(dom), plain.kernel_stats(dom)["fp_ops"]
-    monkeypatch.setenv("PE_SCHED", "32,6")
     sched = pe.compile(wl.poly, wl.schemes)
+    sched.set_tuning(sched_window=32, sched_distance=6)
     b, fb = sched.ptx(dom), sched.kernel_stats(dom)["fp_ops"]
     assert a != b
     assert fa == fb

@@ -50,7 +50,9 @@ def test_reference_compiled_trivariate_nested_programs():
     native = pe.compile(wl.poly, wl.schemes)
     assert imported.info() == native.info()
     assert imported.ptx(pe.DOMAIN_F64) == native.ptx(pe.DOMAIN_F64)
-    assert imported.f64_slices() == 1  # no terms/schemes to slice by
+    # sections are cut on the lowered op stream, so the reference's own
+    # CompiledProgram gets the identical sectioned kernel
+    assert imported.f64_slices() == native.f64_slices() > 1
     with pytest.raises(ValueError):
         imported.dot()
 

@@ -125,12 +125,13 @@ def test_repeatable_and_shard_invariant(cuda_device):
     assert torch.equal(full, again) and torch.equal(full, halves)
 
 
-@pytest.mark.parametrize("next_mode", ["hybrid", "fma", "int", "dir"])
-def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch, next_mode):
-    monkeypatch.setenv("PE_IV_NEXT", next_mode)
-    # The fast interval path (sign-case products, integer nextafter with
-    # sign-flip detection) must equal the strict replay and the oracle on
-    # intervals that straddle zero, touch zero, underflow and overflow.
+@pytest.mark.parametrize("mid", [0, -1])
+def test_interval_fast_path_equals_strict_replay(cuda_device, mid):
+    # The fast interval path (sign-case products, FP64-pipe nextafter with
+    # "did not move" checks, static signs) and the fixup replay (with and
+    # without its finite-case stage) must equal the strict replay and the
+    # oracle on intervals that straddle zero, touch zero, underflow and
+    # overflow.
     rng = np.random.default_rng(21)
     n = 50_000
     x = rng.uniform(-1, 1, n)
@@ -149,11 +150,11 @@ def test_interval_fast_path_equals_strict_replay(cuda_device, monkeypatch, next_
     for scheme, deg in (("estrin", 200), ("horner", 30), ("balanced", 64)):
         wl = W.c5()
         p = pe.Polynomial(np.arange(deg, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, deg + 1))
-        monkeypatch.setenv("PE_IV_FAST", "0")
         slow = pe.compile(p, pe.builtin_scheme(scheme))
+        slow.set_tuning(iv_fast=-1)
         s = pe.Evaluator(pe.IntervalDomain(), slow).evaluate(([lo], [hi]))
-        monkeypatch.delenv("PE_IV_FAST")
         fast = pe.compile(p, pe.builtin_scheme(scheme))
+        fast.set_tuning(iv_mid=mid)
         f = pe.Evaluator(pe.IntervalDomain(), fast).evaluate(([lo], [hi]))
         assert "%facc" not in slow.ptx(pe.DOMAIN_INTERVAL)
         assert "%facc" in fast.ptx(pe.DOMAIN_INTERVAL)
@@ -202,17 +203,25 @@ def test_evaluate_many_matches_single_calls(cuda_device):
         assert np.array_equal(d.cpu().numpy().view(np.int64), single.view(np.int64))
 
 
-@pytest.mark.parametrize("slices", ["1", "3", "7"])
-def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
-    # wide fp64 programs run as K slice kernels (store, then accumulate);
-    # any K must stay inside the fused-fp64 tolerance, host or device buffers
-    monkeypatch.setenv("PE_SLICES", slices)
+@pytest.mark.parametrize("section_ops", [2**32 - 1, 1000, 400])
+@pytest.mark.parametrize("carry", [0, 1])
+def test_sectioned_wide_program_bit_identical(cuda_device, section_ops, carry):
+    # long walks run in barrier-separated sections (coordinates reloaded,
+    # powers rebuilt or carried); the op sequence is unchanged, so every
+    # section count gives the unsectioned kernel's bits — within the fused
+    # tolerance of the oracle, host or device buffers
     rng = np.random.default_rng(4)
     ex = np.unique(rng.integers(0, 20, size=(3000, 3)), axis=0).astype(np.uint32)
     p = pe.Polynomial(ex, rng.normal(size=len(ex)), ("x", "y", "z"))
     sch = [pe.builtin_scheme("balanced")] * 3
-    prog = pe.compile(p, sch)
     pts = [rng.uniform(-1, 1, 10_007) for _ in range(3)]
+    one = pe.compile(p, sch)
+    one.set_tuning(section_ops=2**32 - 1)
+    base = pe.Evaluator(pe.DoubleDomain(), one).evaluate([_t(a, cuda_device) for a in pts]).cpu().numpy()
+    prog = pe.compile(p, sch)
+    prog.set_tuning(section_ops=section_ops, carry_powers=carry)
+    if section_ops < 2**32 - 1:
+        assert prog.f64_slices() > 1
     ref = pyoracle.Oracle(p, sch).eval_f64(pts)
     scale = pyoracle.abs_term_sum(p, pts)
     ev = pe.Evaluator(pe.DoubleDomain(), prog)
@@ -220,6 +229,31 @@ def test_sliced_wide_program_within_tolerance(cuda_device, monkeypatch, slices):
     host = ev.evaluate(pts)
     assert np.all(np.abs(dev - ref) <= 1e-12 * scale)
     assert np.array_equal(dev.view(np.int64), host.view(np.int64))
+    assert np.array_equal(dev.view(np.int64), base.view(np.int64))
+
+
+@pytest.mark.parametrize("domain", ["f64strict", "i64"])
+def test_sectioned_exact_domains(cuda_device, domain):
+    # sections in the bit-exact domains: strict fp64 equals the oracle's
+    # reference op order bit for bit, int64 is exact
+    rng = np.random.default_rng(8)
+    ex = np.unique(rng.integers(0, 12, size=(1500, 3)), axis=0).astype(np.uint32)
+    sch = [pe.builtin_scheme("balanced")] * 3
+    if domain == "i64":
+        p = pe.Polynomial(ex, rng.integers(-8, 9, size=len(ex)).astype(np.int64), ("x", "y", "z"))
+        pts = [rng.integers(-2, 3, 5003).astype(np.int64) for _ in range(3)]
+        prog = pe.compile(p, sch)
+        prog.set_tuning(section_ops=300)
+        got = pe.Evaluator(pe.BigIntDomain(int_pipe=True), prog).evaluate(pts)
+        assert np.array_equal(got, pyoracle.Oracle(p, sch).eval_i64(pts))
+    else:
+        p = pe.Polynomial(ex, rng.normal(size=len(ex)), ("x", "y", "z"))
+        pts = [rng.uniform(-1, 1, 5003) for _ in range(3)]
+        prog = pe.compile(p, sch)
+        prog.set_tuning(section_ops=300)
+        got = pe.Evaluator(pe.DoubleDomain(strict=True), prog).evaluate(pts)
+        ref = pyoracle.Oracle(p, sch).eval_f64(pts)
+        assert np.array_equal(got.view(np.int64), ref.view(np.int64))
 
 
 @pytest.mark.parametrize("domain", ["f64", "i64", "interval"])
@@ -312,7 +346,7 @@ def test_program_shared_across_host_threads(cuda_device):
 
 
 @pytest.mark.parametrize("n", [1, 31, 100_000, 100_003])
-def test_chain_loop_bit_identical_to_straight_line(n, cuda_device, monkeypatch):
+def test_chain_loop_bit_identical_to_straight_line(n, cuda_device):
     # the looped Hörner chain issues the same FMA sequence as the straight-line
     # kernel: results must agree bit for bit (and stay within TOL of the oracle)
     wl = W.c1()
@@ -320,8 +354,8 @@ def test_chain_loop_bit_identical_to_straight_line(n, cuda_device, monkeypatch):
     looped = pe.compile(wl.poly, wl.schemes)
     assert "$Lrun0" in looped.ptx(pe.DOMAIN_F64)
     a = pe.Evaluator(pe.DoubleDomain(), looped).evaluate([_t(pts[0], cuda_device)]).cpu().numpy()
-    monkeypatch.setenv("PE_LOOP", "0")
     flat = pe.compile(wl.poly, wl.schemes)
+    flat.set_tuning(chain_min=2**32 - 1)
     assert "$Lrun0" not in flat.ptx(pe.DOMAIN_F64)
     b = pe.Evaluator(pe.DoubleDomain(), flat).evaluate([_t(pts[0], cuda_device)]).cpu().numpy()
     assert np.array_equal(a.view(np.int64), b.view(np.int64))
@@ -472,7 +506,7 @@ def test_chain_loops_inside_nested_programs(cuda_device):
 
 @pytest.mark.parametrize("n", [1, 5, 33, 4097, 150_001])
 @pytest.mark.parametrize("scheme", ["estrin", "horner", "balanced"])
-def test_interval_sign_partition_bit_exact(n, scheme, cuda_device, monkeypatch):
+def test_interval_sign_partition_bit_exact(n, scheme, cuda_device):
     # Sign-partitioned fast path: x > 0 intervals run the program's x > 0
     # entry, x < 0 intervals the mirrored program q(y) = p(-y) at -x, the
     # rest (touching / straddling zero, invalid) the fixup replay. Results
@@ -494,12 +528,12 @@ def test_interval_sign_partition_bit_exact(n, scheme, cuda_device, monkeypatch):
         lo[60:70], hi[60:70] = -2e-200, -1e-200
         lo[70:80], hi[70:80] = 1e150, 2e150    # overflow
         lo[80:90], hi[80:90] = -2e150, -1e150
-    monkeypatch.setenv("PE_IV_PART_MIN", "1")
     part = pe.compile(p, pe.builtin_scheme(scheme))
+    part.set_tuning(iv_partition_min=1)
     f = pe.Evaluator(pe.IntervalDomain(), part).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
     assert "pe_walk_interval_pos" in part.ptx(pe.DOMAIN_INTERVAL)
-    monkeypatch.setenv("PE_IV_PART", "0")
     plain = pe.compile(p, pe.builtin_scheme(scheme))
+    plain.set_tuning(iv_partition=-1)
     g = pe.Evaluator(pe.IntervalDomain(), plain).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
     assert "pe_walk_interval_pos" not in plain.ptx(pe.DOMAIN_INTERVAL)
     o = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
@@ -509,12 +543,12 @@ def test_interval_sign_partition_bit_exact(n, scheme, cuda_device, monkeypatch):
         assert np.array_equal(b.view(np.int64), c.view(np.int64))
 
 
-def test_interval_sign_partition_host_buffers_and_errors(cuda_device, monkeypatch):
+def test_interval_sign_partition_host_buffers_and_errors(cuda_device):
     # host (pinned-staging) path through the partition, and the invalid-
     # interval status raised by the classifier
-    monkeypatch.setenv("PE_IV_PART_MIN", "1")
     wl = W.c5()
     prog = pe.compile(wl.poly, wl.schemes)
+    prog.set_tuning(iv_partition_min=1)
     lo, hi = wl.points(300_000)
     ev = pe.Evaluator(pe.IntervalDomain(), prog)
     got = ev.evaluate((lo, hi))
