@@ -185,8 +185,9 @@ typedef struct pe_tuning {
   uint32_t block;          /* threads per CTA, 32..1024 */
   uint32_t min_ctas;       /* .minnctapersm of the walk kernel */
   uint32_t sync_every;     /* walk ops between CTA barriers */
-  uint32_t section_ops;    /* long int/fp64 walks: ops per barrier-separated section
-                              (default 3000; UINT32_MAX = never section) */
+  uint32_t section_ops;    /* long int/fp64 walks: ops per section of the persistent
+                              sectioned kernel (default 3000; UINT32_MAX = one plain
+                              kernel) */
   uint32_t sched_window;   /* latency-aware op reordering window (1 = walk order) */
   uint32_t sched_distance; /* producer distance the reordering aims for */
   uint32_t chain_min;      /* shortest Horner run emitted as a loop (default 64;
@@ -194,7 +195,11 @@ typedef struct pe_tuning {
   int32_t iv_fast;         /* interval: -1 = bit-level replay only (no fast path) */
   int32_t iv_mid;          /* interval fixup: -1 = skip the finite-case replay */
   int32_t iv_partition;    /* univariate interval sign partition: -1 = off */
-  int32_t carry_powers;    /* sections: 1 = keep power tables live across sections */
+  uint32_t group_tiles;    /* sectioned kernels: tiles of points a CTA runs through one
+                              section before the next (default 8) */
+  int32_t word_layout;     /* sections: -1 = one coefficient block for the whole walk
+                              (default: one block per section) */
+  int32_t reserved;
   uint64_t iv_partition_min; /* smallest batch that is sign-partitioned (default 65536) */
 } pe_tuning;
 

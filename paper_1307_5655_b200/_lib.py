@@ -59,7 +59,9 @@ class pe_tuning(C.Structure):
         ("iv_fast", C.c_int32),
         ("iv_mid", C.c_int32),
         ("iv_partition", C.c_int32),
-        ("carry_powers", C.c_int32),
+        ("group_tiles", C.c_uint32),
+        ("word_layout", C.c_int32),
+        ("reserved", C.c_int32),
         ("iv_partition_min", C.c_uint64),
     ]
 

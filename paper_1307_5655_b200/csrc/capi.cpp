@@ -455,7 +455,8 @@ pe_status pe_program_set_tuning(pe_program* program, const pe_tuning* t) {
     d.iv_fast = t->iv_fast;
     d.iv_mid = t->iv_mid;
     d.iv_partition = t->iv_partition;
-    d.carry_powers = t->carry_powers;
+    d.group_tiles = t->group_tiles;
+    d.word_layout = t->word_layout;
     d.iv_partition_min = t->iv_partition_min;
     return PE_OK;
   });

@@ -190,7 +190,8 @@ class Emitter {
       : s_(s), d_(d), P_(shape.lanes), block_(shape.block), sync_every_(shape.sync_every),
         paired_(d != Domain::Interval && d != Domain::I64K), min_ctas_(shape.min_ctas),
         K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1),
-        part_(shape.iv_partition), tuning_(t), cuts_(std::move(cuts)) {
+        part_(shape.iv_partition), tuning_(t), cuts_(std::move(cuts)),
+        group_tiles_(t.group_tiles ? t.group_tiles : 8) {
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
 
@@ -247,7 +248,7 @@ class Emitter {
       // exact fast path; points it cannot prove go to the fixup list
       emit_fast_body();
     } else if (cuts_.size() > 1) {
-      emit_sectioned();
+      emit_grouped(img);
     } else {
       emit_prologue();
       emit_powers();
@@ -316,7 +317,7 @@ class Emitter {
 
     std::ostringstream m;
     m << module_header(img, fast ? "interval-fast-path+fixup" : "");
-    m << run_arrays_ << main_entry << fix_entry << part_entry;
+    m << run_arrays_ << funcs_ << main_entry << fix_entry << part_entry;
     img.ptx = m.str();
     img.fp_ops = fp_ops_;
     img.int_ops = int_ops_;
@@ -407,6 +408,7 @@ class Emitter {
       param(".param .u64 pe_pidx");
       param(".param .u64 pe_pcnt");
     }
+    if (cuts_.size() > 1) param(".param .u64 pe_scratch");
     if (n_param_ > 0) param(".param .align 16 .b8 pe_pcoef[" + std::to_string(8 * n_param_) + "]");
     m << ")\n.maxntid " << maxntid << ", 1, 1\n";
     if (min_ctas) m << ".minnctapersm " << min_ctas << "\n";
@@ -446,7 +448,29 @@ class Emitter {
         reg_bound_[r.id] = 1;
       }
     }
+    // Sectioned kernels place the words section by section (each section's
+    // uniform-bound words, then its register-bound words): the constant
+    // working set of a section is one contiguous block.
+    std::vector<std::uint32_t> sec_of(s_.coefs.size(), 0);
+    std::uint32_t nsec = 1;
+    if (cuts_.size() > 1 && tuning_.word_layout >= 0) {
+      nsec = static_cast<std::uint32_t>(cuts_.size());
+      std::vector<char> seen(s_.coefs.size(), 0);
+      std::uint32_t sec = 0;
+      for (std::size_t i = 0; i < s_.ops.size(); ++i) {
+        while (sec + 1 < cuts_.size() && i >= cuts_[sec]) ++sec;
+        for (const Operand* o : {&s_.ops[i].a, &s_.ops[i].b, &s_.ops[i].c}) {
+          if (o->is(Operand::Coef) && !seen[o->id]) {
+            seen[o->id] = 1;
+            sec_of[o->id] = sec;
+          }
+        }
+      }
+      if (s_.result.is(Operand::Coef) && !seen[s_.result.id]) sec_of[s_.result.id] = nsec - 1;
+    }
+    for (std::uint32_t sec = 0; sec < nsec; ++sec) {
     for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
+      if (sec_of[k] != sec) continue;
       if (split && reg_bound_[k]) continue;  // second region, below
       if (d_ == Domain::Interval) {
         const IvCoef c = ivcoef(k);
@@ -470,14 +494,18 @@ class Emitter {
     if (split) {
       if (words_.size() & 1) words_.push_back(0);  // region starts on a pair
       for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
-        if (!reg_bound_[k]) continue;
+        if (!reg_bound_[k] || sec_of[k] != sec) continue;
         coef_lo_[k] = coef_hi_[k] = static_cast<std::uint32_t>(words_.size());
         words_.push_back(scalar_word(k));
       }
+      if (words_.size() & 1) words_.push_back(0);  // next section starts on a pair
+    }
     }
     const auto n = static_cast<std::uint32_t>(words_.size());
     n_const_ = std::min(n, CoefTiers::kConstCap);
-    n_param_ = std::min(n - n_const_, CoefTiers::kParamCap);
+    // sectioned kernels address coefficients from a register (below); the
+    // parameter space cannot be, so their overflow goes to the global tier
+    n_param_ = cuts_.size() > 1 ? 0 : std::min(n - n_const_, CoefTiers::kParamCap);
     n_global_ = n - n_const_ - n_param_;
   }
 
@@ -544,7 +572,8 @@ class Emitter {
         std::string r = "%c" + std::to_string(n_creg_++);
         std::string r2 = "%c" + std::to_string(n_creg_++);
         if (pair_const) {
-          body_ << "  ld.const.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_coef+" << 8 * w << "];\n";
+          body_ << "  ld.const.v2." << ldty() << " {" << r << ", " << r2 << "}, [" << cbase() << "+"
+                << 8 * w << "];\n";
         } else {
           body_ << "  ld.param.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_pcoef+"
                 << 8 * (w - n_const_) << "];\n";
@@ -555,7 +584,7 @@ class Emitter {
     }
     std::string r = "%c" + std::to_string(n_creg_++);
     if (w < n_const_) {
-      body_ << "  ld.const." << ldty() << " " << r << ", [pe_coef+" << 8 * w << "];\n";
+      body_ << "  ld.const." << ldty() << " " << r << ", [" << cbase() << "+" << 8 * w << "];\n";
     } else if (w < n_const_ + n_param_) {
       body_ << "  ld.param." << ldty() << " " << r << ", [pe_pcoef+" << 8 * (w - n_const_) << "];\n";
     } else {
@@ -574,7 +603,7 @@ class Emitter {
   }
   // section suffix of per-section power / coordinate copies (sections
   // after the first reload the coordinates and rebuild the powers they use)
-  std::string sx() const { return sec_ && tuning_.carry_powers <= 0 ? "s" + std::to_string(sec_) : ""; }
+  std::string sx() const { return sec_ ? "s" + std::to_string(sec_) : ""; }
   std::string pw(std::uint32_t id, std::uint32_t lane, bool hi = false) const {
     if (d_ == Domain::Interval) {
       return std::string(fast_ ? "%f" : medium_ ? "%m" : "%") + (hi ? "ph" : "pl") + std::to_string(id) + ln(lane);
@@ -814,36 +843,194 @@ class Emitter {
     emit_ops(0, s_.ops.size());
   }
 
-  // Sectioned walk (scalar domains, long streams): the op sequence is cut at
-  // points where few walk values are live (emit_ptx); each section after the
-  // first starts with a CTA barrier, reloads the coordinates (L1/L2 hits)
-  // and rebuilds the powers it uses, so only the live walk values cross a
-  // section boundary in registers. All warps of the CTA run one section's
-  // code at a time (one instruction window per SM), and each section's
-  // register pressure is its own power table, not the whole program's. The
-  // arithmetic is the unsectioned op sequence, unchanged.
-  void emit_sectioned() {
-    emit_prologue();
-    declare_walk_regs();
+  // Sectioned walk (scalar domains, long streams). A straight-line walk of
+  // 10k+ ops is larger than the SM's instruction and constant caches: if
+  // every CTA ran the whole walk, each CTA would stream all of its code and
+  // coefficients from the GPC caches again (C4: 78 % instruction-cache and
+  // 85 % constant-cache hits, vs 99.5 % / 96 % for walks of ~3k ops). So the
+  // op sequence is cut into sections where few walk values are live
+  // (emit_ptx), and the kernel is persistent over groups of T tiles: a CTA
+  // runs section 0 on T tiles, then section 1 on the same T tiles, ...;
+  // each section's code and constants stay hot for T tiles. Each section is
+  // a non-inlined .func called once per tile (inside a loop ptxas would hoist
+  // the section's thousands of constant loads into registers), values live
+  // across a cut go to a per-CTA scratch slot (L2-resident: grid x T x live x
+  // tile words), coordinates are reloaded per tile (L2 hits after the first
+  // section), each section rebuilds the powers it reads. The arithmetic is
+  // the unsectioned op sequence, unchanged: results are bit-identical.
+  void emit_grouped(KernelImage& img) {
+    const std::uint32_t T = group_tiles_;
+    const auto live = live_at_cuts();
+    std::size_t L = 1;
+    for (const auto& l : live) L = std::max(L, l.size());
+    img.group_tiles = T;
+    img.scratch_values = static_cast<std::uint32_t>(L);
+    // the sections, one function each (kernel parameter names re-declared as
+    // function parameters, so the frame helpers read them unchanged)
+    std::vector<std::string> fparams;
+    for (std::uint32_t i = 0; i < img.n_in; ++i) fparams.push_back("pe_in" + std::to_string(i));
+    for (std::uint32_t i = 0; i < img.n_out; ++i) fparams.push_back("pe_out" + std::to_string(i));
+    fparams.push_back("pe_n");
+    fparams.push_back("pe_gcoef");
+    if (img.has_flag) fparams.push_back("pe_flag");
+    if (img.has_bounds) {
+      for (std::uint32_t v = 0; v < s_.nvars; ++v) fparams.push_back("pe_bound" + std::to_string(v));
+    }
+    fparams.push_back("pe_tbase");  // first point index of the tile
+    fparams.push_back("pe_slot");   // scratch slot of the tile
     std::size_t begin = 0;
     for (std::size_t k = 0; k < cuts_.size(); ++k) {
       const std::size_t end = cuts_[k];
       sec_ = static_cast<std::uint32_t>(k);
+      reset_entry();
+      decls_ << "  .reg .b64 %ix<" << P_ << ">;\n  .reg .pred %pv<" << P_ << ">;\n  .reg .b64 %gsl, %ga;\n";
+      body_ << "  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
+            << "  ld.param.u64 %rd3, [pe_n];\n  sub.u64 %rd12, %rd3, 1;\n"
+            << "  ld.param.u64 %rd1, [pe_tbase];\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
+            << "  ld.param.u64 %gsl, [pe_slot];\n  shl.b64 %rd14, %rd2, 3;\n  add.u64 %gsl, %gsl, %rd14;\n";
+      if (n_global_ > 0) {
+        body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
+      }
+      for (std::uint32_t q = 0; q < P_; ++q) {
+        body_ << "  mul.wide.u32 %rd13, %r2, " << q << ";\n  add.u64 %rd13, %rd1, %rd13;\n"
+              << "  setp.lt.u64 %pv" << q << ", %rd13, %rd3;\n  min.u64 %rd13, %rd13, %rd12;\n"
+              << "  shl.b64 %ix" << q << ", %rd13, 3;\n";
+      }
+      emit_tile_coords(k == 0);
+      // value j of lane q: %gsl + (j * ntid * P + q * ntid) * 8
+      auto slot = [&](std::size_t j, std::uint32_t q) {
+        body_ << "  mul.wide.u32 %ga, %r2, " << (j * P_ + q) * 8 << ";\n  add.u64 %ga, %ga, %gsl;\n";
+      };
+      declare_walk_regs();
       if (k > 0) {
-        body_ << "  bar.sync 0;\n";
-        if (tuning_.carry_powers <= 0) emit_coord_reload();
+        for (std::size_t j = 0; j < live[k - 1].size(); ++j) {
+          for (std::uint32_t q = 0; q < P_; ++q) {
+            slot(j, q);
+            body_ << "  ld.global." << ldty() << " " << reg(live[k - 1][j], q) << ", [%ga];\n";
+          }
+        }
       }
-      if (k == 0 || tuning_.carry_powers <= 0) {
-        std::vector<char> need = k == 0 && tuning_.carry_powers > 0
-                                     ? std::vector<char>(s_.powers.size(), 1)
-                                     : powers_used(begin, end, k + 1 == cuts_.size());
-        emit_powers(&need);
-      }
+      std::vector<char> need = powers_used(begin, end, k + 1 == cuts_.size());
+      emit_powers(&need);
       emit_ops(begin, end);
+      if (k + 1 < cuts_.size()) {
+        for (std::size_t j = 0; j < live[k].size(); ++j) {
+          for (std::uint32_t q = 0; q < P_; ++q) {
+            slot(j, q);
+            body_ << "  st.global." << ldty() << " [%ga], " << reg(live[k][j], q) << ";\n";
+          }
+        }
+      } else {
+        emit_store();
+      }
+      body_ << "  ret;\n";
+      if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
+      if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
+      if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
+      if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+      if (n_tr_ > 0) decls_ << "  .reg .b32 %tr<" << n_tr_ << ">;\n";
+      std::ostringstream f;
+      f << ".func pe_section" << k << "(";
+      for (std::size_t i = 0; i < fparams.size(); ++i) {
+        f << (i ? ",\n  " : "\n  ") << ".param .u64 " << fparams[i];
+      }
+      f << ")\n{\n  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n"
+        << decls_.str() << body_.str() << "}\n\n";
+      funcs_ += f.str();
       begin = end;
     }
-    emit_epilogue();
     sec_ = 0;
+    // the persistent kernel: groups of T tiles, each section over the group
+    reset_entry();
+    decls_ << "  .reg .b64 %gs, %gtl, %gn, %gb, %gstep, %gt, %gtile, %gsl, %gbase;\n"
+           << "  .reg .pred %gp;\n  .reg .b64 %ka<" << fparams.size() << ">;\n";
+    body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n"
+          << "  ld.param.u64 %rd3, [pe_n];\n"
+          << "  ld.param.u64 %gs, [pe_scratch];\n  cvta.to.global.u64 %gs, %gs;\n"
+          << "  mul.wide.u32 %gtl, %r2, " << P_ << ";\n"                       // tile = ntid * P
+          << "  add.u64 %gn, %rd3, %gtl;\n  sub.u64 %gn, %gn, 1;\n  div.u64 %gn, %gn, %gtl;\n"
+          << "  mul.wide.u32 %gb, %r1, " << T << ";\n"
+          << "  mov.u32 %r4, %nctaid.x;\n  mul.wide.u32 %gstep, %r4, " << T << ";\n";
+    for (std::size_t i = 0; i + 2 < fparams.size(); ++i) {
+      body_ << "  ld.param.u64 %ka" << i << ", [" << fparams[i] << "];\n";
+    }
+    body_ << "$Lgroup:\n  setp.ge.u64 %gp, %gb, %gn;\n  @%gp bra.uni $Ldone;\n";
+    for (std::size_t k = 0; k < cuts_.size(); ++k) {
+      const std::string lt = "$Ltile" + std::to_string(k), le = "$Ltend" + std::to_string(k);
+      body_ << "  mov.u64 %gt, 0;\n" << lt << ":\n"
+            << "  add.u64 %gtile, %gb, %gt;\n  setp.ge.u64 %gp, %gtile, %gn;\n  @%gp bra.uni " << le << ";\n"
+            << "  mul.lo.u64 %gbase, %gtile, %gtl;\n"
+            // slot = scratch + ((ctaid * T + t) * L * tile) * 8
+            << "  mul.wide.u32 %gsl, %r1, " << T << ";\n  add.u64 %gsl, %gsl, %gt;\n"
+            << "  mul.lo.u64 %gsl, %gsl, %gtl;\n  mul.lo.u64 %gsl, %gsl, " << 8 * L << ";\n"
+            << "  add.u64 %gsl, %gsl, %gs;\n  {\n";
+      for (std::size_t i = 0; i < fparams.size(); ++i) {
+        const std::string v = i + 2 == fparams.size() ? "%gbase" : i + 1 == fparams.size() ? "%gsl"
+                                                                  : "%ka" + std::to_string(i);
+        body_ << "  .param .u64 a" << i << ";\n  st.param.u64 [a" << i << "], " << v << ";\n";
+      }
+      body_ << "  call.uni pe_section" << k << ", (";
+      for (std::size_t i = 0; i < fparams.size(); ++i) body_ << (i ? ", " : "") << "a" << i;
+      body_ << ");\n  }\n"
+            << "  add.u64 %gt, %gt, 1;\n  setp.lt.u64 %gp, %gt, " << T << ";\n  @%gp bra.uni " << lt << ";\n"
+            << le << ":\n  bar.sync 0;\n";
+    }
+    body_ << "  add.u64 %gb, %gb, %gstep;\n  bra.uni $Lgroup;\n";
+    finish_entry();
+  }
+
+  // SSA registers defined before each cut and read at or after it (or the
+  // result), one list per cut except the last.
+  std::vector<std::vector<std::uint32_t>> live_at_cuts() const {
+    std::unordered_map<std::uint32_t, std::size_t> def, last;
+    auto use = [&](const Operand& o, std::size_t at) {
+      if (o.is(Operand::Reg)) last[o.id] = at;
+    };
+    for (std::size_t i = 0; i < s_.ops.size(); ++i) {
+      use(s_.ops[i].a, i);
+      use(s_.ops[i].b, i);
+      use(s_.ops[i].c, i);
+      def[s_.ops[i].dst] = i;
+    }
+    use(s_.result, s_.ops.size());
+    std::vector<std::vector<std::uint32_t>> out(cuts_.size() > 0 ? cuts_.size() - 1 : 0);
+    for (std::size_t c = 0; c + 1 < cuts_.size(); ++c) {
+      for (const auto& [reg, d] : def) {
+        auto it = last.find(reg);
+        if (d < cuts_[c] && it != last.end() && it->second >= cuts_[c]) out[c].push_back(reg);
+      }
+      std::sort(out[c].begin(), out[c].end());
+    }
+    return out;
+  }
+
+  // Coordinates of the current tile (section-suffixed registers); the first
+  // section also runs the int64 range checks.
+  void emit_tile_coords(bool checks) {
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      body_ << "  ld.param.u64 %rd5, [pe_in" << v << "];\n  cvta.to.global.u64 %rd5, %rd5;\n";
+      for (std::uint32_t q = 0; q < P_; ++q) {
+        if (d_ == Domain::I64F) {
+          decls_ << "  .reg .f64 " << xr(v, q) << ";\n  .reg .b64 " << xi(v, q) << ";\n";
+        } else {
+          decls_ << "  .reg ." << ldty() << " " << xr(v, q) << ";\n";
+        }
+        body_ << "  add.u64 %rd6, %rd5, %ix" << q << ";\n  ld.global.nc." << ioty() << " "
+              << (int_io() ? xi(v, q) : xr(v, q)) << ", [%rd6];\n";
+        if (d_ == Domain::I64F) body_ << "  cvt.rn.f64.s64 " << xr(v, q) << ", " << xi(v, q) << ";\n";
+      }
+    }
+    if (!checks || !int_io()) return;
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      body_ << "  ld.param.u64 %rd8, [pe_bound" << v << "];\n";
+      for (std::uint32_t q = 0; q < P_; ++q) {
+        const std::string ok = "$Lgok" + std::to_string(v) + "_" + std::to_string(q);
+        body_ << "  abs.s64 %rd9, " << xi(v, q) << ";\n  setp.gt.u64 %p2, %rd9, %rd8;\n"
+              << "  @!%p2 bra " << ok << ";\n"
+              << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n"
+              << "  @%pv" << q << " st.global.u32 [%rd7], 1;\n" << ok << ":\n";
+      }
+    }
   }
 
   // Powers read by ops [begin, end) (and by the result, for the last
@@ -863,24 +1050,6 @@ class Emitter {
       if (need[i] && s_.powers[i].exponent > 1) need[s_.powers[i].lo] = need[s_.powers[i].hi] = 1;
     }
     return need;
-  }
-
-  // Section entry: fresh coordinate registers, loaded with plain (coherent)
-  // global loads after the barrier so ptxas cannot reuse the first load.
-  void emit_coord_reload() {
-    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
-      body_ << "  ld.param.u64 %rd5, [pe_in" << v << "];\n  cvta.to.global.u64 %rd5, %rd5;\n";
-      for (std::uint32_t k = 0; k < P_; ++k) {
-        if (d_ == Domain::I64F) {
-          decls_ << "  .reg .f64 " << xr(v, k) << ";\n  .reg .b64 " << xi(v, k) << ";\n";
-        } else {
-          decls_ << "  .reg ." << ldty() << " " << xr(v, k) << ";\n";
-        }
-        body_ << "  add.u64 %rd6, %rd5, %ix" << k << ";\n  ld.global." << ioty() << " "
-              << (int_io() ? xi(v, k) : xr(v, k)) << ", [%rd6];\n";
-        if (d_ == Domain::I64F) body_ << "  cvt.rn.f64.s64 " << xr(v, k) << ", " << xi(v, k) << ";\n";
-      }
-    }
   }
 
   void declare_walk_regs() {
@@ -1667,6 +1836,9 @@ class Emitter {
   Tuning tuning_;
   std::vector<std::size_t> cuts_;  // section boundaries (op indices), ascending, ends with ops.size()
   std::uint32_t sec_ = 0;          // section being emitted
+  std::uint32_t group_tiles_ = 8;  // sectioned kernels: tiles per CTA per section pass
+  std::string funcs_;              // sectioned kernels: the section functions
+  std::string cbase() const { return "pe_coef"; }
   bool fast_ = false;  // emitting the interval fast path
   bool medium_ = false;  // emitting the finite-case replay of the fixup entry
   std::uint32_t gather_ = 0;  // emitting a partitioned entry: 1 front (x > 0), 2 back (x < 0)

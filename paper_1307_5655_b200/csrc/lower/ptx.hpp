@@ -54,7 +54,9 @@ struct KernelImage {
   bool interval_fast_path = false; // fast exact path + fixup entry (strict replay)
   std::uint32_t limbs = 1;         // I64K: 64-bit words per value (= result arrays)
   std::uint32_t chain_loops = 0;   // Hörner runs emitted as counted loops
-  std::uint32_t sections = 1;      // barrier-separated sections of the walk
+  std::uint32_t sections = 1;      // sections of the walk (persistent grouped kernel when > 1)
+  std::uint32_t group_tiles = 0;   // sectioned: tiles per CTA per section pass
+  std::uint32_t scratch_values = 0;  // sectioned: values per point in the scratch slot
   std::string fix_entry;           // fixup kernel symbol (interval fast path)
   // sign-partitioned interval fast path (univariate): 1 = this module also
   // has `part_entry` (points with x > 0, taken from the front of a device
@@ -87,7 +89,8 @@ struct Tuning {
   std::int32_t iv_fast = 0;       // interval fast path + fixup list (-1 = bit-level replay only)
   std::int32_t iv_mid = 0;        // fixup: finite-case replay first (-1 = bit-level only)
   std::int32_t iv_partition = 0;  // univariate sign partition (-1 = off)
-  std::int32_t carry_powers = 0;  // sections: 1 = keep power tables live across sections
+  std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 8)
+  std::int32_t word_layout = 0;   // sections: -1 = all uniform-bound words first (no per-section blocks)
   std::uint64_t iv_partition_min = 0;  // smallest partitioned batch (default 65536)
 };
 

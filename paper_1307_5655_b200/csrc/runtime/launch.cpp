@@ -19,11 +19,13 @@ namespace polyeval::rt {
 namespace {
 // Driver entry points through the runtime (no libcuda link dependency).
 using KernelGetFunctionFn = CUresult (*)(CUfunction*, CUkernel);
+using OccupancyFn = CUresult (*)(int*, CUfunction, int, size_t);
 using LaunchKernelFn = CUresult (*)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                                     unsigned, unsigned, CUstream, void**, void**);
 struct Driver {
   KernelGetFunctionFn get_function = nullptr;
   LaunchKernelFn launch = nullptr;
+  OccupancyFn occupancy = nullptr;
   Driver() {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -34,6 +36,11 @@ struct Driver {
     if (cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess) {
       launch = reinterpret_cast<LaunchKernelFn>(p);
+    }
+    if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      occupancy = reinterpret_cast<OccupancyFn>(p);
     }
     cudaGetLastError();
   }
@@ -108,7 +115,8 @@ namespace {
 // Kernel argument values of one module, in entry_text's parameter order
 // (the parameter-tier coefficient array is appended by the caller).
 std::vector<std::uint64_t> arg_values(const Artifact& a, int device, const LaunchArgs& la,
-                                      std::uint64_t pidx, std::uint64_t pcnt) {
+                                      std::uint64_t pidx, std::uint64_t pcnt,
+                                      std::uint64_t scratch = 0) {
   const auto& img = a.image;
   std::uint64_t gcoef = 0;
   if (!img.global_words.empty()) gcoef = reinterpret_cast<std::uint64_t>(a.global_coefs.at(device));
@@ -131,6 +139,7 @@ std::vector<std::uint64_t> arg_values(const Artifact& a, int device, const Launc
     vals.push_back(pidx);
     vals.push_back(pcnt);
   }
+  if (img.sections > 1) vals.push_back(scratch);
   return vals;
 }
 
@@ -161,8 +170,46 @@ void keep_pool_memory(int device) {
 
 }  // namespace
 
+namespace {
+// Persistent sectioned kernel: one wave of CTAs (occupancy x SMs, at most
+// one per group of tiles) and its stream-ordered scratch slots.
+void launch_grouped(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
+  const auto& img = a.image;
+  const bool dev_ok = device >= 0 && device < Artifact::kMaxDevices;
+  void* fn = dev_ok ? a.fn[device] : nullptr;
+  int per_sm = 1;
+  if (fn && driver().occupancy) {
+    int k = 0;
+    if (driver().occupancy(&k, static_cast<CUfunction>(fn), static_cast<int>(img.block), 0) ==
+            CUDA_SUCCESS && k > 0) {
+      per_sm = k;
+    }
+  }
+  const std::uint64_t tile = static_cast<std::uint64_t>(img.block) * img.lanes;
+  const std::uint64_t tiles = (la.n + tile - 1) / tile;
+  const std::uint64_t groups = (tiles + img.group_tiles - 1) / img.group_tiles;
+  const std::uint64_t grid =
+      std::max<std::uint64_t>(1, std::min<std::uint64_t>(groups, static_cast<std::uint64_t>(per_sm) * sm_count(device)));
+  const size_t bytes = static_cast<size_t>(grid * img.group_tiles * img.scratch_values * tile * 8);
+  keep_pool_memory(device);
+  void* scratch = nullptr;
+  check_cuda(cudaMallocAsync(&scratch, bytes, stream), "cudaMallocAsync(section scratch)");
+  std::vector<std::uint64_t> vals =
+      arg_values(a, device, la, 0, 0, reinterpret_cast<std::uint64_t>(scratch));
+  std::vector<void*> args = arg_ptrs(a, vals);
+  launch_one(a.kernel, fn, dim3(static_cast<unsigned>(grid)), dim3(img.block), args.data(), stream,
+             "launch(sectioned walk)");
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  check_cuda(cudaFreeAsync(scratch, stream), "cudaFreeAsync(section scratch)");
+}
+}  // namespace
+
 void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
   const auto& img = a.image;
+  if (img.sections > 1) {
+    launch_grouped(a, device, la, stream);
+    return;
+  }
   if (img.interval_fast_path) {
     if (!la.list || !la.count) throw std::logic_error("interval fast path needs a fixup list");
     check_cuda(cudaMemsetAsync(reinterpret_cast<void*>(la.count), 0, sizeof(unsigned), stream),
@@ -323,8 +370,9 @@ void ensure_buffers(DeviceCtx& c, int slots, size_t arrays, size_t bytes, bool p
 class CopyPool {
  public:
   static CopyPool& get() {
-    static CopyPool pool;
-    return pool;
+    // never destroyed: its workers block on cv_ until the process ends
+    static CopyPool* pool = new CopyPool;
+    return *pool;
   }
   void copy(void* dst, const void* src, size_t bytes) {
     const size_t parts = std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, bytes >> 20));

@@ -2,7 +2,7 @@
 code-generation options, and the target process of ncu captures.
 
   python scripts/profile_one.py --config c4 --points 4000000 --reps 3 \
-      --tune section_ops=2000 --tune section_ops=3000,carry_powers=1
+      --tune section_ops=2000 --tune section_ops=3000,group_tiles=4
 
 Each --tune (comma-separated pe_tuning fields) compiles the program afresh
 and prints one JSON line {config, tune, ms (best of reps), points/s, sections}.

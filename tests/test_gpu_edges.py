@@ -204,12 +204,13 @@ def test_evaluate_many_matches_single_calls(cuda_device):
 
 
 @pytest.mark.parametrize("section_ops", [2**32 - 1, 1000, 400])
-@pytest.mark.parametrize("carry", [0, 1])
-def test_sectioned_wide_program_bit_identical(cuda_device, section_ops, carry):
-    # long walks run in barrier-separated sections (coordinates reloaded,
-    # powers rebuilt or carried); the op sequence is unchanged, so every
-    # section count gives the unsectioned kernel's bits — within the fused
-    # tolerance of the oracle, host or device buffers
+@pytest.mark.parametrize("tiles", [1, 3, 8])
+def test_sectioned_wide_program_bit_identical(cuda_device, section_ops, tiles):
+    # long walks run as a persistent sectioned kernel (groups of tiles per
+    # section pass, live values through scratch, coordinates reloaded, powers
+    # rebuilt); the op sequence is unchanged, so every section count and
+    # group size gives the unsectioned kernel's bits — within the fused
+    # tolerance of the oracle, host or device buffers, ragged batch
     rng = np.random.default_rng(4)
     ex = np.unique(rng.integers(0, 20, size=(3000, 3)), axis=0).astype(np.uint32)
     p = pe.Polynomial(ex, rng.normal(size=len(ex)), ("x", "y", "z"))
@@ -219,7 +220,7 @@ def test_sectioned_wide_program_bit_identical(cuda_device, section_ops, carry):
     one.set_tuning(section_ops=2**32 - 1)
     base = pe.Evaluator(pe.DoubleDomain(), one).evaluate([_t(a, cuda_device) for a in pts]).cpu().numpy()
     prog = pe.compile(p, sch)
-    prog.set_tuning(section_ops=section_ops, carry_powers=carry)
+    prog.set_tuning(section_ops=section_ops, group_tiles=tiles)
     if section_ops < 2**32 - 1:
         assert prog.f64_slices() > 1
     ref = pyoracle.Oracle(p, sch).eval_f64(pts)
