@@ -333,6 +333,7 @@ class Emitter {
       << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
       << " lanes=" << P_ << (*note ? " " : "") << note << "\n//\n";
     m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
+    if (n_smem_ > 0) m << ".shared .align 16 .b64 pe_scoef[" << n_smem_ << "];\n\n";
     if (n_const_ > 0) {
       m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
       for (std::uint32_t i = 0; i < n_const_; ++i) {
@@ -491,22 +492,36 @@ class Emitter {
         coef_lo_[k] = coef_hi_[k] = word(bits_of(c));
       }
     }
-    if (split) {
-      if (words_.size() & 1) words_.push_back(0);  // region starts on a pair
-      for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
-        if (!reg_bound_[k] || sec_of[k] != sec) continue;
-        coef_lo_[k] = coef_hi_[k] = static_cast<std::uint32_t>(words_.size());
-        words_.push_back(scalar_word(k));
-      }
-      if (words_.size() & 1) words_.push_back(0);  // next section starts on a pair
     }
+    if (words_.size() & 1) words_.push_back(0);  // region starts on a pair
+    const auto region1 = static_cast<std::uint32_t>(words_.size());
+    if (split) {
+      for (std::uint32_t sec = 0; sec < nsec; ++sec) {
+        for (std::size_t k = 0; k < s_.coefs.size(); ++k) {
+          if (!reg_bound_[k] || sec_of[k] != sec) continue;
+          coef_lo_[k] = coef_hi_[k] = static_cast<std::uint32_t>(words_.size());
+          words_.push_back(scalar_word(k));
+        }
+        if (words_.size() & 1) words_.push_back(0);  // next section starts on a pair
+      }
     }
     const auto n = static_cast<std::uint32_t>(words_.size());
-    n_const_ = std::min(n, CoefTiers::kConstCap);
-    // sectioned kernels address coefficients from a register (below); the
-    // parameter space cannot be, so their overflow goes to the global tier
-    n_param_ = cuts_.size() > 1 ? 0 : std::min(n - n_const_, CoefTiers::kParamCap);
-    n_global_ = n - n_const_ - n_param_;
+    if (cuts_.size() > 1) {
+      // Sectioned kernels: the section functions cannot read kernel
+      // parameters. The uniform-bound words take the constant bank; the
+      // register-bound ones (per-thread loads in any case) and any overflow
+      // go to shared memory, filled once per CTA of the persistent kernel
+      // (a global-memory tier here measured 30 % slower on C4: every word an
+      // L1 round trip); beyond that, global memory.
+      n_const_ = std::min(region1, CoefTiers::kConstCap);
+      n_param_ = 0;
+      n_smem_ = std::min(n - n_const_, CoefTiers::kSmemCap);
+    } else {
+      n_const_ = std::min(n, CoefTiers::kConstCap);
+      n_param_ = std::min(n - n_const_, CoefTiers::kParamCap);
+      n_smem_ = 0;
+    }
+    n_global_ = n - n_const_ - n_param_ - n_smem_;
   }
 
   // 64-bit word of scalar coefficient k as the kernel consumes it: the raw
@@ -568,12 +583,17 @@ class Emitter {
       const bool pair_const = w < n_const_ && (w & 1) == 0 && w + 1 < n_const_;
       const bool pair_param = w >= n_const_ && w < n_const_ + n_param_ && ((w - n_const_) & 1) == 0 &&
                               w + 1 < n_const_ + n_param_;
-      if (pair_const || pair_param) {
+      const bool pair_smem = w >= n_const_ && w < n_const_ + n_smem_ && ((w - n_const_) & 1) == 0 &&
+                             w + 1 < n_const_ + n_smem_;
+      if (pair_const || pair_param || pair_smem) {
         std::string r = "%c" + std::to_string(n_creg_++);
         std::string r2 = "%c" + std::to_string(n_creg_++);
         if (pair_const) {
           body_ << "  ld.const.v2." << ldty() << " {" << r << ", " << r2 << "}, [" << cbase() << "+"
                 << 8 * w << "];\n";
+        } else if (pair_smem) {
+          body_ << "  ld.shared.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_scoef+"
+                << 8 * (w - n_const_) << "];\n";
         } else {
           body_ << "  ld.param.v2." << ldty() << " {" << r << ", " << r2 << "}, [pe_pcoef+"
                 << 8 * (w - n_const_) << "];\n";
@@ -587,9 +607,11 @@ class Emitter {
       body_ << "  ld.const." << ldty() << " " << r << ", [" << cbase() << "+" << 8 * w << "];\n";
     } else if (w < n_const_ + n_param_) {
       body_ << "  ld.param." << ldty() << " " << r << ", [pe_pcoef+" << 8 * (w - n_const_) << "];\n";
+    } else if (w < n_const_ + n_smem_) {
+      body_ << "  ld.shared." << ldty() << " " << r << ", [pe_scoef+" << 8 * (w - n_const_) << "];\n";
     } else {
       body_ << "  ld.global.nc." << ldty() << " " << r << ", [%rd20+"
-            << 8 * (w - n_const_ - n_param_) << "];\n";
+            << 8 * (w - n_const_ - n_param_) << "];\n";  // (smem words lead the global array)
     }
     return r;
   }
@@ -888,7 +910,7 @@ class Emitter {
             << "  ld.param.u64 %rd3, [pe_n];\n  sub.u64 %rd12, %rd3, 1;\n"
             << "  ld.param.u64 %rd1, [pe_tbase];\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
             << "  ld.param.u64 %gsl, [pe_slot];\n  shl.b64 %rd14, %rd2, 3;\n  add.u64 %gsl, %gsl, %rd14;\n";
-      if (n_global_ > 0) {
+      if (n_smem_ + n_global_ > 0) {
         body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
       }
       for (std::uint32_t q = 0; q < P_; ++q) {
@@ -953,6 +975,17 @@ class Emitter {
           << "  mov.u32 %r4, %nctaid.x;\n  mul.wide.u32 %gstep, %r4, " << T << ";\n";
     for (std::size_t i = 0; i + 2 < fparams.size(); ++i) {
       body_ << "  ld.param.u64 %ka" << i << ", [" << fparams[i] << "];\n";
+    }
+    if (n_smem_ > 0) {
+      // shared-tier words: copied once per CTA from the head of the global
+      // coefficient array
+      body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n"
+            << "  mov.u32 %r5, %tid.x;\n  mov.u64 %rd18, pe_scoef;\n$Lsfill:\n"
+            << "  setp.ge.u32 %p3, %r5, " << n_smem_ << ";\n  @%p3 bra $Lsfilled;\n"
+            << "  mul.wide.u32 %rd15, %r5, 8;\n  add.u64 %rd16, %rd20, %rd15;\n"
+            << "  ld.global.nc.b64 %rd17, [%rd16];\n  add.u64 %rd16, %rd18, %rd15;\n"
+            << "  st.shared.b64 [%rd16], %rd17;\n  add.u32 %r5, %r5, %r2;\n  bra $Lsfill;\n"
+            << "$Lsfilled:\n  bar.sync 0;\n";
     }
     body_ << "$Lgroup:\n  setp.ge.u64 %gp, %gb, %gn;\n  @%gp bra.uni $Ldone;\n";
     for (std::size_t k = 0; k < cuts_.size(); ++k) {
@@ -1859,7 +1892,7 @@ class Emitter {
   std::unordered_map<std::uint32_t, std::string> pending_;  // second word of a loaded pair
   std::vector<char> reg_bound_;  // coefficient in the register-bound region
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
-  std::uint32_t n_const_ = 0, n_param_ = 0, n_global_ = 0;
+  std::uint32_t n_const_ = 0, n_param_ = 0, n_smem_ = 0, n_global_ = 0;
   std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0, n_tr_ = 0;
   std::uint64_t fp_ops_ = 0, int_ops_ = 0;
   std::ostringstream body_, decls_;

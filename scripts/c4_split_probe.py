@@ -35,7 +35,7 @@ def timed(fn, reps=3):
     return best
 
 
-for K in (1, 2, 4, 6, 8):
+for K in ([int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else (1, 2, 4, 6, 8)):
     evs = []
     for q in range(K):
         lo = xs[len(xs) * q // K]
