@@ -1,25 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the B200 batch polynomial evaluator (BASELINE.json metric).
 
-Default workload = BASELINE configs[1] (C2): dense univariate d1000 and d1023,
-fp64 coefficients U[-1,1], Estrin vs balanced, 1e7 points U[-1,1] per GPU.
-One step = the four (degree, scheme) programs each evaluated over the rank's
-1e7 points (4e7 point evaluations per GPU). Other configs: --config c1|c3|c4|c5.
+Default workload = BASELINE configs[3] (C4): trivariate sparse polynomial,
+10,000 distinct terms (exponents 0..50 per variable), N(0,1) coefficients,
+balanced scheme per variable, fp64, evaluated at 1e8 points U[-1,1]^3 — the
+largest configuration that fits one GPU and the one the 8-GPU scaling target
+is quoted on. One step = one evaluation of the whole 1e8-point batch.
+Other configs: --config c1|c2|c3|c5 (each at its stated batch size).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c4] [--impl reference]
 
-Under torchrun (N > 1) every rank evaluates its own 1e7-point shard of the
-N x 1e7 global batch (weak scaling, no data-path collective); timing is CUDA
-events on the launching stream bracketed by barrier + synchronize, max over
-ranks. `--impl reference` times the reference's own CPU implementation
-(oracle/_ref, the unmodified reference library through its Evaluator API, all
-host threads) on the same workload; rank 0 only.
+Scaling is STRONG: the config's global batch is split into N contiguous
+shards, one per rank (torchrun, NCCL for the barrier / max-reduction only; the
+data path has no collective). Timing: CUDA events on the launching stream,
+W untimed warm-up steps, K timed steps bracketed by barrier + synchronize,
+max over ranks; value = global batch points / (max rank time per step).
+L2 is flushed (256 MiB write) before every timed step.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref,
+the unmodified reference library through its Evaluator API, all host
+threads, one session per thread) on the same workload: rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import sys
 import threading
@@ -36,11 +43,11 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--points", type=int, default=0, help="override points per GPU")
+    ap.add_argument("--points", type=int, default=0, help="override the global batch size")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -64,6 +71,13 @@ def metric_info(cfg: str):
         "c4": "C4: trivariate sparse 10k terms N(0,1), balanced x3, 1e8 points U[-1,1]^3",
         "c5": "C5: Estrin d200 interval, 1e8 intervals [x, x+1e-6]",
     }[cfg]
+
+
+def shard(n_total: int, world: int, rank: int):
+    """Contiguous shard [lo, lo + n) of the global batch for `rank`."""
+    per = (n_total + world - 1) // world
+    lo = min(n_total, rank * per)
+    return lo, min(per, n_total - lo)
 
 
 # ----------------------------------------------------------------- clocks
@@ -122,18 +136,18 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- ncu
 
-# committed `ncu --set full` captures of the dominant kernels, taken with the
-# bench's own per-launch sizes (scripts/gpu_full_round.sh); a capture with
-# several rows (C4: the slice kernels of one evaluate call) is summed
+# committed `ncu --set full` captures of the dominant kernels, taken at the
+# bench's own per-launch sizes (scripts/ncu_captures.sh); a capture with
+# several rows (the launches of one evaluate call) is summed
 NCU_CAPTURES = {
+    ("c4", "C4_trivariate_sparse10k"): "profiles/r2_ncu_c4_raw.csv",
+    ("c5", "C5_interval_estrin_d200"): "profiles/r2_ncu_c5_raw.csv",
     ("c2", "C2_estrin_d1000"): "profiles/r1_ncu_c2_estrin_d1000_raw.csv",
     ("c2", "C2_balanced_d1000"): "profiles/r1_ncu_c2_balanced_d1000_raw.csv",
     ("c2", "C2_estrin_d1023"): "profiles/r1_ncu_c2_estrin_d1023_raw.csv",
     ("c2", "C2_balanced_d1023"): "profiles/r1_ncu_c2_balanced_d1023_raw.csv",
     ("c1", "C1_horner_d1000"): "profiles/r1_ncu_c1_raw.csv",
     ("c3", "C3_bivariate_td40_i64"): "profiles/r1_ncu_c3_raw.csv",
-    ("c4", "C4_trivariate_sparse10k"): "profiles/r1_ncu_c4_raw.csv",
-    ("c5", "C5_interval_estrin_d200"): "profiles/r1_ncu_c5_raw.csv",
 }
 
 
@@ -161,13 +175,13 @@ def ncu_traffic(cfg, program, points):
 
 # ----------------------------------------------------------------- dist
 
-def dist_setup(ngpus):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        import torch.distributed as dist
         import torch
+        import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
@@ -191,6 +205,23 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ----------------------------------------------------------------- CPU legs
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
 def cpu_kind():
     """("reference", host threads) when the unmodified reference library was
     built into oracle/_ref, else ("port", 1): the single-threaded C oracle."""
@@ -201,25 +232,27 @@ def cpu_kind():
     return "port", 1
 
 
-def cpu_reference_rate(wls, sample_points: int, threads: int, pts_cache=None):
+def _cpu_session(wl):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    if pyoracle.ref_available():
+        return pyoracle.Reference(wl.poly, wl.schemes)
+    orc = pyoracle.Oracle(wl.poly, wl.schemes)
+
+    class _Port:  # same call shape as Reference, threads ignored
+        eval_f64 = staticmethod(lambda pts, t: orc.eval_f64(pts))
+        eval_i64 = staticmethod(lambda pts, t: orc.eval_i64(pts))
+        eval_interval = staticmethod(lambda lo, hi, t: orc.eval_interval(lo, hi))
+    return _Port()
+
+
+def cpu_reference_rate(wls, sample_points: int, threads: int):
     """points/s of the unmodified reference (oracle/_ref) on `threads` host
     threads, one Evaluator session per thread over contiguous shards (or of
     the C oracle port when the reference library is absent)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    use_ref = pyoracle.ref_available()
     total_pts, total_s = 0, 0.0
     for wl in wls:
-        if use_ref:
-            ref = pyoracle.Reference(wl.poly, wl.schemes)
-        else:
-            orc = pyoracle.Oracle(wl.poly, wl.schemes)
-
-            class _Port:  # same call shape as Reference, threads ignored
-                eval_f64 = staticmethod(lambda pts, t: orc.eval_f64(pts))
-                eval_i64 = staticmethod(lambda pts, t: orc.eval_i64(pts))
-                eval_interval = staticmethod(lambda lo, hi, t: orc.eval_interval(lo, hi))
-            ref = _Port()
+        ref = _cpu_session(wl)
         if wl.domain == "interval":
             lo, hi = wl.points(sample_points)
             t = time.perf_counter()
@@ -238,17 +271,47 @@ def cpu_reference_rate(wls, sample_points: int, threads: int, pts_cache=None):
 
 
 def calibrate_sample(wls, threads, budget_s):
-    rate, _ = cpu_reference_rate(wls, 256 * threads, threads)
-    n = int(rate * budget_s / 1)  # total points over all programs
-    per = max(threads * 64, n // len(wls))
-    return per
+    rate, _ = cpu_reference_rate(wls, 64 * threads, threads)
+    n = int(rate * budget_s)  # total points over all programs
+    return max(threads * 16, n // len(wls))
 
 
-def host_threads() -> int:
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:  # noqa: BLE001
-        return os.cpu_count() or 1
+def cpu_parallel_rate(wl, workers: int, points: int = 100):
+    """The reference's intra-point threading (Evaluator::evaluate_parallel,
+    eval.hpp:97-140) on `points` points, `workers` threads: points/s."""
+    if wl.domain != "f64":
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    if not pyoracle.ref_available():
+        return None
+    ref = pyoracle.Reference(wl.poly, wl.schemes)
+    pts = wl.points(points)
+    t = time.perf_counter()
+    ref.eval_parallel_f64(pts, workers)
+    return points / (time.perf_counter() - t)
+
+
+def cpu_baseline(wls, seconds):
+    kind, threads = cpu_kind()
+    per = calibrate_sample(wls, threads, seconds)
+    rate, secs = cpu_reference_rate(wls, per, threads)
+    per1 = calibrate_sample(wls, 1, max(1.0, seconds / 6))
+    rate1, secs1 = cpu_reference_rate(wls, per1, 1)
+    par = cpu_parallel_rate(wls[0], threads)
+    return {
+        "value": rate, "unit": "points/s", "cores": threads, "kind": kind,
+        "cpu_model": cpu_model(),
+        "sample": f"{per} points per program x {len(wls)} programs ({secs:.1f} s), "
+                  + ("unmodified reference Evaluator<D>, one session per thread"
+                     if kind == "reference" else "C oracle port, 1 thread"),
+        "single_thread": {"value": rate1, "unit": "points/s",
+                          "sample": f"{per1} points per program ({secs1:.1f} s), 1 thread"},
+        "evaluate_parallel": ({"value": par, "unit": "points/s", "workers": threads,
+                               "sample": f"100 points of {wls[0].name}, reference "
+                                         "Evaluator::evaluate_parallel (intra-point threads)"}
+                              if par is not None else None),
+    }
 
 
 # ----------------------------------------------------------------- reference arm
@@ -274,14 +337,14 @@ def run_reference_arm(args, world, rank):
         "metric": "points/s", "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": {"c3": "int64", "c5": "f64-interval"}.get(args.config, "f64"),
         "data": "synthetic (seeded PCG64, explicit transforms)",
         "config": {"workload": metric_info(args.config), "programs": [w.name for w in wls],
                    "points_per_step": per_step * len(wls)},
         "term_evals_per_s": value * terms,
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads,
-                         "kind": kind,
+                         "kind": kind, "cpu_model": cpu_model(),
                          "sample": f"{per_step} points per program per step, {len(wls)} programs, "
                                    + ("unmodified reference Evaluator<D>, one session per thread"
                                       if kind == "reference" else "C oracle port, 1 thread")},
@@ -300,7 +363,8 @@ def run_native(args, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     wls = workloads(args.config)
-    n = args.points or wls[0].n_points
+    n_total = args.points or wls[0].n_points
+    lo_idx, n = shard(n_total, world, rank)
     domain = wls[0].domain
 
     # programs + kernels (compile is setup, outside the timed region)
@@ -315,22 +379,19 @@ def run_native(args, world, rank, local):
     else:
         evs = [pe.Evaluator(pe.DoubleDomain(), p, device=local) for p in progs]
 
-    # per-rank shard of the global batch: distinct seeded points per rank
+    # this rank's contiguous shard of the global batch (seeded per shard)
     if domain == "interval":
-        lo, hi = wls[0].points(n, offset_tag=7919 * rank)
-        x_lo = [torch.from_numpy(a).to(dev) for a in lo]
-        x_hi = [torch.from_numpy(a).to(dev) for a in hi]
-        host_in = ([torch.from_numpy(a).pin_memory() for a in lo],
-                   [torch.from_numpy(a).pin_memory() for a in hi])
-        inputs = (x_lo, x_hi)
+        lo, hi = wls[0].points(n, offset_tag=rank)
+        inputs = ([torch.from_numpy(a).to(dev) for a in lo], [torch.from_numpy(a).to(dev) for a in hi])
+        host_arrays = (lo, hi)
         outs = [(torch.empty(n, dtype=torch.float64, device=dev),
                  torch.empty(n, dtype=torch.float64, device=dev)) for _ in wls]
         bytes_in = 16 * n * wls[0].poly.nvars
         bytes_out = 16 * n
     else:
-        pts = wls[0].points(n, offset_tag=7919 * rank)
+        pts = wls[0].points(n, offset_tag=rank)
         inputs = [torch.from_numpy(a).to(dev) for a in pts]
-        host_in = [torch.from_numpy(a).pin_memory() for a in pts]
+        host_arrays = pts
         dt = torch.int64 if domain == "i64" else torch.float64
         outs = [torch.empty(n, dtype=dt, device=dev) for _ in wls]
         bytes_in = 8 * n * wls[0].poly.nvars
@@ -345,8 +406,6 @@ def run_native(args, world, rank, local):
     # FP64 / int64-MAD pipe peak on this GPU (roofline denominator)
     import ctypes as C
     from paper_1307_5655_b200 import _lib as L
-    # int64 programs run on the FP64 pipe when the 2^53 exactness proof holds
-    # for the data's range (C3: |x|,|y| <= 2); the denominator is the pipe used
     int_tier = "fp64-exact"
     if domain == "i64":
         _, b53 = progs[0].i64_bounds()
@@ -354,7 +413,7 @@ def run_native(args, world, rank, local):
         if not all(m <= b for m, b in zip(coord_max, b53)):
             int_tier = "int64-imad"
     peak, sms = C.c_double(), C.c_int32()
-    L.check(L.lib().pe_measure_peak(local, 1 if int_tier == "int64-imad" and domain == "i64" else 0,
+    L.check(L.lib().pe_measure_peak(local, 1 if int_tier == "int64-imad" else 0,
                                     C.byref(peak), C.byref(sms)))
     int_peak = C.c_double()
     if domain == "i64":
@@ -381,9 +440,8 @@ def run_native(args, world, rank, local):
     t_total = 0.0
     # The K steps are bracketed as a whole by barrier + synchronize; inside,
     # every step is enqueued back to back (L2 flush outside the step's event
-    # pair, then the evaluate calls), so while the GPU writes one step's
-    # 256 MiB flush the host enqueues the next step and no step's events
-    # include the GPU idling for the host.
+    # pair, then the evaluate calls), so no step's events include the GPU
+    # idling for the host.
     with ClockSampler(torch.cuda.current_device()) as clocks:
         barrier(world)
         torch.cuda.synchronize(dev)
@@ -407,7 +465,7 @@ def run_native(args, world, rank, local):
     launches = pe.launch_count() - launches0
     t_total = max_over_ranks(t_total, world)
     ms_step = t_total / args.steps
-    pts_step = n * len(wls) * world
+    pts_step = n_total * len(wls)  # the global batch, all ranks
     value = pts_step / (ms_step * 1e-3)
 
     # roofline of the dominant kernel (longest average launch)
@@ -430,10 +488,17 @@ def run_native(args, world, rank, local):
     nominal = sms.value * 64 * 1.965e9
     fp_pipe = domain != "i64" or int_tier == "fp64-exact"
     # FLOP accounting: a DFMA is 2 FLOP, an interval endpoint add/mul 1; the
-    # FP64 pipe issues one of either per lane per clock, so the peak FLOP
-    # rate is 2x (FMA code) or 1x (add/mul code) the measured DFMA rate
+    # FP64 pipe issues one of either per lane per clock
     flop_per_op = 1.0 if domain == "interval" else 2.0
     traffic, traffic_src = ncu_traffic(args.config, wls[top].name, n)
+    sections = progs[top].f64_slices() if domain == "f64" else 1
+    kernel_name = f"pe_walk_{domain} [{wls[top].name}]"
+    if domain == "f64" and sections > 1:
+        kernel_name = (f"pe_walk_f64 [{wls[top].name}]: one persistent kernel, {sections} sections "
+                       "(pe_section0..) over groups of 4 tiles")
+    if domain == "interval" and "pe_walk_interval_pos" in progs[top].ptx(pe.DOMAIN_INTERVAL):
+        kernel_name = (f"classify_intervals + pe_walk_interval_pos + pe_walk_interval_neg + "
+                       f"pe_walk_interval_fix [{wls[top].name}] (one evaluate call, sign-partitioned)")
     roofline = {
         "bound": "fp64" if fp_pipe else "int64_mad",
         "int64_tier": int_tier if domain == "i64" else None,
@@ -442,6 +507,7 @@ def run_native(args, world, rank, local):
         "peak": (peak.value * flop_per_op / 1e12) if fp_pipe else peak.value / 1e12,
         "unit": "TFLOP/s" if fp_pipe else "T int64-MAD/s",
         "frac": achieved / peak.value,
+        "frac_vs_nominal": achieved / nominal if fp_pipe else None,
         "achieved_pipe_ops_per_s": achieved, "peak_pipe_ops_per_s": peak.value,
         "peak_source": "measured live: pe_measure_peak microbenchmark (8 independent chains/thread, "
                        "full occupancy, immediate multiplier, best of 16 after 16 warm-up launches) "
@@ -449,10 +515,7 @@ def run_native(args, world, rank, local):
                        f"{nominal / 1e12:.1f} T DFMA/s at 1965 MHz x {sms.value} SMs x 64 lanes "
                        "(MEASURED_PEAKS.json has no FP64 entry)",
         "ops": f"{algo_per_pt} {unit_ops} per point (SURVEY 8d F) x {n} points per launch",
-        "kernel": (f"classify_intervals + pe_walk_interval_pos + pe_walk_interval_neg + "
-                   f"pe_walk_interval_fix [{wls[top].name}] (one evaluate call, sign-partitioned)"
-                   if domain == "interval" and "pe_walk_interval_pos" in progs[top].ptx(pe.DOMAIN_INTERVAL)
-                   else f"pe_walk_{domain} [{wls[top].name}]"),
+        "kernel": kernel_name,
         "issued_fp64_per_point": st["fp_ops"], "issued_int64_per_point": st["int_ops"],
         "hbm_frac": (bytes_in + bytes_out) / (avg[top] * 1e-3) / 1e9 /
                     json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else None,
@@ -461,58 +524,59 @@ def run_native(args, world, rank, local):
         "per_program_ms": {w.name: round(a, 4) for w, a in zip(wls, avg)},
     }
 
-    # e2e through the public API with HOST (pinned) buffers: H2D + walk + D2H
+    # e2e through the public API with HOST buffers: H2D + walk + D2H in the
+    # timed region, pinned (page-locked) and pageable (plain numpy) inputs
     e2e = None
     if not args.no_e2e:
-        if domain == "interval":
-            hout = [(torch.empty(n, dtype=torch.float64).pin_memory(),
-                     torch.empty(n, dtype=torch.float64).pin_memory()) for _ in wls]
-            hin = (tuple(a.numpy() for a in host_in[0]), tuple(a.numpy() for a in host_in[1]))
-        else:
-            dt = torch.int64 if domain == "i64" else torch.float64
-            hout = [torch.empty(n, dtype=dt).pin_memory() for _ in wls]
-            hin = [a.numpy() for a in host_in]
-
-        # several fp64 programs over the same points: one pe_eval_f64_multi
-        # call stages the points once (PCIe is the e2e limiter)
         multi = domain == "f64" and len(progs) > 1
 
-        def e2e_step():
+        def host_call(hin, hout):
             if multi:
-                pe.evaluate_many(progs, hin, outs=[o.numpy() for o in hout], device=local)
+                pe.evaluate_many(progs, hin, outs=hout, device=local)
                 return
             for e, o in zip(evs, hout):
-                if domain == "interval":
-                    e.evaluate(hin, out=(o[0].numpy(), o[1].numpy()))
-                else:
-                    e.evaluate(hin, out=o.numpy())
+                e.evaluate(hin, out=o)
 
-        e2e_step()
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(max(1, args.steps // 2)):
-            e2e_step()
-        el = time.perf_counter() - t0
-        el = max_over_ranks(el, world)
-        k = max(1, args.steps // 2)
-        e2e = {"value": pts_step / (el / k), "unit": "points/s",
-               "h2d_bytes_per_step": bytes_in * (1 if multi else len(wls)),
-               "d2h_bytes_per_step": bytes_out * len(wls),
+        def timed(hin, hout, steps):
+            host_call(hin, hout)
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                host_call(hin, hout)
+            el = max_over_ranks(time.perf_counter() - t0, world)
+            return pts_step / (el / steps)
+
+        k = max(1, args.steps // 4)
+        if domain == "interval":
+            pin_in = (tuple(torch.from_numpy(a).pin_memory().numpy() for a in host_arrays[0]),
+                      tuple(torch.from_numpy(a).pin_memory().numpy() for a in host_arrays[1]))
+            pin_out = [(torch.empty(n, dtype=torch.float64).pin_memory().numpy(),
+                        torch.empty(n, dtype=torch.float64).pin_memory().numpy()) for _ in wls]
+            pag_in = (tuple(np.array(a) for a in host_arrays[0]), tuple(np.array(a) for a in host_arrays[1]))
+            pag_out = [(np.empty(n), np.empty(n)) for _ in wls]
+        else:
+            dt = torch.int64 if domain == "i64" else torch.float64
+            pin_in = [torch.from_numpy(a).pin_memory().numpy() for a in host_arrays]
+            pin_out = [torch.empty(n, dtype=dt).pin_memory().numpy() for _ in wls]
+            pag_in = [np.array(a) for a in host_arrays]
+            pag_out = [np.empty(n, dtype=np.int64 if domain == "i64" else np.float64) for _ in wls]
+        v_pin = timed(pin_in, pin_out, k)
+        v_pag = timed(pag_in, pag_out, k)
+        e2e = {"value": v_pin, "unit": "points/s",
+               "h2d_bytes_per_step": bytes_in * (1 if multi else len(wls)) * world,
+               "d2h_bytes_per_step": bytes_out * len(wls) * world,
                "path": ("pe_eval_f64_multi" if multi else "pe_eval_*")
-                       + " with pinned host buffers (3-slot chunked H2D/walk/D2H pipeline)"}
+                       + " with page-locked host buffers (chunked H2D / walk / D2H pipeline)",
+               "pageable": {"value": v_pag, "unit": "points/s",
+                            "path": "same call with plain numpy (pageable) buffers: host threads "
+                                    "copy through page-locked staging slots"},
+               "steps": k}
 
     # CPU baseline: the unmodified reference on this box's host cores (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            kind, threads = cpu_kind()
-            per = calibrate_sample(wls, threads, args.cpu_seconds)
-            rate, secs = cpu_reference_rate(wls, per, threads)
-            cpu = {"value": rate, "unit": "points/s", "cores": threads, "kind": kind,
-                   "sample": f"{per} points per program x {len(wls)} programs "
-                             f"({secs:.1f} s), "
-                             + ("unmodified reference Evaluator<D> per thread"
-                                if kind == "reference" else "C oracle port, 1 thread")}
+            cpu = cpu_baseline(wls, args.cpu_seconds)
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "points/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -521,12 +585,13 @@ def run_native(args, world, rank, local):
     line = {
         "metric": "points/s", "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": {"c3": "int64", "c5": "f64-interval"}.get(args.config, "f64"),
         "data": "synthetic (seeded PCG64, explicit transforms; SURVEY 8d)",
         "config": {"workload": metric_info(args.config), "programs": [w.name for w in wls],
-                   "points_per_gpu": n, "point_evals_per_step": pts_step,
-                   "parallelism": f"points sharded, {world} rank(s), no collective",
+                   "global_batch": n_total, "points_per_rank": n, "point_evals_per_step": pts_step,
+                   "parallelism": f"global batch in {world} contiguous shard(s), one per rank, "
+                                  "no data-path collective",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "term_evals_per_s": value * terms,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -545,7 +610,7 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         run_reference_arm(args, world, rank)
         return
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
     try:
         run_native(args, world, rank, local)
     finally:

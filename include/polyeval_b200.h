@@ -196,7 +196,7 @@ typedef struct pe_tuning {
   int32_t iv_mid;          /* interval fixup: -1 = skip the finite-case replay */
   int32_t iv_partition;    /* univariate interval sign partition: -1 = off */
   uint32_t group_tiles;    /* sectioned kernels: tiles of points a CTA runs through one
-                              section before the next (default 8) */
+                              section before the next (default 4) */
   int32_t word_layout;     /* sections: -1 = one coefficient block for the whole walk
                               (default: one block per section) */
   int32_t reserved;

@@ -191,7 +191,7 @@ class Emitter {
         paired_(d != Domain::Interval && d != Domain::I64K), min_ctas_(shape.min_ctas),
         K_(d == Domain::I64K ? std::max<std::uint32_t>(1, shape.limbs) : 1),
         part_(shape.iv_partition), tuning_(t), cuts_(std::move(cuts)),
-        group_tiles_(t.group_tiles ? t.group_tiles : 8) {
+        group_tiles_(t.group_tiles ? t.group_tiles : 4) {
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
 
@@ -1869,7 +1869,7 @@ class Emitter {
   Tuning tuning_;
   std::vector<std::size_t> cuts_;  // section boundaries (op indices), ascending, ends with ops.size()
   std::uint32_t sec_ = 0;          // section being emitted
-  std::uint32_t group_tiles_ = 8;  // sectioned kernels: tiles per CTA per section pass
+  std::uint32_t group_tiles_ = 4;  // sectioned kernels: tiles per CTA per section pass
   std::string funcs_;              // sectioned kernels: the section functions
   std::string cbase() const { return "pe_coef"; }
   bool fast_ = false;  // emitting the interval fast path

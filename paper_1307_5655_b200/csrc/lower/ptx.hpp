@@ -90,7 +90,7 @@ struct Tuning {
   std::int32_t iv_fast = 0;       // interval fast path + fixup list (-1 = bit-level replay only)
   std::int32_t iv_mid = 0;        // fixup: finite-case replay first (-1 = bit-level only)
   std::int32_t iv_partition = 0;  // univariate sign partition (-1 = off)
-  std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 8)
+  std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 4)
   std::int32_t word_layout = 0;   // sections: -1 = all uniform-bound words first (no per-section blocks)
   std::uint64_t iv_partition_min = 0;  // smallest partitioned batch (default 65536)
 };

@@ -1,15 +1,22 @@
 #!/bin/bash
-# ncu --set full captures of every config's dominant kernel(s) at the bench's
-# own launch sizes (one GPU, after the same commands ran clean without ncu).
-O=gpurun_out/ncu
-mkdir -p $O
-python scripts/profile_one.py --config c1 --points 100000 --reps 2 > /dev/null && \
-ncu --set full --import-source on --clock-control none -k regex:pe_walk -s 1 -c 1 \
-  -o $O/ncu_c1 python scripts/profile_one.py --config c1 --points 100000 --reps 2 > $O/c1.log 2>&1
-python scripts/profile_one.py --config c4 --points 100000000 --reps 1 > /dev/null && \
-ncu --set full --import-source on --clock-control none -k regex:pe_walk -s 6 -c 6 \
-  -o $O/ncu_c4 python scripts/profile_one.py --config c4 --points 100000000 --reps 2 > $O/c4.log 2>&1
-python scripts/profile_one.py --config c5 --points 100000000 --reps 1 > /dev/null && \
-ncu --set full --import-source on --clock-control none -k regex:pe_walk_interval$ -s 1 -c 1 \
-  -o $O/ncu_c5 python scripts/profile_one.py --config c5 --points 100000000 --reps 2 > $O/c5.log 2>&1
+# Launch lists and `ncu --set full` captures of the bench's dominant kernels at
+# the bench's own launch sizes (one GPU; each command first runs clean
+# without ncu). Outputs under gpurun_out/ncu/; copy the summaries to profiles/.
+#   bash scripts/ncu_captures.sh [c4] [c5] ...
+O=gpurun_out/ncu; mkdir -p $O
+for c in "${@:-c4 c5}"; do
+  case $c in
+    c4) pts=100000000; k="regex:pe_walk" ;;
+    c5) pts=100000000; k="regex:pe_walk|classify" ;;
+    *) pts=10000000; k="regex:pe_walk" ;;
+  esac
+  python scripts/profile_one.py --config $c --points $pts --reps 1 > $O/${c}_plain.log 2>&1 || continue
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_${c}.csv \
+    python bench.py --config $c --steps 2 --warmup 3 --no-cpu --no-e2e > $O/${c}_launches.log 2>&1
+  ncu --set full --import-source on --clock-control none -k $k -s 1 -c 4 \
+    -o $O/ncu_${c} python scripts/profile_one.py --config $c --points $pts --reps 1 > $O/${c}_ncu.log 2>&1
+  ncu -i $O/ncu_${c}.ncu-rep --page raw --csv > $O/r2_ncu_${c}_raw.csv 2>/dev/null
+  ncu -i $O/ncu_${c}.ncu-rep --page details --csv > $O/r2_ncu_${c}_details.csv 2>/dev/null
+  echo $pts > $O/r2_ncu_${c}_points.txt
+done
 echo done > $O/DONE
