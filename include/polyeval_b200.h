@@ -317,7 +317,8 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
 
 /* Roofline denominator microbenchmark on `device`: kind 0 = DFMA/s
  * (FP64 FMA pipe), kind 1 = 64-bit integer multiply-adds/s, kind 2 = SM
- * cycles per dependent DFMA (latency). *sms receives the SM count.
+ * cycles per dependent DFMA (latency), kind 3 = FP64 FMAs/s through the
+ * tensor cores (mma.sync m8n8k4 f64). *sms receives the SM count.
  * Synchronous; for bench.py, not a hot-path call. */
 pe_status pe_measure_peak(int32_t device, int32_t kind, double* ops_per_s, int32_t* sms);
 

@@ -612,7 +612,7 @@ pe_status pe_program_compile_only(const pe_program* program, int32_t domain, uin
 
 pe_status pe_measure_peak(int32_t device, int32_t kind, double* ops_per_s, int32_t* sms) {
   return guarded([&]() -> pe_status {
-    if (!ops_per_s || kind < 0 || kind > 2) return fail(PE_EINVAL, "bad argument");
+    if (!ops_per_s || kind < 0 || kind > 3) return fail(PE_EINVAL, "bad argument");
     if (device >= 0) check_cuda(cudaSetDevice(device), "cudaSetDevice");
     int dev = 0, n_sm = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");

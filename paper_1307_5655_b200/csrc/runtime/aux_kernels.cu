@@ -136,6 +136,28 @@ __global__ void __launch_bounds__(256) imad64_peak_kernel(long long* out, int it
   if (s == 0x123456789LL) out[0] = s;
 }
 
+// FP64 tensor-core probe: mma.sync m8n8k4 f64
+// (DMMA), 8 independent accumulator tiles per warp; one instruction is 8 x 8
+// x 4 = 256 FMAs per warp (a DFMA: 32). Counted in FMAs, like the DFMA probe.
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters, double b) {
+  double c[8][2];
+  const double a = 0.99999904632568359375 + threadIdx.x * 1e-9;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k][0] = c[k][1] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c[k][0]), "+d"(c[k][1])
+                   : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+  if (s == 1234.5) out[0] = s;
+}
+
 // one warp, one dependent DFMA chain: SM cycles per DFMA (latency)
 __global__ void dfma_latency_kernel(double* out, long long* cycles, int iters, double a, double b) {
   double r = threadIdx.x * 1e-3;
@@ -182,6 +204,8 @@ extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s
     cudaEventRecord(t0);
     if (kind == 0) {
       dfma_peak_kernel<<<blocks, threads>>>(static_cast<double*>(buf), iters, 0.999999, 1e-7);
+    } else if (kind == 3) {
+      dmma_peak_kernel<<<blocks, threads>>>(static_cast<double*>(buf), iters / 8, 1e-7);
     } else {
       imad64_peak_kernel<<<blocks, threads>>>(static_cast<long long*>(buf), iters,
                                               0x5851F42D4C957F2DLL, 0x14057B7EF767814FLL);
@@ -196,7 +220,11 @@ extern "C" cudaError_t pe_measure_pipe_peak(int kind, int sms, double* ops_per_s
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   cudaFree(buf);
-  *ops_per_s = static_cast<double>(blocks) * threads * iters * 8 / (best_ms * 1e-3);
+  // FMAs per launch: DFMA / IMAD 8 chains x iters per thread; DMMA 8 tiles x
+  // iters/8 instructions x 256 FMAs per warp = 8 x iters x 8 per thread
+  *ops_per_s = kind == 3
+                   ? static_cast<double>(blocks) * (threads / 32) * (iters / 8) * 8 * 256 / (best_ms * 1e-3)
+                   : static_cast<double>(blocks) * threads * iters * 8 / (best_ms * 1e-3);
   return e;
 }
 

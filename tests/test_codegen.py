@@ -221,3 +221,24 @@ def test_list_scheduler_keeps_ops_and_words(name):
         assert _kernel_words(a) - {0} == _kernel_words(b) - {0}  # (section padding words)
     for op in ("fma.rn.f64", "mul.rn.f64", "add.rn.f64"):
         assert a.count(op) == b.count(op), op
+
+
+def test_cubin_cache_survives_corruption_and_concurrency(tmp_path, monkeypatch):
+    # the on-disk cubin cache: entries carry a length + checksum header and
+    # are published by rename from a per-writer temporary, so concurrent
+    # compiles of one PTX and a truncated entry both end in a valid cubin
+    from concurrent.futures import ThreadPoolExecutor
+    monkeypatch.setenv("PE_CACHE_DIR", str(tmp_path))
+    wl = W.c2(1000, "estrin")
+
+    def build(_):
+        return pe.compile(wl.poly, wl.schemes).compile_only(pe.DOMAIN_F64)
+
+    with ThreadPoolExecutor(4) as ex:
+        sizes = list(ex.map(build, range(4)))
+    assert len(set(sizes)) == 1 and sizes[0] > 0
+    files = [f for f in tmp_path.iterdir() if f.suffix == ".cubin"]
+    assert len(files) == 1 and not [f for f in tmp_path.iterdir() if ".tmp" in f.name]
+    files[0].write_bytes(files[0].read_bytes()[:100])  # truncated entry
+    assert build(0) == sizes[0]
+    assert files[0].stat().st_size > 1000  # rewritten
