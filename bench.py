@@ -398,7 +398,17 @@ def run_native(args, world, rank, local):
         bytes_out = 8 * n
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
-    for e, o in zip(evs, outs):  # JIT + load + first launch
+    for e, o in zip(evs, outs):  # first call: walk VM while the kernel compiles
+        e.evaluate(inputs, out=o, stream=sptr)
+    torch.cuda.synchronize(dev)
+    first_result_s = time.perf_counter() - t_setup
+    # wait for the specialised kernels (background compile) before timing
+    dom_codes = {"f64": [pe.DOMAIN_F64], "interval": [pe.DOMAIN_INTERVAL],
+                 "i64": [pe.DOMAIN_I64F, pe.DOMAIN_I64]}[domain]
+    for p in progs:
+        for dc in dom_codes:
+            p.compile_only(dc)
+    for e, o in zip(evs, outs):
         e.evaluate(inputs, out=o, stream=sptr)
     torch.cuda.synchronize(dev)
     setup_s = time.perf_counter() - t_setup
@@ -597,6 +607,10 @@ def run_native(args, world, rank, local):
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
         "setup_s": setup_s,
+        "first_result_s": first_result_s,
+        "setup_note": "first_result_s: compile + first evaluate of the shard (walk VM while the "
+                      "specialised kernel compiles in the background); setup_s: until the "
+                      "specialised kernel is compiled, loaded and has run once",
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

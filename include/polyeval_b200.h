@@ -199,7 +199,11 @@ typedef struct pe_tuning {
                               section before the next (default 4) */
   int32_t word_layout;     /* sections: -1 = one coefficient block for the whole walk
                               (default: one block per section) */
-  int32_t reserved;
+  int32_t jit_mode;        /* 0 (default): until a domain's specialised kernel is
+                              compiled (on a background thread, started by the first
+                              call), calls run the ahead-of-time walk-VM kernels;
+                              1: every call waits for the specialised kernel;
+                              2: walk VM only */
   uint64_t iv_partition_min; /* smallest batch that is sign-partitioned (default 65536) */
 } pe_tuning;
 
@@ -270,6 +274,10 @@ pe_status pe_program_compile_only(const pe_program* program, int32_t domain,
  * FP64 pipe (bound53, the faster tier). UINT64_MAX = unconstrained. */
 pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63,
                                 uint64_t* bound53);
+
+/* 1 when the specialised kernel of `domain` is compiled (calls then run it),
+ * 0 while calls would run the walk VM (pe_tuning.jit_mode). */
+pe_status pe_program_kernel_ready(const pe_program* program, int32_t domain, int32_t* ready);
 
 /* Barrier-separated sections of the fused fp64 kernel (long walks are cut
  * where few walk values are live; the op sequence is unchanged). */

@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     launch_count,
     limbs_to_int,
     scheme_from_name,
+    set_default_tuning,
     threshold_combine,
 )
 from ._lib import (  # noqa: F401

@@ -61,7 +61,7 @@ class pe_tuning(C.Structure):
         ("iv_partition", C.c_int32),
         ("group_tiles", C.c_uint32),
         ("word_layout", C.c_int32),
-        ("reserved", C.c_int32),
+        ("jit_mode", C.c_int32),
         ("iv_partition_min", C.c_uint64),
     ]
 
@@ -133,6 +133,7 @@ EXPORTS = [
     ("pe_program_i64_bounds", C.c_int,
      [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("pe_program_f64_slices", C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    ("pe_program_kernel_ready", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     ("pe_eval_f64", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.POINTER(pe_exec)]),
     ("pe_eval_f64_multi", C.c_int,

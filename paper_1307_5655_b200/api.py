@@ -154,6 +154,21 @@ class Polynomial:
 
 # ----------------------------------------------------------------- program
 
+_DEFAULT_TUNING: dict = {}
+
+
+def set_default_tuning(**options) -> None:
+    """pe_tuning fields applied to every program compiled afterwards in this
+    process (e.g. jit_mode=1: calls wait for the specialised kernel instead
+    of running the walk VM while it compiles). No arguments: defaults."""
+    names = {f for f, _ in L.pe_tuning._fields_}
+    for k in options:
+        if k not in names:
+            raise ValueError(f"unknown tuning option {k!r}")
+    _DEFAULT_TUNING.clear()
+    _DEFAULT_TUNING.update(options)
+
+
 class CompiledProgram:
     """Owns a native pe_program (immutable, shareable across threads)."""
 
@@ -173,6 +188,8 @@ class CompiledProgram:
             poly.nvars, descs, L.COEFF_I64 if self.integer else L.COEFF_F64, C.byref(h))
         L.check(st)
         self._h = h
+        if _DEFAULT_TUNING:
+            self.set_tuning(**_DEFAULT_TUNING)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -237,6 +254,8 @@ class CompiledProgram:
         self._nvars = nvars
         self.integer = bool(integer)
         self._h = h
+        if _DEFAULT_TUNING:
+            self.set_tuning(**_DEFAULT_TUNING)
         return self
 
     def limbs_needed(self, bounds) -> int:
@@ -310,7 +329,10 @@ class CompiledProgram:
 
     def set_tuning(self, **options) -> None:
         """Code-generation options (pe_tuning fields, e.g. lanes=2,
-        section_ops=4000, iv_fast=-1); drops the generated kernels."""
+        section_ops=4000, iv_fast=-1, jit_mode=1); drops the generated
+        kernels. Fields not given are the process defaults
+        (set_default_tuning), then the library's."""
+        options = {**_DEFAULT_TUNING, **options}
         t = L.pe_tuning()
         names = {f for f, _ in L.pe_tuning._fields_}
         for k, v in options.items():
@@ -318,6 +340,13 @@ class CompiledProgram:
                 raise ValueError(f"unknown tuning option {k!r}")
             setattr(t, k, int(v))
         L.check(L.lib().pe_program_set_tuning(self._h, C.byref(t)))
+
+    def kernel_ready(self, domain: int) -> bool:
+        """True once the specialised kernel of `domain` is compiled (until
+        then calls run the walk VM, pe_tuning.jit_mode 0)."""
+        r = C.c_int32()
+        L.check(L.lib().pe_program_kernel_ready(self._h, domain, C.byref(r)))
+        return bool(r.value)
 
     def compile_only(self, domain: int) -> int:
         nb = C.c_uint64()

@@ -457,6 +457,7 @@ pe_status pe_program_set_tuning(pe_program* program, const pe_tuning* t) {
     d.iv_partition = t->iv_partition;
     d.group_tiles = t->group_tiles;
     d.word_layout = t->word_layout;
+    d.jit_mode = t->jit_mode;
     d.iv_partition_min = t->iv_partition_min;
     return PE_OK;
   });
@@ -593,6 +594,15 @@ pe_status pe_program_i64_bounds(const pe_program* program, uint64_t* bound63, ui
   });
 }
 
+pe_status pe_program_kernel_ready(const pe_program* program, int32_t domain, int32_t* ready) {
+  return guarded([&]() -> pe_status {
+    if (!program || !ready) return fail(PE_EINVAL, "null argument");
+    const Artifact& a = program->impl.artifact(to_domain(domain), false);
+    *ready = a.cubin_ready.load(std::memory_order_acquire) ? 1 : 0;
+    return PE_OK;
+  });
+}
+
 pe_status pe_program_f64_slices(const pe_program* program, uint32_t* slices) {
   return guarded([&]() -> pe_status {
     if (!program || !slices) return fail(PE_EINVAL, "null argument");
@@ -679,7 +689,7 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
     const int dev = resolve_device(exec, out, &kind);
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
     const std::vector<const Artifact*> arts{
-        &p.loaded(strict ? lower::Domain::F64Strict : lower::Domain::F64, dev)};
+        &p.for_launch(strict ? lower::Domain::F64Strict : lower::Domain::F64, dev)};
     std::vector<const void*> ins(coords, coords + p.nvars);
     std::vector<void*> outs{out};
     LaunchArgs la;
@@ -720,7 +730,7 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
     std::vector<const Artifact*> arts;
     std::vector<size_t> base;
     for (size_t j = 0; j < k; ++j) {
-      arts.push_back(&programs[j]->impl.loaded(lower::Domain::F64, dev));
+      arts.push_back(&programs[j]->impl.for_launch(lower::Domain::F64, dev));
       base.push_back(j);
     }
     std::vector<const void*> ins(coords, coords + nv);
@@ -760,7 +770,7 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
     MemKind kind;
     const int dev = resolve_device(exec, out_lo, &kind);
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
-    const Artifact& a = p.loaded(lower::Domain::Interval, dev);
+    const Artifact& a = p.for_launch(lower::Domain::Interval, dev);
     cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     if (exec && exec->deferred_checks && kind == MemKind::Device) {
       // no host round trip: status accumulates on the stream, the fixup
@@ -921,7 +931,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
       const std::vector<std::uint64_t> b53 = caller_bounds ? bounds : p.i53_uniform_bound;
       const bool tier53 = !force_int && i64_proof_holds(p, b53.data(), 53);
       const Artifact& a =
-          p.loaded(tier53 ? lower::Domain::I64F : lower::Domain::I64, dev);
+          p.for_launch(tier53 ? lower::Domain::I64F : lower::Domain::I64, dev);
       StreamState& st = device_ctx(dev).state(s, 0);
       LaunchArgs la;
       la.flag = reinterpret_cast<std::uint64_t>(st.status);
@@ -934,7 +944,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
     // 3-IMAD 64-bit multiply-add). Same bits as the int64 kernel.
     const std::vector<std::uint64_t> b53 = caller_bounds ? bounds : p.i53_uniform_bound;
     if (!force_int && i64_proof_holds(p, b53.data(), 53)) {
-      const Artifact& af = p.loaded(lower::Domain::I64F, dev);
+      const Artifact& af = p.for_launch(lower::Domain::I64F, dev);
       Flag flag(s);
       LaunchArgs la;
       la.flag = reinterpret_cast<std::uint64_t>(flag.dev);
@@ -946,7 +956,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
       }
     }
     // Tier 2: int64 multiply-adds, wrap-free by the 2^63 proof.
-    const Artifact& a = p.loaded(lower::Domain::I64, dev);
+    const Artifact& a = p.for_launch(lower::Domain::I64, dev);
     for (int attempt = 0; attempt < 2; ++attempt) {
       Flag flag(s);
       LaunchArgs la;

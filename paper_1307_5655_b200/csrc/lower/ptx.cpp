@@ -94,20 +94,7 @@ std::string hex64(std::uint64_t u) {
   return buf;
 }
 
-/// Interval injection of a coefficient (reference numeric.cpp:17-26 for
-/// integers; fp64 coefficients are exact points).
-struct IvCoef {
-  double lo, hi;
-};
-IvCoef inject(double c) { return {c, c}; }
-IvCoef inject(std::int64_t c) {
-  const double d = static_cast<double>(c);  // round-to-nearest-even
-  const bool exact = d < 9223372036854775808.0 && d >= -9223372036854775808.0 &&
-                     static_cast<std::int64_t>(d) == c;
-  if (exact) return {d, d};
-  return {std::nextafter(d, -std::numeric_limits<double>::infinity()),
-          std::nextafter(d, std::numeric_limits<double>::infinity())};
-}
+using IvCoef = IntervalWord;
 
 // A Hörner-shaped run acc = fma(acc, B, c_j), j = 1..L, with one multiplier
 // B and scalar coefficients is emitted as a counted loop over a constant
@@ -536,15 +523,7 @@ class Emitter {
 
   // Interval value of coefficient k: injection, then the folded zero-add
   // steps (std::nextafter outward, as interval_add would apply them).
-  IvCoef ivcoef(std::size_t k) const {
-    IvCoef c = inject(s_.coefs[k]);
-    const std::uint32_t w = k < s_.widen.size() ? s_.widen[k] : 0;
-    for (std::uint32_t i = 0; i < w; ++i) {
-      c.lo = std::nextafter(c.lo, -std::numeric_limits<double>::infinity());
-      c.hi = std::nextafter(c.hi, std::numeric_limits<double>::infinity());
-    }
-    return c;
-  }
+  IvCoef ivcoef(std::size_t k) const { return interval_coefficient(s_, k); }
 
   // coefficient words / arithmetic registers
   // The fast interval path needs finite, nonzero, non-straddling coefficient

@@ -92,6 +92,7 @@ struct Tuning {
   std::int32_t iv_partition = 0;  // univariate sign partition (-1 = off)
   std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 4)
   std::int32_t word_layout = 0;   // sections: -1 = all uniform-bound words first (no per-section blocks)
+  std::int32_t jit_mode = 0;      // 0 walk VM until the kernel is compiled, 1 always wait, 2 VM only
   std::uint64_t iv_partition_min = 0;  // smallest partitioned batch (default 65536)
 };
 

@@ -3,7 +3,9 @@
 // power tables: powers.hpp:50-72.
 #include "lower/stream.hpp"
 
+#include <cmath>
 #include <cstdint>
+#include <limits>
 #include <map>
 #include <stdexcept>
 
@@ -247,6 +249,32 @@ bool mirror_stream(const Stream<C>& s, Stream<C>* out) {
   }
   return true;
 }
+
+namespace {
+IntervalWord inject(double c) { return {c, c}; }
+IntervalWord inject(std::int64_t c) {
+  const double d = static_cast<double>(c);  // round-to-nearest-even
+  const bool exact = d < 9223372036854775808.0 && d >= -9223372036854775808.0 &&
+                     static_cast<std::int64_t>(d) == c;
+  if (exact) return {d, d};
+  return {std::nextafter(d, -std::numeric_limits<double>::infinity()),
+          std::nextafter(d, std::numeric_limits<double>::infinity())};
+}
+}  // namespace
+
+template <typename C>
+IntervalWord interval_coefficient(const Stream<C>& s, std::size_t k) {
+  IntervalWord c = inject(s.coefs[k]);
+  const std::uint32_t w = k < s.widen.size() ? s.widen[k] : 0;
+  for (std::uint32_t i = 0; i < w; ++i) {
+    c.lo = std::nextafter(c.lo, -std::numeric_limits<double>::infinity());
+    c.hi = std::nextafter(c.hi, std::numeric_limits<double>::infinity());
+  }
+  return c;
+}
+
+template IntervalWord interval_coefficient(const Stream<double>&, std::size_t);
+template IntervalWord interval_coefficient(const Stream<std::int64_t>&, std::size_t);
 
 template bool mirror_stream(const Stream<double>&, Stream<double>*);
 template bool mirror_stream(const Stream<std::int64_t>&, Stream<std::int64_t>*);

@@ -106,6 +106,15 @@ Stream<C> lower_fused(const front::FlatProgram<C>& program);
 template <typename C>
 bool mirror_stream(const Stream<C>& s, Stream<C>* out);
 
+/// Interval value of coefficient k of a strict stream: the reference
+/// injection (numeric.cpp:17-26: exact -> [c, c], else one ulp outward)
+/// followed by the folded zero-add steps (one std::nextafter outward each).
+struct IntervalWord {
+  double lo, hi;
+};
+template <typename C>
+IntervalWord interval_coefficient(const Stream<C>& s, std::size_t k);
+
 /// Stable 64-bit FNV-1a over arbitrary bytes (cache keys, stream hashes).
 inline std::uint64_t fnv1a(const void* data, std::size_t n,
                            std::uint64_t h = 1469598103934665603ull) {

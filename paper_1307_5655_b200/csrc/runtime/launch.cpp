@@ -104,6 +104,13 @@ int sm_count(int device) {
   return n;
 }
 
+extern "C" cudaError_t pe_launch_vm(int domain, const std::uint32_t* code, std::uint32_t nops,
+                                    std::uint32_t nslots, std::uint32_t result,
+                                    const std::uint64_t* lo, const std::uint64_t* hi,
+                                    std::uint32_t nvars, const void* const* in, void* out0,
+                                    void* out1, unsigned long long n, unsigned* flag,
+                                    const unsigned long long* bounds, cudaStream_t stream);
+
 extern "C" cudaError_t pe_launch_classify_intervals(const double* lo, const double* hi,
                                                     unsigned long long n, unsigned* idx,
                                                     unsigned* counts, unsigned* fix_list,
@@ -206,6 +213,24 @@ void launch_grouped(const Artifact& a, int device, const LaunchArgs& la, cudaStr
 
 void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream) {
   const auto& img = a.image;
+  if (a.vm) {
+    const lower::VmProgram& p = a.vm->prog;
+    const VmDevice& dv = a.vm->dev.at(device);
+    std::vector<const void*> in;
+    for (auto v : la.ins) in.push_back(reinterpret_cast<const void*>(v));
+    check_cuda(pe_launch_vm(static_cast<int>(p.domain), static_cast<const std::uint32_t*>(dv.code),
+                            p.nops, p.nslots, p.result, static_cast<const std::uint64_t*>(dv.lo),
+                            static_cast<const std::uint64_t*>(dv.hi), p.nvars, in.data(),
+                            reinterpret_cast<void*>(la.outs.at(0)),
+                            la.outs.size() > 1 ? reinterpret_cast<void*>(la.outs[1]) : nullptr, la.n,
+                            reinterpret_cast<unsigned*>(la.flag),
+                            la.bounds.empty() ? nullptr
+                                              : reinterpret_cast<const unsigned long long*>(la.bounds.data()),
+                            stream),
+               "launch(walk VM)");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    return;
+  }
   if (img.sections > 1) {
     launch_grouped(a, device, la, stream);
     return;

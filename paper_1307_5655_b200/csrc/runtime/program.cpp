@@ -126,7 +126,7 @@ void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, const
 }  // namespace
 
 Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
-  std::lock_guard<std::mutex> lock(mu);
+  std::unique_lock<std::mutex> lock(mu);
   auto& slot = artifacts[static_cast<int>(d)];
   if (!slot) {
     auto a = std::make_unique<Artifact>();
@@ -151,19 +151,97 @@ Artifact& Program::artifact(lower::Domain d, bool need_cubin) const {
     }
     slot = std::move(a);
   }
-  if (need_cubin && slot->cubin.empty()) {
-    CompileResult r = compile_ptx_cached(slot->image.ptx, slot->image.entry);
-    if (!r.ok) throw std::logic_error(r.log);
-    slot->cubin = std::move(r.cubin);
-    slot->compile_seconds = r.seconds;
+  Artifact& a = *slot;
+  lock.unlock();  // ptxas runs outside the program lock
+  if (need_cubin) {
+    // once per artifact: a second caller (e.g. a blocking call while the
+    // background compile runs) waits for the first
+    std::call_once(a.compiled, [&a] {
+      CompileResult r = compile_ptx_cached(a.image.ptx, a.image.entry);
+      if (!r.ok) throw std::logic_error(r.log);
+      std::vector<char> mirror_cubin;
+      if (a.mirror) {
+        CompileResult m = compile_ptx_cached(a.mirror->image.ptx, a.mirror->image.entry);
+        if (!m.ok) throw std::logic_error(m.log);
+        a.mirror->cubin = std::move(m.cubin);
+        a.mirror->compile_seconds = m.seconds;
+      }
+      a.cubin = std::move(r.cubin);
+      a.compile_seconds = r.seconds;
+      a.cubin_ready.store(true, std::memory_order_release);
+    });
   }
-  if (need_cubin && slot->mirror && slot->mirror->cubin.empty()) {
-    CompileResult r = compile_ptx_cached(slot->mirror->image.ptx, slot->mirror->image.entry);
-    if (!r.ok) throw std::logic_error(r.log);
-    slot->mirror->cubin = std::move(r.cubin);
-    slot->mirror->compile_seconds = r.seconds;
+  return a;
+}
+
+const Artifact& Program::for_launch(lower::Domain d, int device) const {
+  if (tuning.jit_mode == 1) return loaded(d, device);
+  if (tuning.jit_mode == 2) {
+    if (Artifact* v = loaded_vm(d, device)) return *v;
+    throw std::invalid_argument("program too large for the walk VM (jit_mode 2)");
   }
-  return *slot;
+  Artifact& a = artifact(d, false);
+  if (a.cubin_ready.load(std::memory_order_acquire)) return loaded(d, device);
+  {
+    // first use: compile in the background, answer this call with the VM
+    std::lock_guard<std::mutex> lock(mu);
+    const int k = static_cast<int>(d);
+    if (!(jit_started >> k & 1u)) {
+      jit_started |= 1u << k;
+      jit_threads.emplace_back([this, d] {
+        try {
+          artifact(d, true);
+        } catch (...) {
+          // a failing compile resurfaces (and throws) on the next blocking use
+        }
+      });
+    }
+  }
+  if (Artifact* v = loaded_vm(d, device)) return *v;
+  return loaded(d, device);  // beyond the VM's slot file: wait for the compile
+}
+
+Artifact* Program::loaded_vm(lower::Domain d, int device) const {
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = vm_arts[static_cast<int>(d)];
+  if (!slot) {
+    const bool strict = d == lower::Domain::F64Strict || d == lower::Domain::Interval;
+    if (!integer && (d == lower::Domain::I64 || d == lower::Domain::I64F)) {
+      throw std::invalid_argument("pe_eval_i64 needs a program with int64 coefficients");
+    }
+    auto a = std::make_unique<Artifact>();
+    a->vm = std::make_unique<VmImage>();
+    a->vm->prog = integer ? lower::build_vm(strict ? lower::lower_strict(i->flat)
+                                                   : lower::lower_fused(i->flat), d)
+                          : lower::build_vm(strict ? lower::lower_strict(f->flat)
+                                                   : lower::lower_fused(f->flat), d);
+    const bool iv = d == lower::Domain::Interval;
+    const bool i64 = d == lower::Domain::I64 || d == lower::Domain::I64F;
+    a->image.domain = d;
+    a->image.nvars = nvars;
+    a->image.n_in = iv ? 2 * nvars : nvars;
+    a->image.n_out = iv ? 2 : 1;
+    a->image.has_flag = iv || i64;
+    a->image.has_bounds = i64;
+    a->image.entry = std::string("pe_vm_") + lower::domain_name(d);
+    slot = std::move(a);
+  }
+  Artifact& a = *slot;
+  if (a.vm->prog.nslots > pe_vm_max_slots()) return nullptr;
+  auto it = a.vm->dev.find(device);
+  if (it == a.vm->dev.end()) {
+    const lower::VmProgram& p = a.vm->prog;
+    VmDevice dv;
+    auto upload = [](void** dst, const void* src, size_t bytes, const char* what) {
+      check_cuda(cudaMalloc(dst, std::max<size_t>(bytes, 8)), what);
+      if (bytes) check_cuda(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), what);
+    };
+    upload(&dv.code, p.code.data(), p.code.size() * 4, "VM program upload");
+    upload(&dv.lo, p.lo.data(), p.lo.size() * 8, "VM coefficient upload");
+    if (!p.hi.empty()) upload(&dv.hi, p.hi.data(), p.hi.size() * 8, "VM coefficient upload");
+    a.vm->dev[device] = dv;
+  }
+  return &a;
 }
 
 namespace {
@@ -236,13 +314,29 @@ Artifact::~Artifact() {
   for (auto& [dev, ptr] : global_coefs) {
     if (cudaSetDevice(dev) == cudaSuccess) cudaFree(ptr);
   }
+  if (vm) {
+    for (auto& [dev, dv] : vm->dev) {
+      if (cudaSetDevice(dev) != cudaSuccess) continue;
+      cudaFree(dv.code);
+      cudaFree(dv.lo);
+      if (dv.hi) cudaFree(dv.hi);
+    }
+  }
   if (library) cudaLibraryUnload(library);
 }
 
 void Program::release() const {
+  std::vector<std::thread> jobs;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    jobs.swap(jit_threads);
+  }
+  for (auto& t : jobs) t.join();
   std::lock_guard<std::mutex> lock(mu);
   for (auto& a : artifacts) a.reset();
+  for (auto& a : vm_arts) a.reset();
   limb_arts.clear();
+  jit_started = 0;
 }
 
 namespace {

@@ -13,11 +13,17 @@
 #include <string>
 #include <vector>
 
+#include <atomic>
+#include <thread>
+
 #include "front/flat.hpp"
 #include "front/forest.hpp"
 #include "front/split.hpp"
 #include "front/terms.hpp"
 #include "lower/ptx.hpp"
+#include "lower/vm.hpp"
+
+extern "C" unsigned pe_vm_max_slots(void);
 
 namespace polyeval::rt {
 
@@ -27,8 +33,24 @@ struct CudaError : std::runtime_error {
 
 void check_cuda(cudaError_t e, const char* what);
 
-/// One specialised kernel: generated PTX, its cubin, and the loaded handle.
+/// Device copies of a walk-VM program (op list + coefficient words).
+struct VmDevice {
+  void* code = nullptr;
+  void* lo = nullptr;
+  void* hi = nullptr;
+};
+struct VmImage {
+  lower::VmProgram prog;
+  std::map<int, VmDevice> dev;
+};
+
+/// One specialised kernel: generated PTX, its cubin, and the loaded handle
+/// — or (vm set) the walk-VM form of the same stream for the AOT
+/// interpreter kernels.
 struct Artifact {
+  std::unique_ptr<VmImage> vm;
+  std::once_flag compiled;          // the cubin is built once (possibly in the background)
+  std::atomic<bool> cubin_ready{false};
   lower::KernelImage image;
   std::vector<char> cubin;
   double compile_seconds = 0.0;
@@ -92,17 +114,29 @@ struct Program {
 
   mutable std::mutex mu;
   mutable std::array<std::unique_ptr<Artifact>, 5> artifacts;
+  mutable std::array<std::unique_ptr<Artifact>, 5> vm_arts;  // walk-VM forms
+  mutable std::vector<std::thread> jit_threads;              // background compiles
+  mutable std::uint32_t jit_started = 0;                     // bit per domain
   mutable std::map<std::uint32_t, std::unique_ptr<Artifact>> limb_arts;  // I64K by limb count
 
-  /// Generated (and compiled) artifact for a domain; thread-safe.
+  /// Generated (and compiled) artifact for a domain; thread-safe. With
+  /// need_cubin it waits for a background compile of the same artifact.
   Artifact& artifact(lower::Domain d, bool need_cubin) const;
+  /// The kernel a call launches on `device` (tuning.jit_mode): the
+  /// specialised kernel once compiled; before that (default) the walk VM,
+  /// while the specialised kernel compiles on a background thread.
+  const Artifact& for_launch(lower::Domain d, int device) const;
+  /// Walk-VM artifact for a domain, uploaded to `device`; null when the
+  /// program's slot file exceeds the VM kernels'.
+  Artifact* loaded_vm(lower::Domain d, int device) const;
   /// Loaded kernel handle + global-tier coefficients on `device`.
   Artifact& loaded(lower::Domain d, int device) const;
   /// K-limb exact integer kernel (Domain::I64K): generated (+ compiled), or
   /// loaded on `device`.
   Artifact& limb_artifact(std::uint32_t limbs, bool need_cubin) const;
   Artifact& loaded_limbs(std::uint32_t limbs, int device) const;
-  /// Unloads every kernel library and frees the device coefficient copies.
+  /// Joins background compiles, unloads every kernel library and frees the
+  /// device copies.
   void release() const;
   ~Program() { release(); }
 };

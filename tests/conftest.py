@@ -23,3 +23,11 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.fail("gpu test requires CUDA (no silent CPU fallback)")
     return torch.device("cuda:0")
+
+
+def pytest_sessionstart(session):
+    # The parity tests exercise the specialised kernels: every call waits for
+    # its kernel's compile. tests/test_gpu_vm.py covers the walk VM (the
+    # default for a program's first calls) and the switch-over explicitly.
+    import paper_1307_5655_b200 as pe
+    pe.set_default_tuning(jit_mode=1)
