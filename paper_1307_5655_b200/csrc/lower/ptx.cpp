@@ -245,7 +245,7 @@ class Emitter {
     img.sections = static_cast<std::uint32_t>(std::max<std::size_t>(1, cuts_.size()));
     const std::string main_entry = entry_text(img, img.entry, 0, min_ctas_);
 
-    // fixup entry: exact replay of the listed points, one per thread
+    // fixup entry: exact replay of the listed points
     std::string fix_entry;
     if (fast) {
       img.fix_entry = img.entry + "_fix";
@@ -254,7 +254,20 @@ class Emitter {
       sync_every_ = 0;  // threads past the list length leave at once
       reset_entry();
       fix_ = true;
-      emit_fix_prologue();
+      // Persistent when the coefficients are all in the constant bank (a
+      // function cannot read kernel parameters): a grid of a few CTAs per SM
+      // strides over the list and calls the replay as a non-inlined
+      // function per point — inside a loop ptxas would hoist the replay's
+      // coefficient loads out and spill them. The list is sized for the
+      // whole batch, so one thread per slot would launch n/128 CTAs that
+      // mostly exit at once (C5: 0.59 ms of 12.2 per 1e8 intervals).
+      const bool persistent = n_param_ == 0;
+      img.fix_persistent = persistent;
+      if (persistent) {
+        emit_fix_function_prologue();
+      } else {
+        emit_fix_prologue();
+      }
       if (tuning_.iv_mid >= 0) {
         // finite-case replay first; the bit-level replay only on %pmid
         decls_ << "  .reg .pred %pmid;\n  .reg .f64 %macc;\n";
@@ -275,17 +288,21 @@ class Emitter {
       emit_powers();
       emit_walk();
       emit_store();
-      // one listed point per thread, no grid-stride loop: a loop would let
-      // ptxas hoist every coefficient load out of it and spill them
       body_ << "$Lnextpt:\n";
       finish_entry();
       fix_ = false;
       // 128-thread CTAs, .minnctapersm 6 (<= 80 registers, no spills for
-      // C5): the replay is latency-bound, so every listed point gets its own
-      // thread and occupancy helps (C5 fixup per 1e8: 612 -> 590 us at 6,
-      // 584 us at 8 but with spills; profiles/r1_c5_fix_shape.txt).
+      // C5): the replay is latency-bound, so occupancy helps (C5 fixup per
+      // 1e8: 612 -> 590 us at 6, 584 us at 8 but with spills;
+      // profiles/r1_c5_fix_shape.txt).
       img.fix_block = 128;
       img.fix_ctas_per_sm = 6;
+      if (persistent) {
+        funcs_ += fix_function_text();
+        reset_entry();
+        emit_fix_loop();
+        finish_entry();
+      }
       fix_entry = entry_text(img, img.fix_entry, img.fix_block, img.fix_ctas_per_sm);
       P_ = lanes;
       sync_every_ = sync;
@@ -1540,28 +1557,28 @@ class Emitter {
   //    accumulator. Zero endpoints either give the same value as the zero
   //    rule or a zero that the next step flags; NaN/inf always reach one of
   //    the two products ({A1,A2} and {B1,B2} are both endpoint pairs).
+  // nextafter of a value whose sign is unknown statically: RD(v - dmin) /
+  // RU(v + dmin), dmin the smallest subnormal. For every finite v the exact
+  // difference lies strictly between v and its neighbour on that side, or is
+  // the neighbour itself (subnormal v), so directed rounding lands on
+  // std::nextafter — zero included (-> -dmin / +dmin). Two cases differ:
+  //  * +-inf: RD(+inf - dmin) stays +inf (std: DBL_MAX) — an infinite
+  //    endpoint never turns finite on the fast path (a product with it is
+  //    inf or NaN, a sum inf or NaN), so the final finiteness test sends
+  //    the point to the exact replay;
+  //  * v = +dmin down gives -0 (std: +0), v = -dmin up gives +0 (std: -0).
+  //    A zero endpoint's sign is washed out by the next step (+-0 -/+ dmin
+  //    is the same), by a product (the zero rule / a zero product is then
+  //    stepped) and by a sum with a nonzero value; it is visible only as a
+  //    result endpoint or, as the upper endpoint of a non-positive interval,
+  //    through the straddle test (which flags it). Result endpoints equal
+  //    to zero are flagged (emit_fast_exit).
+  // One FP64 add per step, no "did not move" test (the former FMA-based
+  // step needed an integer compare per step: 532 of C5's ~1350 ALU ops per
+  // interval).
   void fnext(const std::string& dst, const std::string& src, bool up) {
-    // FP64-pipe nextafter: RN(v +- |v| * phi), phi = 2^-53 (1 + 2^-52).
-    // For a finite normal v the exact increment is strictly between 1/2 and
-    // 3/2 of the spacing on its side, so RN lands on the neighbour (also
-    // across binades and into the subnormal range, and DBL_MAX up gives +inf).
-    // For 0 and subnormals it returns v unchanged — caught by the "did not
-    // move" test, OR-accumulated into 4 rotating predicates so the checks do
-    // not form one serial chain; inf gives NaN, caught at the end. The test
-    // is a 32-bit compare of the low words on the ALU pipe (a step of one ulp
-    // changes the bit pattern by +-1, so the low words differ iff the value
-    // moved; C5 per 1e7: 1.56 ms vs 1.88 with an FP64 compare,
-    // profiles/r1_c5_check_modes.txt).
-    const std::string a = tmp_f();
-    body_ << "  abs.f64 " << a << ", " << src << ";\n";
-    if (!up) body_ << "  neg.f64 " << a << ", " << a << ";\n";
-    body_ << "  fma.rn.f64 " << dst << ", " << a << ", 0d3CA0000000000001, " << src << ";\n";
-    const std::string l0 = tmp_r(), h0 = tmp_r(), l1 = tmp_r(), h1 = tmp_r();
-    body_ << "  mov.b64 {" << l0 << ", " << h0 << "}, " << dst << ";\n"
-          << "  mov.b64 {" << l1 << ", " << h1 << "}, " << src << ";\n"
-          << "  setp.eq.or.b32 %pb" << (nb_ & 3) << ", " << l0 << ", " << l1 << ", %pb"
-          << (nb_ & 3) << ";\n";
-    ++nb_;
+    body_ << "  " << (up ? "add.rp" : "sub.rm") << ".f64 " << dst << ", " << src
+          << ", 0d0000000000000001;\n";
   }
 
   // nextafter of a value whose sign is known statically (sign != 0): the
@@ -1737,6 +1754,12 @@ class Emitter {
     for (std::uint32_t k = 0; k < P_; ++k) {
       fcheck_finite(reg(s_.result.id, k, false));
       fcheck_finite(reg(s_.result.id, k, true));
+      // a zero result endpoint may carry the wrong sign (fnext)
+      for (bool hi : {false, true}) {
+        body_ << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << reg(s_.result.id, k, hi)
+              << ", 0d0000000000000000, %pb" << (nb_ & 3) << ";\n";
+        ++nb_;
+      }
     }
     // special: append the thread's valid point indices to the fixup list
     body_ << "  setp.lt.s64 %pslow, %facc, 0;\n"
@@ -1790,6 +1813,69 @@ class Emitter {
             << "  add.u64 %rd6, %rd5, %ix0;\n  ld.global.nc.f64 " << xr(i / 2, 0, i % 2 == 1)
             << ", [%rd6];\n";
     }
+  }
+
+  // Persistent fixup: the replay of one listed point as a function of the
+  // point index (and the coordinate / result pointers, passed through from
+  // the kernel's parameters of the same names).
+  std::vector<std::string> fix_params() const {
+    std::vector<std::string> ps;
+    for (std::uint32_t i = 0; i < 2 * s_.nvars; ++i) ps.push_back("pe_in" + std::to_string(i));
+    ps.push_back("pe_out0");
+    ps.push_back("pe_out1");
+    ps.push_back("pe_gcoef");
+    ps.push_back("pe_pt");
+    return ps;
+  }
+  void emit_fix_function_prologue() {
+    if (n_global_ > 0) {
+      body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n";
+    }
+    decls_ << "  .reg .b64 %ix<1>;\n  .reg .pred %pv<1>;\n";
+    for (std::uint32_t v = 0; v < s_.nvars; ++v) {
+      decls_ << "  .reg .f64 " << xr(v, 0, false) << ", " << xr(v, 0, true) << ";\n";
+    }
+    body_ << "  ld.param.u64 %rd13, [pe_pt];\n  shl.b64 %ix0, %rd13, 3;\n"
+          << "  setp.eq.u64 %pv0, %rd13, %rd13;\n";
+    for (std::uint32_t i = 0; i < 2 * s_.nvars; ++i) {
+      body_ << "  ld.param.u64 %rd5, [pe_in" << i << "];\n  cvta.to.global.u64 %rd5, %rd5;\n"
+            << "  add.u64 %rd6, %rd5, %ix0;\n  ld.global.nc.f64 " << xr(i / 2, 0, i % 2 == 1)
+            << ", [%rd6];\n";
+    }
+  }
+  std::string fix_function_text() const {
+    std::ostringstream f;
+    const auto ps = fix_params();
+    f << ".func pe_fix_point(";
+    for (std::size_t i = 0; i < ps.size(); ++i) f << (i ? ",\n  " : "\n  ") << ".param .u64 " << ps[i];
+    f << ")\n{\n  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n" << decls_.str()
+      << body_.str() << "}\n\n";
+    return f.str();
+  }
+  // the kernel: slot = global thread index, strided by the grid, while
+  // slot < min(count, cap)
+  void emit_fix_loop() {
+    const auto ps = fix_params();
+    decls_ << "  .reg .b64 %fk<" << ps.size() << ">;\n";
+    body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
+          << "  mul.wide.u32 %rd1, %r1, %r2;\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd1, %rd1, %rd2;\n"
+          << "  mov.u32 %r4, %nctaid.x;\n  mul.wide.u32 %rd4, %r4, %r2;\n"
+          << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
+          << "  ld.global.u32 %r5, [%rd14];\n  cvt.u64.u32 %rd3, %r5;\n"
+          << "  ld.param.u64 %rd16, [pe_cap];\n  min.u64 %rd3, %rd3, %rd16;\n"
+          << "  ld.param.u64 %rd15, [pe_list];\n  cvta.to.global.u64 %rd15, %rd15;\n";
+    for (std::size_t i = 0; i + 1 < ps.size(); ++i) {
+      body_ << "  ld.param.u64 %fk" << i << ", [" << ps[i] << "];\n";
+    }
+    body_ << "$Lfix:\n  setp.ge.u64 %p1, %rd1, %rd3;\n  @%p1 bra $Ldone;\n"
+          << "  shl.b64 %rd17, %rd1, 2;\n  add.u64 %rd17, %rd15, %rd17;\n"
+          << "  ld.global.u32 %r6, [%rd17];\n  cvt.u64.u32 %fk" << ps.size() - 1 << ", %r6;\n  {\n";
+    for (std::size_t i = 0; i < ps.size(); ++i) {
+      body_ << "  .param .u64 a" << i << ";\n  st.param.u64 [a" << i << "], %fk" << i << ";\n";
+    }
+    body_ << "  call.uni pe_fix_point, (";
+    for (std::size_t i = 0; i < ps.size(); ++i) body_ << (i ? ", " : "") << "a" << i;
+    body_ << ");\n  }\n  add.u64 %rd1, %rd1, %rd4;\n  bra $Lfix;\n";
   }
 
   void emit_epilogue() {

@@ -69,6 +69,7 @@ struct KernelImage {
   std::uint64_t iv_partition_min = 65536;  // smaller batches skip the partition
   std::uint32_t fix_block = 128;   // fixup kernel CTA size (.maxntid)
   std::uint32_t fix_ctas_per_sm = 4;  // fixup grid: CTAs per SM (.minnctapersm)
+  bool fix_persistent = false;     // fixup entry strides over the list (grid: CTAs per SM x SMs)
   // instruction counts per point (roofline bookkeeping)
   std::uint64_t fp_ops = 0;        // FP64 add/mul/fma issued per point
   std::uint64_t int_ops = 0;       // int64 add/mul/mad per point

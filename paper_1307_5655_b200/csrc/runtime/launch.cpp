@@ -304,8 +304,12 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
     // past the device-side count exit at once
     const std::uint64_t fb = img.fix_block;
     // (a caller-bound list can be larger than this call's batch)
-    const unsigned fix_grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(0x7fffffffull, (std::min(la.cap, la.n) + fb - 1) / fb));
+    std::uint64_t fix_ctas = (std::min(la.cap, la.n) + fb - 1) / fb;
+    if (img.fix_persistent) {
+      fix_ctas = std::min<std::uint64_t>(fix_ctas, static_cast<std::uint64_t>(img.fix_ctas_per_sm) *
+                                                       sm_count(device));
+    }
+    const unsigned fix_grid = static_cast<unsigned>(std::min<std::uint64_t>(0x7fffffffull, fix_ctas));
     launch_one(a.fix_kernel, dev_ok ? a.fix_fn[device] : nullptr,
                dim3(fix_grid ? fix_grid : 1), dim3(static_cast<unsigned>(fb)), args.data(), stream,
                "launch(fixup)");

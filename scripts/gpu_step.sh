@@ -1,7 +1,5 @@
-O=gpurun_out/g12; mkdir -p $O
-python scripts/fp64_peaks.py > $O/peaks.json 2>&1
-nvidia-smi -q -d CLOCK > $O/clocks.txt 2>&1
-T=""
-for s in 500 1000 2000; do T="$T --tune lanes=2,block=256,section_ops=$s --tune lanes=2,block=384,section_ops=$s"; done
-T="$T --tune section_ops=3000,group_tiles=2 --tune section_ops=3000,group_tiles=3 --tune section_ops=2500 --tune section_ops=3500"
-timeout 1500 python scripts/profile_one.py --config c4 --points 100000000 --reps 2 $T > $O/c4_sweep.jsonl 2>&1
+O=gpurun_out/g14; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q -k "interval or c5 or vm or smoke" > $O/pytest_iv.log 2>&1; echo "pytest exit $?" >> $O/pytest_iv.log
+timeout 700 python scripts/fuzz_gpu.py 480 130000 > $O/fuzz.json 2>&1
+timeout 900 python bench.py --config c5 --no-cpu > $O/bench_c5.json 2> $O/bench_c5.err
+PE_CACHE_DIR=off timeout 900 python scripts/first_call.py > $O/first_call.jsonl 2>&1

@@ -185,20 +185,23 @@ def test_coefficient_words_in_domain_format(domain):
 
 
 def test_interval_fixup_entry_has_finite_case_replay():
-    # The fixup entry replays a listed point with the finite-case primitives
-    # first (directed-rounding nextafter, plain products + scan-order
-    # min/max, NaN-poisoned accumulator) and keeps the bit-level replay
-    # behind the %pmid branch; one listed point per thread (no grid-stride
-    # loop, which would let ptxas hoist and spill the coefficient loads).
+    # The fixup replays a listed point with the finite-case primitives first
+    # (directed-rounding nextafter, plain products + scan-order min/max,
+    # NaN-poisoned accumulator) and keeps the bit-level replay behind the
+    # %pmid branch. The replay is a function of the point index; the entry
+    # strides over the list and calls it per point (inside a loop ptxas
+    # would hoist and spill the replay's coefficient loads).
     wl = W.c5()
     prog = pe.compile(wl.poly, wl.schemes)
     ptx = prog.ptx(pe.DOMAIN_INTERVAL)
+    fn = ptx[ptx.index(".func pe_fix_point"):ptx.index(".visible .entry")]
+    assert "%macc" in fn and "@%pmid bra $Lexact" in fn
+    assert "sub.rm.f64" in fn and "add.rn.f64 %tf" in fn
     fix = ptx[ptx.index(".entry pe_walk_interval_fix"):]
-    assert "%macc" in fix and "@%pmid bra $Lexact" in fix
-    assert "sub.rm.f64" in fix and "add.rn.f64 %tf" in fix
-    assert "bra $Lfix" not in fix
+    assert "call.uni pe_fix_point" in fix and "bra $Lfix" in fix
     prog.set_tuning(iv_mid=-1)
     ptx0 = prog.ptx(pe.DOMAIN_INTERVAL)
+    assert prog.compile_only(pe.DOMAIN_INTERVAL) > 0
     assert "%macc" not in ptx0
 
 
