@@ -337,7 +337,10 @@ class Emitter {
       << " nvars=" << s_.nvars << " ops=" << s_.ops.size() << " powers=" << s_.powers.size()
       << " lanes=" << P_ << (*note ? " " : "") << note << "\n//\n";
     m << ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
-    if (n_smem_ > 0) m << ".shared .align 16 .b64 pe_scoef[" << n_smem_ << "];\n\n";
+    if (n_smem_ > 0) {
+      m << ".shared .align 16 .b64 pe_scoef[" << n_smem_ << "];\n"
+        << ".shared .align 8 .b64 pe_mbar;\n\n";
+    }
     if (n_const_ > 0) {
       m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
       for (std::uint32_t i = 0; i < n_const_; ++i) {
@@ -973,15 +976,18 @@ class Emitter {
       body_ << "  ld.param.u64 %ka" << i << ", [" << fparams[i] << "];\n";
     }
     if (n_smem_ > 0) {
-      // shared-tier words: copied once per CTA from the head of the global
-      // coefficient array
+      // shared-tier words: one TMA bulk copy per CTA (cp.async.bulk, 1-D)
+      // from the head of the global coefficient array, completing on an
+      // mbarrier that every thread waits on before the first section
       body_ << "  ld.param.u64 %rd20, [pe_gcoef];\n  cvta.to.global.u64 %rd20, %rd20;\n"
-            << "  mov.u32 %r5, %tid.x;\n  mov.u64 %rd18, pe_scoef;\n$Lsfill:\n"
-            << "  setp.ge.u32 %p3, %r5, " << n_smem_ << ";\n  @%p3 bra $Lsfilled;\n"
-            << "  mul.wide.u32 %rd15, %r5, 8;\n  add.u64 %rd16, %rd20, %rd15;\n"
-            << "  ld.global.nc.b64 %rd17, [%rd16];\n  add.u64 %rd16, %rd18, %rd15;\n"
-            << "  st.shared.b64 [%rd16], %rd17;\n  add.u32 %r5, %r5, %r2;\n  bra $Lsfill;\n"
-            << "$Lsfilled:\n  bar.sync 0;\n";
+            << "  mov.u64 %rd18, pe_scoef;\n  mov.u64 %rd19, pe_mbar;\n"
+            << "  mov.u32 %r5, %tid.x;\n  setp.ne.u32 %p3, %r5, 0;\n  @%p3 bra $Lsarmed;\n"
+            << "  mbarrier.init.shared::cta.b64 [%rd19], 1;\n  fence.proxy.async.shared::cta;\n"
+            << "  mbarrier.arrive.expect_tx.shared::cta.b64 %rd17, [%rd19], " << 8 * n_smem_ << ";\n"
+            << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%rd18], [%rd20], "
+            << 8 * n_smem_ << ", [%rd19];\n"
+            << "$Lsarmed:\n  bar.sync 0;\n$Lswait:\n"
+            << "  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%rd19], 0;\n  @!%p3 bra $Lswait;\n";
     }
     body_ << "$Lgroup:\n  setp.ge.u64 %gp, %gb, %gn;\n  @%gp bra.uni $Ldone;\n";
     for (std::size_t k = 0; k < cuts_.size(); ++k) {

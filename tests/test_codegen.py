@@ -66,6 +66,8 @@ def test_sections_are_functions_over_tile_groups():
     assert ptx.count("call.uni pe_section") == k
     assert ptx.count("ld.global.nc.f64 %x") == 3 * k
     assert ptx.count("ld.global.f64 %v") == ptx.count("st.global.f64 [%ga]") > 0
+    # the shared-memory coefficient tier arrives by one TMA bulk copy per CTA
+    assert "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes" in ptx
     assert prog.compile_only(pe.DOMAIN_F64) > 0
 
 
