@@ -323,6 +323,29 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
                            const double* const* hi, size_t n, double* out_lo,
                            double* out_hi, const pe_exec* exec);
 
+/* Arbitrary-width exact evaluation — the reference BigIntDomain with
+ * multi-limb coefficients and points (the paper's Figure-1 workload:
+ * bench.cpp:59-187, 64..2048-bit coefficients and points). Values are
+ * little-endian two's-complement 64-bit words.
+ *   pe_program_create_wide: term t has exponents[t*nvars ..] and coefficient
+ *     words coeff_words[t*coeff_limbs .. +coeff_limbs). Exponent rows must be
+ *     distinct (zero coefficients are dropped). Only pe_eval_wide evaluates
+ *     such a program (the other pe_eval_* return PE_EINVAL).
+ *   pe_program_wide_limbs: limbs of the result for points of point_limbs
+ *     words (the static magnitude bound of the walk's result).
+ *   pe_eval_wide: coords[v][i*point_limbs + k] is word k of coordinate v of
+ *     point i; out[i*out_limbs + k] receives word k of the result
+ *     (sign-extended; out_limbs must be >= pe_program_wide_limbs, else
+ *     PE_EOVERFLOW). Host or device buffers; one CTA per point. */
+pe_status pe_program_create_wide(const uint32_t* exponents, const uint64_t* coeff_words,
+                                 uint32_t coeff_limbs, size_t nterms, uint32_t nvars,
+                                 const pe_scheme_desc* schemes, pe_program** out);
+pe_status pe_program_wide_limbs(const pe_program* program, uint32_t point_limbs,
+                                uint32_t* out_limbs);
+pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
+                       uint32_t point_limbs, size_t n, uint64_t* out, uint32_t out_limbs,
+                       const pe_exec* exec);
+
 /* Roofline denominator microbenchmark on `device`: kind 0 = DFMA/s
  * (FP64 FMA pipe), kind 1 = 64-bit integer multiply-adds/s, kind 2 = SM
  * cycles per dependent DFMA (latency), kind 3 = FP64 FMAs/s through the

@@ -94,6 +94,13 @@ def ref_lib():
                                    C.POINTER(C.c_size_t)]
         lib.ref_eval_limbs.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32,
                                         C.c_void_p, C.c_int]
+        lib.ref_create_wide.argtypes = [C.POINTER(C.c_uint32), C.c_void_p, C.c_uint32, C.c_size_t,
+                                        C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]
+        lib.ref_eval_wide_check.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_size_t,
+                                            C.c_void_p, C.c_uint32, C.c_int, C.POINTER(C.c_size_t)]
+        lib.ref_time_wide.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_size_t, C.c_int,
+                                      C.POINTER(C.c_double)]
         lib.ref_last_error.restype = C.c_char_p
         _ref = lib
     return _ref
@@ -305,3 +312,51 @@ class Reference:
         buf = (C.c_uint32 * max(1, n.value))()
         ref_lib().ref_exponents(self._h, v, buf, n.value, C.byref(n))
         return list(buf)[: n.value]
+
+
+class ReferenceWide:
+    """The unmodified reference BigIntDomain walk with arbitrary-precision
+    coefficients and points (the paper's Figure-1 workload), for checking and
+    timing pe_eval_wide. Values are little-endian two's-complement words."""
+
+    def __init__(self, exponents, coeff_words, schemes):
+        lib = ref_lib()
+        e = np.ascontiguousarray(np.asarray(exponents, dtype=np.uint32))
+        if e.ndim == 1:
+            e = e.reshape(-1, 1)
+        w = np.ascontiguousarray(np.asarray(coeff_words, dtype=np.uint64))
+        self.nvars = e.shape[1]
+        up, lo, cut = _scheme_arrays(schemes)
+        h = C.c_void_p()
+        self._keep = (e, w)
+        if lib.ref_create_wide(e.ctypes.data_as(C.POINTER(C.c_uint32)), w.ctypes.data, w.shape[1],
+                               e.shape[0], self.nvars, up, lo, cut, C.byref(h)):
+            raise ValueError(lib.ref_last_error().decode())
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                ref_lib().ref_destroy(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+    def mismatches(self, coords, got, threads=8):
+        """Points whose result words `got` (n, out_limbs) differ from the
+        reference BigInt result; coords: one (n, point_limbs) array per variable."""
+        cols = [np.ascontiguousarray(c, dtype=np.uint64) for c in coords]
+        g = np.ascontiguousarray(got, dtype=np.uint64)
+        bad = C.c_size_t()
+        if ref_lib().ref_eval_wide_check(self._h, _ptrs(cols), cols[0].shape[1], cols[0].shape[0],
+                                         g.ctypes.data, g.shape[1], threads, C.byref(bad)):
+            raise ValueError(ref_lib().ref_last_error().decode())
+        return bad.value
+
+    def seconds(self, coords, threads=1):
+        cols = [np.ascontiguousarray(c, dtype=np.uint64) for c in coords]
+        t = C.c_double()
+        if ref_lib().ref_time_wide(self._h, _ptrs(cols), cols[0].shape[1], cols[0].shape[0], threads,
+                                   C.byref(t)):
+            raise ValueError(ref_lib().ref_last_error().decode())
+        return t.value

@@ -23,6 +23,7 @@
 #include <polyeval/tree.hpp>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -354,6 +355,121 @@ int ref_eval_limbs(void* h, const std::int64_t* const* coords, std::size_t n, st
       }
       for (std::uint32_t k = 0; k < K; ++k) out[k * n + i] = mag[k];
     }
+    return 0;
+  });
+}
+
+}  // extern "C"
+
+// ---- arbitrary-width integers (the paper's Figure-1 workload) ----
+
+namespace {
+BigInt big_of_words(const std::uint64_t* w, std::uint32_t L) {  // two's complement
+  const bool neg = L && (w[L - 1] >> 63);
+  std::vector<std::uint64_t> m(w, w + L);
+  if (neg) {
+    unsigned __int128 c = 1;
+    for (auto& x : m) {
+      const unsigned __int128 t = static_cast<unsigned __int128>(~x) + c;
+      x = static_cast<std::uint64_t>(t);
+      c = t >> 64;
+    }
+  }
+  return BigInt::from_words(m, neg);
+}
+
+// one BigIntDomain session per thread over contiguous shards of the points
+template <typename Fn>
+void wide_sharded(const RefProgram& rp, std::size_t n, int threads, Fn&& per_point) {
+  threads = std::max(1, threads);
+  const std::size_t per = (n + threads - 1) / threads;
+  std::vector<std::exception_ptr> errors(threads);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      try {
+        Evaluator<BigIntDomain> session(BigIntDomain{}, *rp.program);
+        const std::size_t lo = t * per, hi = std::min(n, lo + per);
+        for (std::size_t i = lo; i < hi; ++i) per_point(session, i);
+      } catch (...) {
+        errors[t] = std::current_exception();
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (auto& e : errors) {
+    if (e) std::rethrow_exception(e);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+// A program whose coefficient t is words[t*coeff_limbs .. +coeff_limbs)
+// (two's complement), built by the reference's own canonicalize / build /
+// lazy heights / compile.
+int ref_create_wide(const std::uint32_t* exps, const std::uint64_t* words, std::uint32_t coeff_limbs,
+                    std::size_t nterms, std::uint32_t nvars, const int* upper, const int* lower,
+                    const std::uint64_t* cutoff, void** out) {
+  return guarded([&] {
+    auto rp = std::make_unique<RefProgram>();
+    rp->integer = true;
+    rp->nvars = nvars;
+    std::vector<std::string> vars;
+    for (std::uint32_t v = 0; v < nvars; ++v) {
+      vars.push_back(nvars <= 3 ? std::string(1, "xyz"[v]) : "x" + std::to_string(v));
+    }
+    std::vector<Term> raw(nterms);
+    for (std::size_t t = 0; t < nterms; ++t) {
+      raw[t].coefficient = big_of_words(words + t * coeff_limbs, coeff_limbs);
+      raw[t].exponents.assign(exps + t * nvars, exps + (t + 1) * nvars);
+    }
+    Polynomial p = Polynomial::canonicalize(std::move(raw), vars);
+    std::vector<FunctionScheme> schemes;
+    for (std::uint32_t v = 0; v < nvars; ++v) schemes.push_back(scheme_of(upper[v], lower[v], cutoff[v]));
+    EvaluationTree tree = nvars == 1 ? build(p, schemes[0], 0) : build_multivariate(p, schemes);
+    compute_lazy_heights(tree);
+    rp->program = std::make_unique<CompiledProgram>(compile(tree));
+    rp->tree = std::make_unique<EvaluationTree>(std::move(tree));
+    *out = rp.release();
+    return 0;
+  });
+}
+
+// Compares results (out_limbs two's-complement words per point) with the
+// reference BigInt results at the same points; *mismatches = differing points.
+int ref_eval_wide_check(void* h, const std::uint64_t* const* coords, std::uint32_t point_limbs,
+                        std::size_t n, const std::uint64_t* got, std::uint32_t out_limbs, int threads,
+                        std::size_t* mismatches) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    std::vector<char> bad(n, 0);
+    wide_sharded(rp, n, threads, [&](Evaluator<BigIntDomain>& s, std::size_t i) {
+      std::vector<BigInt> pt(rp.nvars);
+      for (std::size_t v = 0; v < rp.nvars; ++v) pt[v] = big_of_words(coords[v] + i * point_limbs, point_limbs);
+      const BigInt want = s.evaluate(std::span<const BigInt>(pt));
+      bad[i] = !(want == big_of_words(got + i * out_limbs, out_limbs));
+    });
+    *mismatches = static_cast<std::size_t>(std::count(bad.begin(), bad.end(), 1));
+    return 0;
+  });
+}
+
+// Wall time of evaluating the n points (BigIntDomain, `threads` sessions).
+int ref_time_wide(void* h, const std::uint64_t* const* coords, std::uint32_t point_limbs, std::size_t n,
+                  int threads, double* seconds) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    std::vector<std::vector<BigInt>> pts(n, std::vector<BigInt>(rp.nvars));
+    for (std::size_t i = 0; i < n; ++i) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) pts[i][v] = big_of_words(coords[v] + i * point_limbs, point_limbs);
+    }
+    std::vector<std::size_t> sink(n);
+    const auto t0 = std::chrono::steady_clock::now();
+    wide_sharded(rp, n, threads, [&](Evaluator<BigIntDomain>& s, std::size_t i) {
+      sink[i] = s.evaluate(std::span<const BigInt>(pts[i])).bit_length();
+    });
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return 0;
   });
 }

@@ -15,7 +15,13 @@ from .api import (  # noqa: F401
     Polynomial,
     builtin_scheme,
     compile,
+    compile_wide,
     evaluate,
+    evaluate_wide,
+    ints_to_words,
+    limbs_for,
+    wide_limbs,
+    words_to_ints,
     evaluate_many,
     evaluate_parallel,
     launch_count,

@@ -149,6 +149,13 @@ EXPORTS = [
     ("pe_eval_interval", C.c_int,
      [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p,
       C.c_void_p, C.POINTER(pe_exec)]),
+    ("pe_program_create_wide", C.c_int,
+     [C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.c_uint32, C.c_size_t, C.c_uint32,
+      C.POINTER(pe_scheme_desc), C.POINTER(C.c_void_p)]),
+    ("pe_program_wide_limbs", C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
+    ("pe_eval_wide", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32, C.c_size_t, C.c_void_p, C.c_uint32,
+      C.POINTER(pe_exec)]),
     ("pe_measure_peak", C.c_int,
      [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     ("pe_synchronize", C.c_int, [C.POINTER(pe_exec)]),

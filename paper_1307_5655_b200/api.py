@@ -661,5 +661,120 @@ def evaluate_parallel(program: CompiledProgram, points, domain, workers: int):
     return Evaluator(domain, program).evaluate_parallel(points, workers)
 
 
+# ----------------------------------------------------------------- wide integers
+
+def ints_to_words(values, limbs: int) -> np.ndarray:
+    """Python ints -> (n, limbs) uint64 words, little-endian two's complement.
+    Raises OverflowError if a value needs more than 64 * limbs - 1 bits."""
+    vals = [int(v) for v in values]
+    out = np.zeros((len(vals), limbs), dtype=np.uint64)
+    top = 1 << (64 * limbs)
+    for i, v in enumerate(vals):
+        if not -(top >> 1) <= v < (top >> 1):
+            raise OverflowError(f"value needs more than {64 * limbs - 1} bits")
+        u = v % top
+        for k in range(limbs):
+            out[i, k] = (u >> (64 * k)) & 0xFFFFFFFFFFFFFFFF
+    return out
+
+
+def words_to_ints(words) -> list:
+    """(n, limbs) uint64 two's-complement words -> Python ints."""
+    w = np.asarray(words, dtype=np.uint64)
+    limbs = w.shape[1]
+    top = 1 << (64 * limbs)
+    out = []
+    for row in w:
+        v = 0
+        for k in range(limbs - 1, -1, -1):
+            v = (v << 64) | int(row[k])
+        out.append(v - top if v >> (64 * limbs - 1) else v)
+    return out
+
+
+def limbs_for(values) -> int:
+    """Smallest limb count holding every value in two's complement."""
+    bits = max((abs(int(v)).bit_length() for v in values), default=0)
+    return max(1, (bits + 1 + 63) // 64)
+
+
+def compile_wide(exponents, coefficients, schemes) -> CompiledProgram:
+    """A program with arbitrary-precision integer coefficients (Python ints;
+    the reference's BigInt Polynomial), evaluated by evaluate_wide — the
+    paper's Figure-1 workload (pe_program_create_wide). Exponent rows must be
+    distinct."""
+    e = np.ascontiguousarray(np.asarray(exponents, dtype=np.int64))
+    if e.ndim == 1:
+        e = e.reshape(-1, 1)
+    if e.size and (e.min() < 0 or e.max() >= 2**32):
+        raise ValueError("exponents must lie in [0, 2^32)")
+    e = np.ascontiguousarray(e.astype(np.uint32))
+    nvars = e.shape[1]
+    if isinstance(schemes, FunctionScheme):
+        schemes = [schemes] * nvars
+    if len(schemes) != nvars:
+        raise ValueError("need exactly one scheme per variable")
+    coefs = [int(c) for c in coefficients]
+    if len(coefs) != e.shape[0]:
+        raise ValueError("one coefficient per term")
+    limbs = limbs_for(coefs)
+    words = np.ascontiguousarray(ints_to_words(coefs, limbs))
+    descs = (L.pe_scheme_desc * nvars)(*[s.desc() for s in schemes])
+    h = C.c_void_p()
+    L.check(L.lib().pe_program_create_wide(e.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                           words.ctypes.data_as(C.POINTER(C.c_uint64)), limbs,
+                                           e.shape[0], nvars, descs, C.byref(h)))
+    self = CompiledProgram.__new__(CompiledProgram)
+    self.poly = None
+    self.schemes = tuple(schemes)
+    self._nvars = nvars
+    self.integer = True
+    self._h = h
+    self.wide = True
+    return self
+
+
+def wide_limbs(program: CompiledProgram, point_limbs: int) -> int:
+    """Result limbs the static bound needs for points of point_limbs words."""
+    k = C.c_uint32()
+    L.check(L.lib().pe_program_wide_limbs(program.handle, point_limbs, C.byref(k)))
+    return k.value
+
+
+def evaluate_wide(program: CompiledProgram, points, point_limbs: int | None = None,
+                  device: int = -1, as_words: bool = False):
+    """Exact evaluation at integer points of any size (pe_eval_wide, one CTA
+    per point). points: one sequence of Python ints per variable, or one
+    (n, point_limbs) uint64 word array per variable. Returns Python ints (or
+    the (n, out_limbs) result words with as_words=True)."""
+    if len(points) != program.nvars:
+        raise ValueError("evaluation point arity mismatch")
+    cols = []
+    if point_limbs is None:
+        if all(isinstance(p, np.ndarray) and p.ndim == 2 for p in points):
+            point_limbs = points[0].shape[1]
+        else:
+            point_limbs = max(limbs_for(p) for p in points)
+    for p in points:
+        if isinstance(p, np.ndarray) and p.ndim == 2:
+            if p.shape[1] != point_limbs or p.dtype != np.uint64:
+                raise ValueError("word arrays must be (n, point_limbs) uint64")
+            cols.append(np.ascontiguousarray(p))
+        else:
+            cols.append(np.ascontiguousarray(ints_to_words(p, point_limbs)))
+    n = {c.shape[0] for c in cols}
+    if len(n) != 1:
+        raise ValueError("all coordinate arrays must have the same length")
+    n = n.pop()
+    out_limbs = wide_limbs(program, point_limbs)
+    out = np.zeros((n, out_limbs), dtype=np.uint64)
+    ptrs = (C.c_void_p * len(cols))(*[c.ctypes.data for c in cols])
+    ex = L.pe_exec()
+    ex.device = device
+    L.check(L.lib().pe_eval_wide(program.handle, ptrs, point_limbs, n, out.ctypes.data, out_limbs,
+                                 C.byref(ex)))
+    return out if as_words else words_to_ints(out)
+
+
 def launch_count() -> int:
     return int(L.lib().pe_launch_count())

@@ -39,6 +39,16 @@ extern "C" cudaError_t pe_launch_narrow_limbs(const unsigned long long* const* l
                                               size_t n, long long* out, unsigned* flag, int sms,
                                               cudaStream_t stream);
 extern "C" cudaError_t pe_measure_dfma_latency(double* cycles_per_op);
+extern "C" cudaError_t pe_launch_wide(const std::uint32_t* code, std::uint32_t nops,
+                                      const std::uint32_t* slot_off, const std::uint32_t* slot_w,
+                                      const std::uint32_t* coef_off, const std::uint32_t* coef_w,
+                                      const std::uint64_t* coef_words, std::uint32_t nvars,
+                                      const std::uint64_t* const* in, std::uint32_t point_limbs,
+                                      std::uint64_t* out, std::uint32_t out_limbs,
+                                      std::uint32_t result, std::uint32_t result_w,
+                                      std::uint32_t arena, std::uint32_t tmp_w,
+                                      std::uint64_t* scratch, unsigned grid, unsigned long long n,
+                                      cudaStream_t stream);
 
 struct pe_program {
   polyeval::rt::Program impl;
@@ -369,6 +379,171 @@ pe_status pe_program_create(const uint32_t* exponents, const void* coeffs, size_
   });
 }
 
+pe_status pe_program_create_wide(const uint32_t* exponents, const uint64_t* coeff_words,
+                                 uint32_t coeff_limbs, size_t nterms, uint32_t nvars,
+                                 const pe_scheme_desc* schemes, pe_program** out) {
+  return guarded([&]() -> pe_status {
+    if (!out) return fail(PE_EINVAL, "out is null");
+    *out = nullptr;
+    if (nvars == 0) return fail(PE_EINVAL, "nvars must be >= 1");
+    if (!schemes) return fail(PE_EINVAL, "schemes is null");
+    if (coeff_limbs == 0) return fail(PE_EINVAL, "coeff_limbs must be >= 1");
+    if (nterms > 0 && (!exponents || !coeff_words)) return fail(PE_EINVAL, "terms are null");
+    if (nterms >= (std::size_t{1} << 62)) return fail(PE_EINVAL, "too many terms");
+    // keep the nonzero terms; each gets the placeholder coefficient
+    // (index + 1) the front end builds the tree with
+    auto wf = std::make_unique<WideFront>();
+    std::vector<std::uint32_t> exps;
+    std::vector<std::int64_t> ph;
+    for (size_t t = 0; t < nterms; ++t) {
+      const uint64_t* w = coeff_words + t * coeff_limbs;
+      if (std::all_of(w, w + coeff_limbs, [](uint64_t x) { return x == 0; })) continue;
+      wf->coefs.emplace_back(w, w + coeff_limbs);
+      exps.insert(exps.end(), exponents + t * nvars, exponents + (t + 1) * nvars);
+      ph.push_back(static_cast<std::int64_t>(wf->coefs.size()));
+    }
+    std::vector<std::uint32_t> order(ph.size());
+    for (std::uint32_t k = 0; k < order.size(); ++k) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+      return std::lexicographical_compare(exps.begin() + a * nvars, exps.begin() + (a + 1) * nvars,
+                                          exps.begin() + b * nvars, exps.begin() + (b + 1) * nvars);
+    });
+    for (size_t k = 1; k < order.size(); ++k) {
+      if (std::equal(exps.begin() + order[k] * nvars, exps.begin() + (order[k] + 1) * nvars,
+                     exps.begin() + order[k - 1] * nvars)) {
+        return fail(PE_EINVAL, "wide programs need distinct exponent rows");
+      }
+    }
+    auto h = std::make_unique<pe_program>();
+    Program& p = h->impl;
+    p.nvars = nvars;
+    p.integer = true;
+    p.i = build_front(p, exps.data(), ph.data(), ph.size(), nvars, schemes);
+    p.wide = std::move(wf);
+    *out = h.release();
+    return PE_OK;
+  });
+}
+
+pe_status pe_program_wide_limbs(const pe_program* program, uint32_t point_limbs,
+                                uint32_t* out_limbs) {
+  return guarded([&]() -> pe_status {
+    if (!program || !out_limbs) return fail(PE_EINVAL, "null argument");
+    const Program& p = program->impl;
+    if (!p.wide) return fail(PE_EINVAL, "not a wide program (pe_program_create_wide)");
+    std::lock_guard<std::mutex> lock(p.mu);
+    auto it = p.wide->plans.find(point_limbs);
+    if (it == p.wide->plans.end()) {
+      it = p.wide->plans.emplace(point_limbs, plan_wide(p.i->flat, p.wide->coefs, point_limbs)).first;
+    }
+    *out_limbs = it->second.result_limbs;
+    return PE_OK;
+  });
+}
+
+pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
+                       uint32_t point_limbs, size_t n, uint64_t* out, uint32_t out_limbs,
+                       const pe_exec* exec) {
+  return guarded([&]() -> pe_status {
+    if (!program) return fail(PE_EINVAL, "program is null");
+    const Program& p = program->impl;
+    if (!p.wide) return fail(PE_EINVAL, "not a wide program (pe_program_create_wide)");
+    if (n == 0) return PE_OK;
+    if (!coords || !out) return fail(PE_EINVAL, "null buffer");
+    for (uint32_t v = 0; v < p.nvars; ++v) {
+      if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
+    }
+    if (p.nvars > 16) return fail(PE_EINVAL, "at most 16 variables");
+    uint32_t need = 0;
+    const pe_status st = pe_program_wide_limbs(program, point_limbs, &need);
+    if (st != PE_OK) return st;
+    if (out_limbs < need) {
+      return fail(PE_EOVERFLOW, "results need " + std::to_string(need) + " limbs");
+    }
+    MemKind kind;
+    const int dev = resolve_device(exec, out, &kind);
+    check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    cudaStream_t s = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    const WidePlan* plan;
+    WideDevice dv;
+    {
+      std::lock_guard<std::mutex> lock(p.mu);
+      plan = &p.wide->plans.at(point_limbs);
+      auto& slot = p.wide->dev[{dev, point_limbs}];
+      if (!slot.code) {
+        auto up = [](void** d, const void* src, size_t bytes) {
+          check_cuda(cudaMalloc(d, std::max<size_t>(bytes, 8)), "cudaMalloc(wide plan)");
+          if (bytes) check_cuda(cudaMemcpy(*d, src, bytes, cudaMemcpyHostToDevice), "wide plan upload");
+        };
+        up(&slot.code, plan->code.data(), plan->code.size() * 4);
+        up(&slot.slot_off, plan->slot_off.data(), plan->slot_off.size() * 4);
+        up(&slot.slot_w, plan->slot_w.data(), plan->slot_w.size() * 4);
+        up(&slot.coef_off, plan->coef_off.data(), plan->coef_off.size() * 4);
+        up(&slot.coef_w, plan->coef_w.data(), plan->coef_w.size() * 4);
+        up(&slot.coef_words, plan->coef_words.data(), plan->coef_words.size() * 8);
+      }
+      dv = slot;
+    }
+    // inputs / outputs on the device (host buffers are copied: the walk of
+    // one point is long, so staging is a small part of a wide call)
+    std::vector<const std::uint64_t*> din(p.nvars);
+    std::vector<void*> owned;
+    auto cleanup = [&] {
+      for (void* q : owned) cudaFreeAsync(q, s);
+    };
+    try {
+      for (uint32_t v = 0; v < p.nvars; ++v) {
+        int d2 = -1;
+        if (classify(coords[v], &d2) == MemKind::Device) {
+          din[v] = coords[v];
+        } else {
+          void* q = nullptr;
+          check_cuda(cudaMallocAsync(&q, n * point_limbs * 8, s), "cudaMallocAsync(wide input)");
+          owned.push_back(q);
+          check_cuda(cudaMemcpyAsync(q, coords[v], n * point_limbs * 8, cudaMemcpyHostToDevice, s),
+                     "wide input H2D");
+          din[v] = static_cast<const std::uint64_t*>(q);
+        }
+      }
+      std::uint64_t* dout = out;
+      if (kind != MemKind::Device) {
+        void* q = nullptr;
+        check_cuda(cudaMallocAsync(&q, n * out_limbs * 8, s), "cudaMallocAsync(wide output)");
+        owned.push_back(q);
+        dout = static_cast<std::uint64_t*>(q);
+      }
+      const int sms = device_ctx(dev).sms;
+      const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(n, 4ull * sms));
+      const size_t per_cta = static_cast<size_t>(plan->arena) + 5ull * plan->tmp_w;
+      void* scratch = nullptr;
+      check_cuda(cudaMallocAsync(&scratch, grid * per_cta * 8, s), "cudaMallocAsync(wide arena)");
+      owned.push_back(scratch);
+      check_cuda(pe_launch_wide(static_cast<const std::uint32_t*>(dv.code), plan->nops,
+                                static_cast<const std::uint32_t*>(dv.slot_off),
+                                static_cast<const std::uint32_t*>(dv.slot_w),
+                                static_cast<const std::uint32_t*>(dv.coef_off),
+                                static_cast<const std::uint32_t*>(dv.coef_w),
+                                static_cast<const std::uint64_t*>(dv.coef_words), p.nvars, din.data(),
+                                point_limbs, dout, out_limbs, plan->result, plan->result_limbs,
+                                plan->arena, plan->tmp_w, static_cast<std::uint64_t*>(scratch), grid, n,
+                                s),
+                 "launch(wide walk)");
+      launch_counter().fetch_add(1, std::memory_order_relaxed);
+      if (kind != MemKind::Device) {
+        check_cuda(cudaMemcpyAsync(out, dout, n * out_limbs * 8, cudaMemcpyDeviceToHost, s), "wide D2H");
+      }
+      cleanup();
+      if (kind != MemKind::Device || (exec && exec->synchronize)) {
+        check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    return PE_OK;
+  });
+}
+
 pe_status pe_program_check_registers(const pe_program* program) {
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
@@ -672,6 +847,7 @@ pe_status pe_eval_f64(const pe_program* program, const double* const* coords, si
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
     const Program& p = program->impl;
+    if (p.wide) return fail(PE_EINVAL, "a wide program evaluates through pe_eval_wide");
     if (n == 0) return PE_OK;
     if (!coords || !out) return fail(PE_EINVAL, "null buffer");
     for (uint32_t v = 0; v < p.nvars; ++v) {
@@ -711,6 +887,7 @@ pe_status pe_eval_f64_multi(const pe_program* const* programs, size_t k,
     for (size_t j = 0; j < k; ++j) {
       if (!programs[j] || !outs[j]) return fail(PE_EINVAL, "null program or output");
       if (programs[j]->impl.nvars != nv) return fail(PE_EINVAL, "programs differ in variable count");
+      if (programs[j]->impl.wide) return fail(PE_EINVAL, "a wide program evaluates through pe_eval_wide");
     }
     for (uint32_t v = 0; v < nv; ++v) {
       if (!coords[v]) return fail(PE_EINVAL, "evaluation point arity mismatch");
@@ -749,6 +926,7 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
     const Program& p = program->impl;
+    if (p.wide) return fail(PE_EINVAL, "a wide program evaluates through pe_eval_wide");
     if (n == 0) return PE_OK;
     if (!lo || !hi || !out_lo || !out_hi) return fail(PE_EINVAL, "null buffer");
     std::vector<const void*> ins;
@@ -848,6 +1026,7 @@ pe_status pe_eval_limbs(const pe_program* program, const int64_t* const* coords,
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
     const Program& p = program->impl;
+    if (p.wide) return fail(PE_EINVAL, "a wide program evaluates through pe_eval_wide");
     if (!p.integer) return fail(PE_EINVAL, "pe_eval_limbs needs a program with int64 coefficients");
     if (limbs < 1 || limbs > 8) return fail(PE_EINVAL, "limbs must be 1..8");
     if (n == 0) return PE_OK;
@@ -900,6 +1079,7 @@ pe_status pe_eval_i64(const pe_program* program, const int64_t* const* coords, s
   return guarded([&]() -> pe_status {
     if (!program) return fail(PE_EINVAL, "program is null");
     const Program& p = program->impl;
+    if (p.wide) return fail(PE_EINVAL, "a wide program evaluates through pe_eval_wide");
     if (!p.integer) return fail(PE_EINVAL, "pe_eval_i64 needs a program with int64 coefficients");
     if (n == 0) return PE_OK;
     if (!coords || !out) return fail(PE_EINVAL, "null buffer");

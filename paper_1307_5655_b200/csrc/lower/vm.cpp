@@ -18,7 +18,7 @@ std::uint64_t bits(double d) {
 }  // namespace
 
 template <typename C>
-VmProgram build_vm(const Stream<C>& s, Domain d) {
+VmProgram build_vm(const Stream<C>& s, Domain d, bool distinct_dst) {
   if (d == Domain::I64K) throw std::invalid_argument("the walk VM has no K-limb domain");
   if ((d == Domain::F64Strict || d == Domain::Interval) && !s.strict) {
     throw std::logic_error("strict domain needs a strict stream");
@@ -83,14 +83,16 @@ VmProgram build_vm(const Stream<C>& s, Domain d) {
     const VOp& op = ops[i];
     std::uint32_t enc[3];
     for (int k = 0; k < 3; ++k) enc[k] = operand(op.src[k], op.in[k]);
+    std::vector<std::uint32_t> released;
     for (int k = 0; k < 3; ++k) {  // release values read here for the last time
       const std::int64_t v = op.in[k];
       if (v >= 0 && last[static_cast<std::size_t>(v)] == static_cast<std::int64_t>(i) &&
           slot_of[static_cast<std::size_t>(v)] >= 0) {
-        free_slots.push_back(static_cast<std::uint32_t>(slot_of[static_cast<std::size_t>(v)]));
+        released.push_back(static_cast<std::uint32_t>(slot_of[static_cast<std::size_t>(v)]));
         slot_of[static_cast<std::size_t>(v)] = -1;
       }
     }
+    if (!distinct_dst) free_slots.insert(free_slots.end(), released.begin(), released.end());
     std::uint32_t dst;
     if (last[op.dst] < 0) {
       dst = top;  // dead value (never read): any scratch slot
@@ -102,6 +104,7 @@ VmProgram build_vm(const Stream<C>& s, Domain d) {
     }
     if (last[op.dst] >= 0) slot_of[op.dst] = dst;
     if (dst >= top) top = dst + 1;
+    if (distinct_dst) free_slots.insert(free_slots.end(), released.begin(), released.end());
     vm.code.insert(vm.code.end(), {op.kind, dst, enc[0], enc[1], enc[2]});
   }
   vm.nops = static_cast<std::uint32_t>(ops.size());
@@ -128,7 +131,7 @@ VmProgram build_vm(const Stream<C>& s, Domain d) {
   return vm;
 }
 
-template VmProgram build_vm(const Stream<double>&, Domain);
-template VmProgram build_vm(const Stream<std::int64_t>&, Domain);
+template VmProgram build_vm(const Stream<double>&, Domain, bool);
+template VmProgram build_vm(const Stream<std::int64_t>&, Domain, bool);
 
 }  // namespace polyeval::lower

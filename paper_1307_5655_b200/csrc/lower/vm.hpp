@@ -36,7 +36,10 @@ struct VmProgram {
   std::vector<std::uint64_t> hi;    // interval upper endpoints (else empty)
 };
 
+/// `distinct_dst`: never give an op a destination slot that one of its
+/// operands occupies (the wide-integer kernels write results limb by limb
+/// while reading the operands).
 template <typename C>
-VmProgram build_vm(const Stream<C>& s, Domain d);
+VmProgram build_vm(const Stream<C>& s, Domain d, bool distinct_dst = false);
 
 }  // namespace polyeval::lower

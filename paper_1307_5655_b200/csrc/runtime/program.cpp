@@ -325,6 +325,13 @@ Artifact::~Artifact() {
   if (library) cudaLibraryUnload(library);
 }
 
+WideFront::~WideFront() {
+  for (auto& [key, d] : dev) {
+    if (cudaSetDevice(key.first) != cudaSuccess) continue;
+    for (void* p : {d.code, d.slot_off, d.slot_w, d.coef_off, d.coef_w, d.coef_words}) cudaFree(p);
+  }
+}
+
 void Program::release() const {
   std::vector<std::thread> jobs;
   {

@@ -22,6 +22,7 @@
 #include "front/terms.hpp"
 #include "lower/ptx.hpp"
 #include "lower/vm.hpp"
+#include "runtime/wide.hpp"
 
 extern "C" unsigned pe_vm_max_slots(void);
 
@@ -95,6 +96,19 @@ struct Front {
   front::FlatProgram<C> flat;
 };
 
+/// Wide programs (pe_program_create_wide): the terms' coefficient words and
+/// the plans per point width, with their device copies.
+struct WideDevice {
+  void *code = nullptr, *slot_off = nullptr, *slot_w = nullptr, *coef_off = nullptr,
+       *coef_w = nullptr, *coef_words = nullptr;
+};
+struct WideFront {
+  std::vector<std::vector<std::uint64_t>> coefs;  // by term, two's complement words
+  std::map<std::uint32_t, WidePlan> plans;         // by point limbs
+  std::map<std::pair<int, std::uint32_t>, WideDevice> dev;  // (device, point limbs)
+  ~WideFront();
+};
+
 struct Program {
   std::uint32_t nvars = 0;
   bool integer = false;  // coefficient type int64 (else fp64)
@@ -103,6 +117,7 @@ struct Program {
 
   std::unique_ptr<Front<double>> f;         // fp64 coefficients
   std::unique_ptr<Front<std::int64_t>> i;   // int64 coefficients
+  std::unique_ptr<WideFront> wide;          // multi-limb coefficients (i holds placeholders)
 
   front::WalkStats stats;
   lower::Tuning tuning;  // code-generation options (pe_program_set_tuning)

@@ -138,3 +138,31 @@ def c5() -> Workload:
 
 
 ALL = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+
+
+def fig1(degree: int, coeff_bits: int = 64, point_bits: int = 64, n_points: int = 64,
+         seed: int = 0):
+    """The paper's Figure-1 workload (reference bench.cpp:59-187 run_grid):
+    dense degree-d polynomial, coefficients uniform in [1, 2^coeff_bits)
+    (zero redrawn), points with exactly point_bits bits (top bit set).
+    Returns (exponents, coefficients as Python ints, points as Python ints).
+    Seeded PCG64 words through explicit transforms, like every config here."""
+    rng = _rng(7000 + 131 * degree + seed)
+
+    def rand_bits(bits):
+        words = (bits + 63) // 64
+        raw = rng.bit_generator.random_raw(words).astype(np.uint64)
+        v = 0
+        for w in raw[::-1]:
+            v = (v << 64) | int(w)
+        return v & ((1 << bits) - 1)
+
+    coefs = []
+    for _ in range(degree + 1):
+        c = rand_bits(coeff_bits)
+        while c == 0:
+            c = rand_bits(coeff_bits)
+        coefs.append(c)
+    exps = list(range(degree, -1, -1))
+    points = [rand_bits(point_bits - 1) + (1 << (point_bits - 1)) for _ in range(n_points)]
+    return exps, coefs, points

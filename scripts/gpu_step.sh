@@ -1,5 +1,6 @@
-O=gpurun_out/g14; mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q -k "interval or c5 or vm or smoke" > $O/pytest_iv.log 2>&1; echo "pytest exit $?" >> $O/pytest_iv.log
-timeout 700 python scripts/fuzz_gpu.py 480 130000 > $O/fuzz.json 2>&1
-timeout 900 python bench.py --config c5 --no-cpu > $O/bench_c5.json 2> $O/bench_c5.err
-PE_CACHE_DIR=off timeout 900 python scripts/first_call.py > $O/first_call.jsonl 2>&1
+O=gpurun_out/g15; mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+for c in c4 c2 c3 c1 c5; do timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; done
+timeout 600 python bench.py --impl reference > $O/bench_ref_c4.json 2> $O/bench_ref_c4.err
+timeout 2000 bash scripts/ncu_captures.sh c4 c5 c2e1000 c3

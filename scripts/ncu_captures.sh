@@ -12,7 +12,7 @@ for c in "${@:-c4 c5}"; do
   esac
   python scripts/profile_one.py --config $c --points $pts --reps 1 > $O/${c}_plain.log 2>&1 || continue
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_${c}.csv \
-    python bench.py --config $c --steps 2 --warmup 3 --no-cpu --no-e2e > $O/${c}_launches.log 2>&1
+    python bench.py --config ${c:0:2} --steps 2 --warmup 3 --no-cpu --no-e2e > $O/${c}_launches.log 2>&1
   ncu --set full --import-source on --clock-control none -k $k -s 1 -c 4 \
     -o $O/ncu_${c} python scripts/profile_one.py --config $c --points $pts --reps 1 > $O/${c}_ncu.log 2>&1
   ncu -i $O/ncu_${c}.ncu-rep --page raw --csv > $O/r2_ncu_${c}_raw.csv 2>/dev/null
