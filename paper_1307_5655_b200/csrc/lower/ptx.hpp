@@ -35,7 +35,7 @@ const char* domain_name(Domain d);
 struct CoefTiers {
   static constexpr std::uint32_t kConstCap = 8000;
   static constexpr std::uint32_t kParamCap = 3900;
-  static constexpr std::uint32_t kSmemCap = 6144;  // 48 KB static shared (sectioned kernels)
+  static constexpr std::uint32_t kSmemCap = 6140;  // 48 KB static shared less the mbarrier
 };
 
 struct KernelImage {

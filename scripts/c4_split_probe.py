@@ -42,7 +42,7 @@ for K in ([int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else (1,
         hi = xs[len(xs) * (q + 1) // K] if q + 1 < K else 10**9
         sel = (e[:, 0] >= lo) & (e[:, 0] < hi)
         p = pe.compile(pe.Polynomial(e[sel], c[sel]), wl.schemes)
-        p.set_tuning(section_ops=2**32 - 1)
+        p.set_tuning(section_ops=2**32 - 1, jit_mode=1)
         evs.append(pe.Evaluator(pe.DoubleDomain(), p))
     outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in evs]
 

@@ -247,3 +247,16 @@ def test_cubin_cache_survives_corruption_and_concurrency(tmp_path, monkeypatch):
     files[0].write_bytes(files[0].read_bytes()[:100])  # truncated entry
     assert build(0) == sizes[0]
     assert files[0].stat().st_size > 1000  # rewritten
+
+
+def test_sectioned_kernel_with_all_coefficient_tiers_compiles():
+    # 20k distinct coefficients: constant bank, the shared-memory tier up to
+    # the 48 KB static limit (with the TMA mbarrier), global beyond
+    rng = np.random.default_rng(12)
+    d = 20_000
+    p = pe.Polynomial(np.arange(d, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, d + 1))
+    prog = pe.compile(p, pe.builtin_scheme("estrin"))
+    assert prog.f64_slices() > 1
+    ptx = prog.ptx(pe.DOMAIN_F64)
+    assert "ld.shared" in ptx and "ld.global.nc.f64 %c" in ptx
+    assert prog.compile_only(pe.DOMAIN_F64) > 0
