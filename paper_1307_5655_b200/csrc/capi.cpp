@@ -47,8 +47,8 @@ extern "C" cudaError_t pe_launch_wide(const std::uint32_t* code, std::uint32_t n
                                       std::uint64_t* out, std::uint32_t out_limbs,
                                       std::uint32_t result, std::uint32_t result_w,
                                       std::uint32_t arena, std::uint32_t tmp_w,
-                                      std::uint64_t* scratch, unsigned grid, unsigned long long n,
-                                      cudaStream_t stream);
+                                      std::uint64_t* scratch, unsigned grid, unsigned threads,
+                                      unsigned long long n, cudaStream_t stream);
 
 struct pe_program {
   polyeval::rt::Program impl;
@@ -512,9 +512,16 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
         owned.push_back(q);
         dout = static_cast<std::uint64_t*>(q);
       }
+      // CTA size by value width (a narrow walk would leave most of a wide
+      // CTA idle at every barrier); as many CTAs as fit 1024 threads per SM,
+      // at most 4 GB of arenas
       const int sms = device_ctx(dev).sms;
-      const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(n, 4ull * sms));
+      const unsigned threads = plan->tmp_w <= 64 ? 32 : plan->tmp_w <= 256 ? 64
+                               : plan->tmp_w <= 1024 ? 128 : 256;
       const size_t per_cta = static_cast<size_t>(plan->arena) + 5ull * plan->tmp_w;
+      const std::uint64_t by_mem = std::max<std::uint64_t>(1, (std::uint64_t{4} << 30) / (per_cta * 8));
+      const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
+          {n, static_cast<std::uint64_t>(sms) * (1024 / threads), by_mem}));
       void* scratch = nullptr;
       check_cuda(cudaMallocAsync(&scratch, grid * per_cta * 8, s), "cudaMallocAsync(wide arena)");
       owned.push_back(scratch);
@@ -525,8 +532,8 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
                                 static_cast<const std::uint32_t*>(dv.coef_w),
                                 static_cast<const std::uint64_t*>(dv.coef_words), p.nvars, din.data(),
                                 point_limbs, dout, out_limbs, plan->result, plan->result_limbs,
-                                plan->arena, plan->tmp_w, static_cast<std::uint64_t*>(scratch), grid, n,
-                                s),
+                                plan->arena, plan->tmp_w, static_cast<std::uint64_t*>(scratch), grid,
+                                threads, n, s),
                  "launch(wide walk)");
       launch_counter().fetch_add(1, std::memory_order_relaxed);
       if (kind != MemKind::Device) {

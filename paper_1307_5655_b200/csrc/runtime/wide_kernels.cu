@@ -24,8 +24,8 @@
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kMaxThreads = 256;  // CTA size is chosen per plan (32..256)
+constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr std::uint32_t kCoef = 0x80000000u, kZero = 0x40000000u;
 constexpr int kMaxVars = 16;
 
@@ -58,6 +58,7 @@ __device__ __forceinline__ std::uint64_t limb(const Num& x, std::uint32_t k) {
 // Returns this thread's carry in (chunks are ordered by thread index).
 __device__ bool block_carry_in(bool g, bool p, bool cin0, std::uint32_t* s_pair) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
   // inclusive scan of (g, p) pairs: (g2,p2) o (g1,p1) = (g2 | (p2 & g1), p2 & p1)
   // represented as carry-out given carry-in 0 / 1
   bool c0 = g, c1 = p;
@@ -74,14 +75,14 @@ __device__ bool block_carry_in(bool g, bool p, bool cin0, std::uint32_t* s_pair)
   __syncthreads();
   if (threadIdx.x == 0) {
     bool c = cin0;
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < nwarps; ++w) {
       const std::uint32_t t = s_pair[w];
-      s_pair[kWarps + w] = c ? 1u : 0u;  // carry into warp w
+      s_pair[nwarps + w] = c ? 1u : 0u;  // carry into warp w
       c = c ? (t & 2u) : (t & 1u);
     }
   }
   __syncthreads();
-  const bool wcin = s_pair[kWarps + warp] != 0;
+  const bool wcin = s_pair[nwarps + warp] != 0;
   // carry into this lane = exclusive scan applied to the warp's carry in
   const bool e0 = __shfl_up_sync(0xffffffffu, c0, 1), e1 = __shfl_up_sync(0xffffffffu, c1, 1);
   const bool cin = lane == 0 ? wcin : (wcin ? e1 : e0);
@@ -94,7 +95,8 @@ __device__ bool block_carry_in(bool g, bool p, bool cin0, std::uint32_t* s_pair)
 // holds an operand).
 __device__ void big_add(std::uint64_t* r, std::uint32_t w, const Num& x, const Num& y, bool cin0,
                         std::uint32_t* s_pair) {
-  const std::uint32_t chunk = (w + kThreads - 1) / kThreads;
+  const std::uint32_t T = blockDim.x;
+  const std::uint32_t chunk = (w + T - 1) / T;
   const std::uint32_t lo = threadIdx.x * chunk, hi = min(w, lo + chunk);
   bool g = false, p = true;  // carry out for carry in 0 / 1 over [lo, hi)
   for (std::uint32_t k = lo; k < hi; ++k) {
@@ -122,7 +124,8 @@ __device__ void big_add(std::uint64_t* r, std::uint32_t w, const Num& x, const N
 // r = -x over w limbs (~x + 1)
 __device__ void big_neg(std::uint64_t* r, std::uint32_t w, const Num& x, std::uint32_t* s_pair,
                         std::uint64_t* tmp) {
-  for (std::uint32_t k = threadIdx.x; k < w; k += kThreads) tmp[k] = ~limb(x, k);
+  const std::uint32_t T = blockDim.x;
+  for (std::uint32_t k = threadIdx.x; k < w; k += T) tmp[k] = ~limb(x, k);
   __syncthreads();
   big_add(r, w, Num{tmp, w}, Num{nullptr, 0}, true, s_pair);
 }
@@ -138,6 +141,7 @@ struct Tmp {
 // operand nor a scratch buffer.
 __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const Tmp& t,
                         std::uint32_t* s_pair) {
+  const std::uint32_t T = blockDim.x;
   const bool nx = negative(x), ny = negative(y);
   if (nx) {  // magnitudes (the top limb may then use the sign bit: read as unsigned)
     big_neg(t.ta, x.w, x, s_pair, t.c0);
@@ -160,7 +164,7 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
   const std::uint32_t wa = s_w[0], wb = s_w[1];
   // column k: sum_i a_i * b_(k-i) as 192 bits (c0, c1, c2); thread t owns
   // columns t, t + T, ...
-  for (std::uint32_t k = threadIdx.x; k < w; k += kThreads) {
+  for (std::uint32_t k = threadIdx.x; k < w; k += T) {
     std::uint64_t a0 = 0, a1 = 0, a2 = 0;
     const std::uint32_t i_lo = k + 1 > wb ? k + 1 - wb : 0, i_hi = min(k + 1, wa);
     for (std::uint32_t i = i_lo; i < i_hi; ++i) {
@@ -182,7 +186,7 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
   __syncthreads();
   // product = c0 + (c1 << 64) + (c2 << 128); every part is <= the product,
   // so each fits w limbs with the sign bit clear (the shifted-out limbs are 0)
-  for (std::uint32_t k = threadIdx.x; k < w; k += kThreads) {
+  for (std::uint32_t k = threadIdx.x; k < w; k += T) {
     t.ta[k] = k >= 1 ? t.c1[k - 1] : 0;
     t.tb[k] = k >= 2 ? t.c2[k - 2] : 0;
   }
@@ -206,8 +210,9 @@ __device__ Num operand(const WideArgs& a, std::uint64_t* arena, std::uint32_t o,
   return Num{arena + a.slot_off[o], w};
 }
 
-__global__ void __launch_bounds__(kThreads) wide_walk_kernel(const WideArgs a) {
-  __shared__ std::uint32_t s_pair[2 * kWarps];
+__global__ void __launch_bounds__(kMaxThreads) wide_walk_kernel(const WideArgs a) {
+  const std::uint32_t T = blockDim.x;
+  __shared__ std::uint32_t s_pair[2 * kMaxWarps];
   std::uint64_t* arena = a.scratch + static_cast<size_t>(blockIdx.x) * (a.arena + 5ull * a.tmp_w);
   Tmp t;
   t.ta = arena + a.arena;
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) wide_walk_kernel(const WideArgs a) {
     for (std::uint32_t v = 0; v < a.nvars; ++v) {
       const Num x{a.in[v] + i * a.point_limbs, a.point_limbs};
       std::uint64_t* d = arena + a.slot_off[v];
-      for (std::uint32_t k = threadIdx.x; k < a.slot_w[v]; k += kThreads) d[k] = limb(x, k);
+      for (std::uint32_t k = threadIdx.x; k < a.slot_w[v]; k += T) d[k] = limb(x, k);
     }
     __syncthreads();
     for (std::uint32_t op = 0; op < a.nops; ++op) {
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(kThreads) wide_walk_kernel(const WideArgs a) {
     }
     const Num res = operand(a, arena, a.result, a.result_w);
     std::uint64_t* o = a.out + i * a.out_limbs;
-    for (std::uint32_t k = threadIdx.x; k < a.out_limbs; k += kThreads) o[k] = limb(res, k);
+    for (std::uint32_t k = threadIdx.x; k < a.out_limbs; k += T) o[k] = limb(res, k);
     __syncthreads();
   }
 }
@@ -253,7 +258,8 @@ extern "C" cudaError_t pe_launch_wide(const std::uint32_t* code, std::uint32_t n
                                       std::uint32_t result, std::uint32_t result_w,
                                       std::uint32_t arena,
                                       std::uint32_t tmp_w, std::uint64_t* scratch,
-                                      unsigned grid, unsigned long long n, cudaStream_t stream) {
+                                      unsigned grid, unsigned threads, unsigned long long n,
+                                      cudaStream_t stream) {
   if (nvars > kMaxVars) return cudaErrorInvalidValue;
   if (n == 0) return cudaSuccess;
   WideArgs a{};
@@ -275,8 +281,8 @@ extern "C" cudaError_t pe_launch_wide(const std::uint32_t* code, std::uint32_t n
   a.result_w = result_w;
   a.arena = arena;
   a.tmp_w = tmp_w;
-  wide_walk_kernel<<<grid, kThreads, 0, stream>>>(a);
+  if (threads < 32 || threads > kMaxThreads || threads % 32) return cudaErrorInvalidValue;
+  wide_walk_kernel<<<grid, threads, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
-extern "C" unsigned pe_wide_threads(void) { return kThreads; }

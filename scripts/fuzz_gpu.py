@@ -8,7 +8,11 @@ oracle: fp64 strict and intervals bit-exact, fused fp64 within 1e-12·Σ|terms|,
 int64 exact, K-limb integers word-exact against the unmodified reference.
 Prints one JSON summary line; any mismatch is reported with its seed.
 
-  python scripts/fuzz_gpu.py [seconds] [first_seed]
+  python scripts/fuzz_gpu.py [seconds] [first_seed] [tuning]
+
+tuning: comma-separated pe_tuning fields applied to every program (default
+jit_mode=1: the specialised kernels), e.g. "jit_mode=2" (walk VM only) or
+"jit_mode=1,section_ops=200,group_tiles=3" (every larger walk sectioned).
 """
 import json
 import os
@@ -131,6 +135,10 @@ def check(seed):
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
+    tune = {"jit_mode": 1}
+    if len(sys.argv) > 3:
+        tune = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[3].split(",") if kv)}
+    pe.set_default_tuning(**tune)
     t0 = time.time()
     cases, checks, failures = 0, {}, []
     while time.time() - t0 < budget:
@@ -143,7 +151,7 @@ def main():
                              "where": traceback.format_exc().splitlines()[-2][:200]})
         cases += 1
         seed += 1
-    print(json.dumps({"cases": cases, "checks": checks, "failures": failures,
+    print(json.dumps({"cases": cases, "checks": checks, "failures": failures, "tuning": tune,
                       "seconds": round(time.time() - t0, 1)}), flush=True)
 
 
