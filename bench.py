@@ -141,7 +141,7 @@ class ClockSampler:
 # several rows (the launches of one evaluate call) is summed
 NCU_CAPTURES = {
     ("c4", "C4_trivariate_sparse10k"): "profiles/r2_ncu_c4_raw.csv",
-    ("c5", "C5_interval_estrin_d200"): "profiles/r2_ncu_c5_raw.csv",
+    ("c5", "C5_interval_estrin_d200"): "profiles/r2_ncu_c5_split_raw.csv",
     ("c2", "C2_estrin_d1000"): "profiles/r1_ncu_c2_estrin_d1000_raw.csv",
     ("c2", "C2_balanced_d1000"): "profiles/r1_ncu_c2_balanced_d1000_raw.csv",
     ("c2", "C2_estrin_d1023"): "profiles/r1_ncu_c2_estrin_d1023_raw.csv",
@@ -506,7 +506,11 @@ def run_native(args, world, rank, local):
     if domain == "f64" and sections > 1:
         kernel_name = (f"pe_walk_f64 [{wls[top].name}]: one persistent kernel, {sections} sections "
                        "(pe_section0..) over groups of 4 tiles")
-    if domain == "interval" and "pe_walk_interval_pos" in progs[top].ptx(pe.DOMAIN_INTERVAL):
+    iv_ptx = progs[top].ptx(pe.DOMAIN_INTERVAL) if domain == "interval" else ""
+    if "pe_walk_interval_split" in iv_ptx:
+        kernel_name = (f"pe_walk_interval_split + pe_walk_interval_fix [{wls[top].name}] (one "
+                       "evaluate call: one-pass sign split, then the fixup replay)")
+    elif "pe_walk_interval_pos" in iv_ptx:
         kernel_name = (f"classify_intervals + pe_walk_interval_pos + pe_walk_interval_neg + "
                        f"pe_walk_interval_fix [{wls[top].name}] (one evaluate call, sign-partitioned)")
     roofline = {

@@ -182,6 +182,30 @@ class Emitter {
     if (K_ > 8) throw std::invalid_argument("at most 8 limbs");
   }
 
+  /// The interval fast path of this program for one point as a function
+  /// `name(lo, hi) -> (lo, hi, slow)`, preceded by its constant array under
+  /// symbol `sym` (the split kernel's mirrored half lives in the program's
+  /// module). Empty when the coefficients do not all fit the constant bank.
+  std::string point_module(const std::string& name, std::uint32_t role, const std::string& sym) {
+    sym_ = sym;
+    assign_words();
+    if (!(n_param_ == 0 && n_global_ == 0 && n_smem_ == 0) || !interval_fast_path_ok()) return {};
+    const_words_ = n_const_;
+    std::ostringstream m;
+    m << ".const .align 16 .b64 " << sym_ << "[" << n_const_ << "] = {";
+    for (std::uint32_t i = 0; i < n_const_; ++i) {
+      if (i) m << (i % 8 == 0 ? ",\n  " : ", ");
+      m << hex64(words_[i]);
+    }
+    m << "};\n\n" << point_function(name, role);
+    return m.str();
+  }
+  std::uint32_t const_words() const { return const_words_; }
+  void set_split_funcs(std::string text, std::uint32_t mirror_words) {
+    split_funcs_ = std::move(text);
+    mirror_words_ = mirror_words;
+  }
+
   KernelImage run() {
     KernelImage img;
     img.domain = d_;
@@ -212,6 +236,11 @@ class Emitter {
 
     const bool part = fast && part_ != 0 && s_.nvars == 1;
     img.iv_partition = part ? part_ : 0;
+    // one-pass sign split (the program's and the mirrored program's point
+    // functions in this module): when both coefficient sets fit the bank
+    const bool split = part && part_ == 1 && !split_funcs_.empty() && n_param_ == 0 &&
+                       n_global_ == 0 && n_const_ + mirror_words_ <= CoefTiers::kConstCap;
+    if (split) img.iv_partition = 3;
     if (part && part_ == 2) {
       // mirrored program: only the negative-coordinate entry
       img.entry += "_neg";
@@ -310,7 +339,16 @@ class Emitter {
 
     // positive-coordinate entry of the sign-partitioned fast path
     std::string part_entry;
-    if (part) {
+    if (split) {
+      funcs_ += ".shared .align 8 .b64 pe_sp_lo[512];\n.shared .align 8 .b64 pe_sp_hi[512];\n"
+                ".shared .align 4 .b32 pe_sp_idx[512];\n.shared .align 4 .b32 pe_sp_w[72];\n\n";
+      funcs_ += split_funcs_ + point_function("pe_iv_pos", 1);
+      img.part_entry = img.entry + "_split";
+      reset_entry();
+      emit_split_entry();
+      finish_entry();
+      part_entry = entry_text(img, img.part_entry, 0, 0);
+    } else if (part) {
       img.part_entry = img.entry + "_pos";
       reset_entry();
       gather_ = 1;
@@ -342,7 +380,7 @@ class Emitter {
         << ".shared .align 8 .b64 pe_mbar;\n\n";
     }
     if (n_const_ > 0) {
-      m << ".const .align 16 .b64 pe_coef[" << n_const_ << "] = {";
+      m << ".const .align 16 .b64 " << sym_ << "[" << n_const_ << "] = {";
       for (std::uint32_t i = 0; i < n_const_; ++i) {
         if (i) m << (i % 8 == 0 ? ",\n  " : ", ");
         m << hex64(words_[i]);
@@ -1884,6 +1922,157 @@ class Emitter {
     body_ << ");\n  }\n  add.u64 %rd1, %rd1, %rd4;\n  bra $Lfix;\n";
   }
 
+  // ---------------- one-pass sign split (interval fast path) ----------------
+  // role 1: the program at [lo, hi] with lo > 0; role 2: the mirrored
+  // program q(y) = p(-y) at [-hi, -lo] (hi < 0). Statically positive
+  // coordinate, no straddle checks (the split kernel classified it).
+  std::string point_function(const std::string& name, std::uint32_t role) {
+    const std::uint32_t lanes = P_;
+    P_ = 1;
+    reset_entry();
+    decls_ << "  .reg .f64 " << xr(0, 0, false) << ", " << xr(0, 0, true) << ";\n"
+           << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n  .reg .pred %pb<4>;\n";
+    body_ << "  ld.param.f64 " << xr(0, 0, false) << ", [pe_a_lo];\n"
+          << "  ld.param.f64 " << xr(0, 0, true) << ", [pe_a_hi];\n";
+    if (role == 2) {
+      const std::string t = tmp_f();
+      body_ << "  neg.f64 " << t << ", " << xr(0, 0, true) << ";\n"
+            << "  neg.f64 " << xr(0, 0, true) << ", " << xr(0, 0, false) << ";\n"
+            << "  mov.f64 " << xr(0, 0, false) << ", " << t << ";\n";
+    }
+    body_ << "  mov.b64 %facc, 0;\n  mov.u32 %r3, 0;\n";
+    for (int i = 0; i < 4; ++i) body_ << "  setp.ne.b32 %pb" << i << ", %r3, %r3;\n";
+    fast_ = true;
+    gather_ = role;
+    emit_powers();
+    emit_walk();
+    const std::string rl = reg(s_.result.id, 0, false), rh = reg(s_.result.id, 0, true);
+    fcheck_finite(rl);
+    fcheck_finite(rh);
+    for (const std::string* r : {&rl, &rh}) {  // a zero result may carry the wrong sign
+      body_ << "  setp.eq.or.f64 %pb" << (nb_ & 3) << ", " << *r << ", 0d0000000000000000, %pb"
+            << (nb_ & 3) << ";\n";
+      ++nb_;
+    }
+    body_ << "  setp.lt.s64 %pslow, %facc, 0;\n"
+          << "  or.pred %pslow, %pslow, %pb0;\n  or.pred %pslow, %pslow, %pb1;\n"
+          << "  or.pred %pslow, %pslow, %pb2;\n  or.pred %pslow, %pslow, %pb3;\n"
+          << "  selp.u32 pe_r_slow, 1, 0, %pslow;\n"
+          << "  mov.f64 pe_r_lo, " << rl << ";\n  mov.f64 pe_r_hi, " << rh << ";\n";
+    fast_ = false;
+    gather_ = 0;
+    body_ << "  ret;\n";
+    if (n_creg_ > 0) decls_ << "  .reg ." << ldty() << " %c<" << n_creg_ << ">;\n";
+    if (n_tf_ > 0) decls_ << "  .reg .f64 %tf<" << n_tf_ << ">;\n";
+    if (n_tu_ > 0) decls_ << "  .reg .b64 %tu<" << n_tu_ << ">;\n";
+    if (n_tp_ > 0) decls_ << "  .reg .pred %tp<" << n_tp_ << ">;\n";
+    if (n_tr_ > 0) decls_ << "  .reg .b32 %tr<" << n_tr_ << ">;\n";
+    std::ostringstream f;
+    f << ".func (.reg .f64 pe_r_lo, .reg .f64 pe_r_hi, .reg .b32 pe_r_slow) " << name
+      << "(.param .f64 pe_a_lo, .param .f64 pe_a_hi)\n{\n"
+      << "  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n" << decls_.str()
+      << body_.str() << "}\n\n";
+    P_ = lanes;
+    return f.str();
+  }
+
+  // The split entry: each CTA takes ntid consecutive intervals, classifies
+  // them (lo > 0 / hi < 0 / the rest -> fixup list, invalid -> status bit 2),
+  // packs the two signs into shared memory (warp ballots + a CTA prefix), and
+  // thread t evaluates packed slot t with the program's (x > 0) or the
+  // mirrored program's (x < 0) point function. Warps are sign-uniform except
+  // the one at the boundary. Each interval is read and written once (the
+  // classifier + gather path read every input sector twice).
+  void emit_split_entry() {
+    decls_ << "  .reg .b64 %sl, %sh, %ix<1>, %sa, %sb;\n  .reg .pred %pv<1>, %sp, %sn, %so, %sx;\n"
+           << "  .reg .b32 %smp, %smn, %slt, %sw, %slane, %sslot, %sq, %sfl;\n"
+           << "  .reg .f64 %sxl, %sxh, %srl, %srh;\n";
+    body_ << "  mov.u32 %r1, %ctaid.x;\n  mov.u32 %r2, %ntid.x;\n  mov.u32 %r3, %tid.x;\n"
+          << "  mul.wide.u32 %rd1, %r1, %r2;\n  cvt.u64.u32 %rd2, %r3;\n  add.u64 %rd13, %rd1, %rd2;\n"
+          << "  ld.param.u64 %rd3, [pe_n];\n  sub.u64 %rd12, %rd3, 1;\n"
+          << "  setp.lt.u64 %pv0, %rd13, %rd3;\n  min.u64 %rd13, %rd13, %rd12;\n"
+          << "  shl.b64 %ix0, %rd13, 3;\n"
+          << "  ld.param.u64 %rd5, [pe_in0];\n  cvta.to.global.u64 %rd5, %rd5;\n"
+          << "  add.u64 %rd6, %rd5, %ix0;\n  ld.global.nc.f64 %sxl, [%rd6];\n"
+          << "  ld.param.u64 %rd5, [pe_in1];\n  cvta.to.global.u64 %rd5, %rd5;\n"
+          << "  add.u64 %rd6, %rd5, %ix0;\n  ld.global.nc.f64 %sxh, [%rd6];\n"
+          << "  ld.param.u64 %rd7, [pe_flag];\n  cvta.to.global.u64 %rd7, %rd7;\n"
+          << "  ld.param.u64 %rd14, [pe_count];\n  cvta.to.global.u64 %rd14, %rd14;\n"
+          << "  ld.param.u64 %rd15, [pe_list];\n  cvta.to.global.u64 %rd15, %rd15;\n"
+          << "  ld.param.u64 %rd16, [pe_cap];\n"
+          // classify (reference Interval(lo, hi) rejects NaN / lo > hi)
+          << "  setp.le.f64 %sx, %sxl, %sxh;\n  and.pred %sx, %sx, %pv0;\n"
+          << "  setp.gt.f64 %sp, %sxl, 0d0000000000000000;\n  and.pred %sp, %sp, %sx;\n"
+          << "  setp.lt.f64 %sn, %sxh, 0d0000000000000000;\n  and.pred %sn, %sn, %sx;\n"
+          << "  or.pred %so, %sp, %sn;\n  not.pred %so, %so;\n  and.pred %so, %so, %pv0;\n"
+          << "  not.pred %p2, %sx;\n  and.pred %p2, %p2, %pv0;\n"
+          << "  @%p2 atom.global.or.b32 %r6, [%rd7], 2;\n";
+    // the rest go to the fixup list (rare)
+    auto append = [&](const char* pred, const char* index_reg) {
+      body_ << "  @" << pred << " atom.global.add.u32 %r4, [%rd14], 1;\n"
+            << "  cvt.u64.u32 %rd17, %r4;\n  setp.lt.u64 %p3, %rd17, %rd16;\n"
+            << "  not.pred %p4, %p3;\n  and.pred %p4, %p4, " << pred << ";\n"
+            << "  @%p4 atom.global.or.b32 %r6, [%rd7], 4;\n"
+            << "  and.pred %p3, %p3, " << pred << ";\n"
+            << "  cvt.u32.u64 %r5, " << index_reg << ";\n"
+            << "  shl.b64 %rd17, %rd17, 2;\n  add.u64 %rd17, %rd15, %rd17;\n"
+            << "  @%p3 st.global.u32 [%rd17], %r5;\n";
+    };
+    body_ << "  add.u64 %rd18, %rd1, %rd2;\n";
+    append("%so", "%rd18");
+    // pack: warp ballots, then a CTA prefix over the warps
+    body_ << "  and.b32 %slane, %r3, 31;\n  shr.u32 %sw, %r3, 5;\n"
+          << "  mov.u32 %r4, 1;\n  shl.b32 %slt, %r4, %slane;\n  sub.u32 %slt, %slt, 1;\n"
+          << "  vote.sync.ballot.b32 %smp, %sp, 0xffffffff;\n"
+          << "  vote.sync.ballot.b32 %smn, %sn, 0xffffffff;\n"
+          << "  setp.eq.u32 %p5, %slane, 0;\n  mov.u64 %sa, pe_sp_w;\n"
+          << "  mul.wide.u32 %sb, %sw, 4;\n  add.u64 %sb, %sa, %sb;\n"
+          << "  popc.b32 %r4, %smp;\n  @%p5 st.shared.u32 [%sb], %r4;\n"
+          << "  popc.b32 %r4, %smn;\n  @%p5 st.shared.u32 [%sb+64], %r4;\n"
+          << "  bar.sync 0;\n"
+          << "  setp.ne.u32 %p5, %r3, 0;\n  @%p5 bra $Lsplit_scanned;\n"
+          << "  shr.u32 %r5, %r2, 5;\n  mov.u32 %r6, 0;\n  mov.u32 %r7, 0;\n  mov.u32 %r4, 0;\n"
+          << "$Lsplit_scan:\n  setp.ge.u32 %p6, %r4, %r5;\n  @%p6 bra $Lsplit_scan_done;\n"
+          << "  mul.wide.u32 %sb, %r4, 4;\n  add.u64 %sb, %sa, %sb;\n"
+          << "  ld.shared.u32 %sq, [%sb];\n  st.shared.u32 [%sb+128], %r6;\n  add.u32 %r6, %r6, %sq;\n"
+          << "  ld.shared.u32 %sq, [%sb+64];\n  st.shared.u32 [%sb+192], %r7;\n  add.u32 %r7, %r7, %sq;\n"
+          << "  add.u32 %r4, %r4, 1;\n  bra $Lsplit_scan;\n$Lsplit_scan_done:\n"
+          << "  st.shared.u32 [pe_sp_w+256], %r6;\n  st.shared.u32 [pe_sp_w+260], %r7;\n"
+          << "$Lsplit_scanned:\n  bar.sync 0;\n"
+          << "  ld.shared.u32 %r6, [pe_sp_w+256];\n  ld.shared.u32 %r7, [pe_sp_w+260];\n"
+          << "  mul.wide.u32 %sb, %sw, 4;\n  add.u64 %sb, %sa, %sb;\n"
+          << "  and.b32 %r4, %smp, %slt;\n  popc.b32 %r4, %r4;\n  ld.shared.u32 %r5, [%sb+128];\n"
+          << "  add.u32 %sslot, %r5, %r4;\n"
+          << "  and.b32 %r4, %smn, %slt;\n  popc.b32 %r4, %r4;\n  ld.shared.u32 %r5, [%sb+192];\n"
+          << "  add.u32 %r5, %r5, %r4;\n  add.u32 %r5, %r5, %r6;\n  selp.u32 %sslot, %sslot, %r5, %sp;\n"
+          << "  or.pred %p5, %sp, %sn;\n  @!%p5 bra $Lsplit_packed;\n"
+          << "  mul.wide.u32 %sb, %sslot, 8;\n  mov.u64 %sa, pe_sp_lo;\n  add.u64 %sa, %sa, %sb;\n"
+          << "  st.shared.f64 [%sa], %sxl;\n  mov.u64 %sa, pe_sp_hi;\n  add.u64 %sa, %sa, %sb;\n"
+          << "  st.shared.f64 [%sa], %sxh;\n  mul.wide.u32 %sb, %sslot, 4;\n  mov.u64 %sa, pe_sp_idx;\n"
+          << "  add.u64 %sa, %sa, %sb;\n  st.shared.u32 [%sa], %r3;\n"
+          << "$Lsplit_packed:\n  bar.sync 0;\n"
+          // slot tid: x > 0 (program) or x < 0 (mirrored program)
+          << "  add.u32 %r5, %r6, %r7;\n  setp.ge.u32 %p5, %r3, %r5;\n  @%p5 bra $Ldone;\n"
+          << "  mul.wide.u32 %sb, %r3, 8;\n  mov.u64 %sa, pe_sp_lo;\n  add.u64 %sa, %sa, %sb;\n"
+          << "  ld.shared.f64 %sxl, [%sa];\n  mov.u64 %sa, pe_sp_hi;\n  add.u64 %sa, %sa, %sb;\n"
+          << "  ld.shared.f64 %sxh, [%sa];\n  mul.wide.u32 %sb, %r3, 4;\n  mov.u64 %sa, pe_sp_idx;\n"
+          << "  add.u64 %sa, %sa, %sb;\n  ld.shared.u32 %r4, [%sa];\n"
+          << "  cvt.u64.u32 %rd18, %r4;\n  add.u64 %rd18, %rd1, %rd18;\n"
+          << "  setp.lt.u32 %p6, %r3, %r6;\n"
+          << "  {\n  .param .f64 a0;\n  .param .f64 a1;\n"
+          << "  st.param.f64 [a0], %sxl;\n  st.param.f64 [a1], %sxh;\n"
+          << "  @!%p6 bra $Lsplit_neg;\n  call (%srl, %srh, %sfl), pe_iv_pos, (a0, a1);\n"
+          << "  bra $Lsplit_called;\n"
+          << "$Lsplit_neg:\n  call (%srl, %srh, %sfl), pe_iv_neg, (a0, a1);\n$Lsplit_called:\n  }\n"
+          << "  setp.ne.u32 %p7, %sfl, 0;\n";
+    append("%p7", "%rd18");
+    body_ << "  @%p7 bra $Ldone;\n  shl.b64 %rd18, %rd18, 3;\n"
+          << "  ld.param.u64 %rd9, [pe_out0];\n  cvta.to.global.u64 %rd9, %rd9;\n"
+          << "  add.u64 %rd10, %rd9, %rd18;\n  st.global.f64 [%rd10], %srl;\n"
+          << "  ld.param.u64 %rd9, [pe_out1];\n  cvta.to.global.u64 %rd9, %rd9;\n"
+          << "  add.u64 %rd10, %rd9, %rd18;\n  st.global.f64 [%rd10], %srh;\n";
+  }
+
   void emit_epilogue() {
     emit_store();
     finish_entry();
@@ -1942,7 +2131,9 @@ class Emitter {
   std::uint32_t sec_ = 0;          // section being emitted
   std::uint32_t group_tiles_ = 4;  // sectioned kernels: tiles per CTA per section pass
   std::string funcs_;              // sectioned kernels: the section functions
-  std::string cbase() const { return "pe_coef"; }
+  std::string sym_ = "pe_coef";    // name of the module's constant-bank coefficient array
+  std::string cbase() const { return sym_; }
+  std::string split_funcs_;        // the mirrored program's point function (+ its constants)
   bool fast_ = false;  // emitting the interval fast path
   bool medium_ = false;  // emitting the finite-case replay of the fixup entry
   std::uint32_t gather_ = 0;  // emitting a partitioned entry: 1 front (x > 0), 2 back (x < 0)
@@ -1964,6 +2155,7 @@ class Emitter {
   std::vector<char> reg_bound_;  // coefficient in the register-bound region
   std::vector<std::uint32_t> coef_lo_, coef_hi_;
   std::uint32_t n_const_ = 0, n_param_ = 0, n_smem_ = 0, n_global_ = 0;
+  std::uint32_t const_words_ = 0, mirror_words_ = 0;
   std::uint32_t n_creg_ = 0, n_tf_ = 0, n_tu_ = 0, n_tp_ = 0, n_tr_ = 0;
   std::uint64_t fp_ops_ = 0, int_ops_ = 0;
   std::ostringstream body_, decls_;
@@ -2104,9 +2296,12 @@ std::vector<std::size_t> section_cuts(const Stream<C>& s, std::size_t target) {
 }
 }  // namespace
 
+// the split entry stages one interval per thread in 512-entry shared arrays
+inline bool block_ok(std::uint32_t block) { return block <= 512; }
+
 template <typename C>
 KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shape,
-                     const Tuning& tuning) {
+                     const Tuning& tuning, const Stream<C>* mirror) {
   const bool scalar = domain == Domain::F64 || domain == Domain::F64Strict ||
                       domain == Domain::I64 || domain == Domain::I64F;
   // Long scalar walks are emitted in sections (Emitter::emit_sectioned);
@@ -2154,12 +2349,23 @@ KernelImage emit_ptx(const Stream<C>& stream_in, Domain domain, KernelShape shap
   if (shape.min_ctas == 0) shape.min_ctas = def.min_ctas;
   if (shape.limbs == 0) shape.limbs = 1;
   Emitter<C> e(stream, domain, shape, tuning, cuts);
+  if (mirror && domain == Domain::Interval && shape.iv_partition == 1 && block_ok(shape.block)) {
+    // the one-pass sign split: the mirrored program's point function joins
+    // this module under its own constant array
+    KernelShape ms = shape;
+    ms.iv_partition = 2;
+    Emitter<C> eq(*mirror, domain, ms, tuning, {mirror->ops.size()});
+    std::string text = eq.point_module("pe_iv_neg", 2, "pe_qcoef");
+    if (!text.empty()) e.set_split_funcs(std::move(text), eq.const_words());
+  }
   KernelImage img = e.run();
   img.iv_partition_min = tuning.iv_partition_min ? tuning.iv_partition_min : 65536;
   return img;
 }
 
-template KernelImage emit_ptx(const Stream<double>&, Domain, KernelShape, const Tuning&);
-template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, KernelShape, const Tuning&);
+template KernelImage emit_ptx(const Stream<double>&, Domain, KernelShape, const Tuning&,
+                              const Stream<double>*);
+template KernelImage emit_ptx(const Stream<std::int64_t>&, Domain, KernelShape, const Tuning&,
+                              const Stream<std::int64_t>*);
 
 }  // namespace polyeval::lower

@@ -64,6 +64,8 @@ struct KernelImage {
   // index list); 2 = module of the mirrored program q(y) = p(-y) whose only
   // entry `entry` takes points with x < 0 from the back of the list and
   // evaluates q at -x. Both entries take two extra parameters (list, counts).
+  // 3 = `part_entry` is the one-pass split kernel (classify, pack by sign in
+  // shared memory, evaluate p or q per packed slot); no mirror module.
   std::uint32_t iv_partition = 0;
   std::string part_entry;
   std::uint64_t iv_partition_min = 65536;  // smaller batches skip the partition
@@ -90,7 +92,7 @@ struct Tuning {
   std::uint32_t chain_min = 0;    // shortest Hörner run emitted as a loop; UINT32_MAX = never
   std::int32_t iv_fast = 0;       // interval fast path + fixup list (-1 = bit-level replay only)
   std::int32_t iv_mid = 0;        // fixup: finite-case replay first (-1 = bit-level only)
-  std::int32_t iv_partition = 0;  // univariate sign partition (-1 = off)
+  std::int32_t iv_partition = 0;  // univariate sign partition (-1 off, 2 = classifier path only)
   std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 4)
   std::int32_t word_layout = 0;   // sections: -1 = all uniform-bound words first (no per-section blocks)
   std::int32_t jit_mode = 0;      // 0 walk VM until the kernel is compiled, 1 always wait, 2 VM only
@@ -122,8 +124,12 @@ struct KernelShape {
 KernelShape default_shape(Domain d, std::uint32_t powers, std::uint64_t distinct_coefs,
                           const Tuning& t);
 
+/// `mirror` (interval domain, univariate, shape.iv_partition == 1): the
+/// strict stream of q(y) = p(-y) (mirror_stream); when both programs'
+/// coefficients fit the constant bank the module gains the one-pass sign
+/// split entry (KernelImage::iv_partition 3).
 template <typename C>
 KernelImage emit_ptx(const Stream<C>& stream, Domain domain, KernelShape shape = {},
-                     const Tuning& tuning = {});
+                     const Tuning& tuning = {}, const Stream<C>* mirror = nullptr);
 
 }  // namespace polyeval::lower

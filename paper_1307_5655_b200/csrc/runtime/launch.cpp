@@ -242,6 +242,8 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   }
   // below ~64K intervals the extra launches outweigh the cheaper walk
   const bool part = a.partitioned() && la.n <= 0xffffffffull && la.n >= img.iv_partition_min;
+  // one-pass sign split (iv_partition 3): classify + pack + walk in one kernel
+  const bool split = img.iv_partition == 3 && la.n <= 0xffffffffull && la.n >= img.iv_partition_min;
   void* scratch = nullptr;  // partition: n u32 point indices + 2 u32 list lengths
   if (part) {
     keep_pool_memory(device);
@@ -292,7 +294,11 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   const std::uint64_t tile = block * img.lanes;
   const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
-  if (!part) {
+  if (split) {
+    launch_one(a.part_kernel, dev_ok ? a.part_fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
+               dim3(static_cast<unsigned>(block)), args.data(), stream, "launch(walk split)");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+  } else if (!part) {
     launch_one(a.kernel, dev_ok ? a.fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
                dim3(static_cast<unsigned>(block)), args.data(), stream, "launch(walk)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);

@@ -114,9 +114,14 @@ void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, const
   lower::KernelShape shape;
   if (nvars == 1 && t.iv_partition >= 0) shape.iv_partition = 1;
   const auto s = lower::lower_strict(prog);
-  a.image = lower::emit_ptx(s, lower::Domain::Interval, shape, t);
   lower::Stream<C> q;
-  if (a.image.iv_partition != 1 || !lower::mirror_stream(s, &q)) return;
+  const bool mirrored = shape.iv_partition == 1 && lower::mirror_stream(s, &q);
+  // tuning iv_partition 2: the classifier path even where the split fits
+  a.image = lower::emit_ptx(s, lower::Domain::Interval, shape, t,
+                            mirrored && t.iv_partition != 2 ? &q : nullptr);
+  // iv_partition 3: the split kernel carries both programs; 1: the
+  // classifier path needs the mirrored program's module
+  if (a.image.iv_partition != 1 || !mirrored) return;
   lower::KernelShape ms;
   ms.iv_partition = 2;
   auto m = std::make_unique<Artifact>();

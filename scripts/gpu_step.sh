@@ -1,4 +1,5 @@
-O=gpurun_out/g16; mkdir -p $O
-timeout 1200 python -m pytest tests/test_gpu_wide.py tests/test_gpu_edges.py -x -q -k "wide or sliced or section" > $O/pytest_wide.log 2>&1; echo "pytest exit $?" >> $O/pytest_wide.log
-timeout 1500 python scripts/fig1_grid.py --quick > $O/fig1_quick.jsonl 2>&1
-timeout 2000 bash scripts/ncu_captures.sh c4 c2e1000 c3
+O=gpurun_out/g17; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_wide.py -x -q > $O/pytest_wide.log 2>&1; echo "pytest exit $?" >> $O/pytest_wide.log
+timeout 1800 python scripts/fig1_grid.py > $O/fig1_grid.jsonl 2>&1
+timeout 500 python scripts/fuzz_gpu.py 420 140000 jit_mode=1,section_ops=150,group_tiles=3 > $O/fuzz_sections.json 2>&1
+timeout 500 python scripts/fuzz_gpu.py 420 150000 jit_mode=2 > $O/fuzz_vm.json 2>&1

@@ -507,12 +507,15 @@ def test_chain_loops_inside_nested_programs(cuda_device):
 
 @pytest.mark.parametrize("n", [1, 5, 33, 4097, 150_001])
 @pytest.mark.parametrize("scheme", ["estrin", "horner", "balanced"])
-def test_interval_sign_partition_bit_exact(n, scheme, cuda_device):
-    # Sign-partitioned fast path: x > 0 intervals run the program's x > 0
-    # entry, x < 0 intervals the mirrored program q(y) = p(-y) at -x, the
-    # rest (touching / straddling zero, invalid) the fixup replay. Results
-    # must equal the unpartitioned kernel and the oracle bit for bit, for
-    # every list length (empty lists, partial CTAs, ragged tails).
+@pytest.mark.parametrize("mode", ["split", "classify"])
+def test_interval_sign_partition_bit_exact(n, scheme, mode, cuda_device):
+    # Sign-partitioned fast path: x > 0 intervals run the program, x < 0
+    # intervals the mirrored program q(y) = p(-y) at -x, the rest (touching /
+    # straddling zero, invalid) the fixup replay — either in one kernel that
+    # packs each CTA's intervals by sign in shared memory ("split", the
+    # default) or through the classifier kernel and two gathered entries.
+    # Results must equal the unpartitioned kernel and the oracle bit for
+    # bit, for every list length (empty lists, partial CTAs, ragged tails).
     rng = np.random.default_rng(1000 + n)
     deg = {"estrin": 200, "horner": 37, "balanced": 64}[scheme]
     p = pe.Polynomial(np.arange(deg, -1, -1).reshape(-1, 1), rng.uniform(-1, 1, deg + 1))
@@ -530,13 +533,15 @@ def test_interval_sign_partition_bit_exact(n, scheme, cuda_device):
         lo[70:80], hi[70:80] = 1e150, 2e150    # overflow
         lo[80:90], hi[80:90] = -2e150, -1e150
     part = pe.compile(p, pe.builtin_scheme(scheme))
-    part.set_tuning(iv_partition_min=1)
+    part.set_tuning(iv_partition_min=1, iv_partition=2 if mode == "classify" else 0)
     f = pe.Evaluator(pe.IntervalDomain(), part).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
-    assert "pe_walk_interval_pos" in part.ptx(pe.DOMAIN_INTERVAL)
+    entry = "pe_walk_interval_pos" if mode == "classify" else "pe_walk_interval_split"
+    assert entry in part.ptx(pe.DOMAIN_INTERVAL)
     plain = pe.compile(p, pe.builtin_scheme(scheme))
     plain.set_tuning(iv_partition=-1)
     g = pe.Evaluator(pe.IntervalDomain(), plain).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
     assert "pe_walk_interval_pos" not in plain.ptx(pe.DOMAIN_INTERVAL)
+    assert "pe_walk_interval_split" not in plain.ptx(pe.DOMAIN_INTERVAL)
     o = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
     for a, b, c in zip(f, g, o):
         a, b = a.cpu().numpy(), b.cpu().numpy()
