@@ -42,10 +42,12 @@ for bits, degree, n in grid:
         got = pe.evaluate_wide(prog, cols, as_words=True)  # warm-up + checked result
         ref = pyoracle.ReferenceWide(exps, cw, [sch])
         bad = ref.mismatches(cols, got, threads=threads)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        pe.evaluate_wide(prog, cols, as_words=True)
-        gpu_s = time.perf_counter() - t
+        gpu_s = 1e30
+        for _ in range(3):  # best of 3 (host staging + one launch + D2H per call)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            pe.evaluate_wide(prog, cols, as_words=True)
+            gpu_s = min(gpu_s, time.perf_counter() - t)
         m = min(n, 64 if bits == 64 else 8)
         sub = [c[:m] for c in cols]
         ref1 = m / ref.seconds(sub, threads=1)

@@ -142,6 +142,7 @@ def main():
     t0 = time.time()
     cases, checks, failures = 0, {}, []
     while time.time() - t0 < budget:
+        print(f"seed {seed} t={time.time() - t0:.1f}", file=sys.stderr, flush=True)
         try:
             for d in check(seed):
                 checks[d.rstrip("0123456789") if d.startswith("limbs") else d] = \
