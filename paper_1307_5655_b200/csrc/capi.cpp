@@ -523,6 +523,7 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
       const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
           {n, static_cast<std::uint64_t>(sms) * (1024 / threads), by_mem}));
       void* scratch = nullptr;
+      keep_pool_memory(dev);
       check_cuda(cudaMallocAsync(&scratch, grid * per_cta * 8, s), "cudaMallocAsync(wide arena)");
       owned.push_back(scratch);
       check_cuda(pe_launch_wide(static_cast<const std::uint32_t*>(dv.code), plan->nops,

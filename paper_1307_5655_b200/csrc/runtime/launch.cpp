@@ -104,6 +104,22 @@ int sm_count(int device) {
   return n;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; with its default release threshold (0) every synchronisation hands
+// the memory back to the driver and the next call maps it again (C5: 400 MB
+// per 1e8-interval call, ~4 ms). Keep it pooled instead.
+void keep_pool_memory(int device) {
+  static std::mutex m;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lock(m);
+  if (!done.insert(device).second) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    std::uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+
 extern "C" cudaError_t pe_launch_vm(int domain, const std::uint32_t* code, std::uint32_t nops,
                                     std::uint32_t nslots, std::uint32_t result,
                                     const std::uint64_t* lo, const std::uint64_t* hi,
@@ -157,22 +173,6 @@ std::vector<void*> arg_ptrs(const Artifact& a, std::vector<std::uint64_t>& vals)
     args.push_back(const_cast<std::uint64_t*>(a.image.param_words.data()));
   }
   return args;
-}
-
-// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
-// pool; with its default release threshold (0) every synchronisation hands
-// the memory back to the driver and the next call maps it again (C5: 400 MB
-// per 1e8-interval call, ~4 ms). Keep it pooled instead.
-void keep_pool_memory(int device) {
-  static std::mutex m;
-  static std::set<int> done;
-  std::lock_guard<std::mutex> lock(m);
-  if (!done.insert(device).second) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    std::uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
 }
 
 }  // namespace

@@ -37,6 +37,10 @@ struct Staging {
 
 int sm_count(int device);
 
+/// Raises the release threshold of the device's default memory pool once, so
+/// stream-ordered scratch stays mapped between calls.
+void keep_pool_memory(int device);
+
 /// Launches one artifact (and its interval fixup entry) on `stream`.
 void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t stream);
 

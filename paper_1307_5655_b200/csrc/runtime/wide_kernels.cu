@@ -191,6 +191,16 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
     t.tb[k] = k >= 2 ? t.c2[k - 2] : 0;
   }
   __syncthreads();
+  if (wa <= 1 || wb <= 1) {
+    // one partial product per column: c2 is zero, product = c0 + (c1 << 64)
+    if (nx == ny) {
+      big_add(r, w, Num{t.c0, w}, Num{t.ta, w}, false, s_pair);
+    } else {
+      big_add(t.c1, w, Num{t.c0, w}, Num{t.ta, w}, false, s_pair);
+      big_neg(r, w, Num{t.c1, w}, s_pair, t.tb);
+    }
+    return;
+  }
   big_add(t.c1, w, Num{t.c0, w}, Num{t.ta, w}, false, s_pair);
   if (nx == ny) {
     big_add(r, w, Num{t.c1, w}, Num{t.tb, w}, false, s_pair);
