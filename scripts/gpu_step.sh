@@ -1,6 +1,7 @@
 # Scratch: the command of the most recent gpurun call (see gpu_full_round.sh for a full round).
-O=gpurun_out/g18; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q -k "interval or c5 or vm or smoke or partition" > $O/pytest_iv.log 2>&1; echo "pytest exit $?" >> $O/pytest_iv.log
+O=gpurun_out/s1; mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 timeout 900 python bench.py --config c5 --no-cpu > $O/bench_c5.json 2> $O/bench_c5.err
+timeout 900 python bench.py --config c4 --no-cpu > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 1200 bash scripts/ncu_captures.sh c5
-timeout 600 python scripts/fuzz_gpu.py 480 160000 > $O/fuzz.json 2>&1

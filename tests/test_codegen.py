@@ -260,3 +260,25 @@ def test_sectioned_kernel_with_all_coefficient_tiers_compiles():
     ptx = prog.ptx(pe.DOMAIN_F64)
     assert "ld.shared" in ptx and "ld.global.nc.f64 %c" in ptx
     assert prog.compile_only(pe.DOMAIN_F64) > 0
+
+
+def test_interval_injection_of_int64_coefficients_above_2_53():
+    # reference from_integer (numeric.cpp:17-26): an int64 coefficient that is
+    # not a double becomes [next_down(RN(c)), next_up(RN(c))]; exact ones a
+    # point interval. The words are baked into the constant bank.
+    import struct
+
+    def word(d):
+        return "0x%016X" % struct.unpack("<Q", struct.pack("<d", d))[0]
+
+    c = 2**53 + 1
+    p = pe.Polynomial(np.array([[1], [0]]), np.array([c, 5], dtype=np.int64))
+    ptx = pe.compile(p, pe.builtin_scheme("horner")).ptx(pe.DOMAIN_INTERVAL)
+    near = float(c)  # RN-even: 2^53
+    assert near == 2.0**53
+    assert f"{word(np.nextafter(near, -np.inf))}, {word(np.nextafter(near, np.inf))}" in ptx
+    assert word(5.0) in ptx
+    # exactly representable large coefficient: no widening
+    q = pe.Polynomial(np.array([[1], [0]]), np.array([2**60, 5], dtype=np.int64))
+    ptx = pe.compile(q, pe.builtin_scheme("horner")).ptx(pe.DOMAIN_INTERVAL)
+    assert word(2.0**60) in ptx and word(np.nextafter(2.0**60, np.inf)) not in ptx

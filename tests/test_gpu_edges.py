@@ -565,3 +565,29 @@ def test_interval_sign_partition_host_buffers_and_errors(cuda_device):
     bad_lo[12345] = hi[0][12345] + 1.0
     with pytest.raises(ValueError):
         ev.evaluate(([bad_lo], hi))
+
+
+@pytest.mark.parametrize("scheme", ["direct", "horner", "estrin", "balanced"])
+@pytest.mark.parametrize("mode", ["kernel", "vm", "strict_replay"])
+def test_interval_int64_coefficients_above_2_53_bit_exact(scheme, mode, cuda_device):
+    # int64 coefficients that are not doubles are injected as the one-ulp-
+    # widened interval around the nearest double (reference from_integer,
+    # numeric.cpp:17-26; stream.cpp inject / interval_coefficient). Checked
+    # against the golden vectors generated by the unmodified reference and
+    # the oracle, through the specialised kernel (fast path + sign split),
+    # the walk VM and the bit-level strict replay.
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "wide_int64_interval.npz"))
+    p = pe.Polynomial(z["exponents"], z["coefficients"])
+    assert p.coefficients.dtype == np.int64 and np.any(np.abs(p.coefficients.astype(object)) > 2**53)
+    lo, hi = z["lo0"], z["hi0"]
+    prog = pe.compile(p, pe.builtin_scheme(scheme))
+    prog.set_tuning(**{"kernel": dict(jit_mode=1, iv_partition_min=1), "vm": dict(jit_mode=2),
+                       "strict_replay": dict(jit_mode=1, iv_fast=-1)}[mode])
+    glo, ghi = pe.Evaluator(pe.IntervalDomain(), prog).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
+    glo, ghi = glo.cpu().numpy(), ghi.cpu().numpy()
+    assert np.array_equal(glo.view(np.int64), z[f"out_lo_{scheme}"].view(np.int64))
+    assert np.array_equal(ghi.view(np.int64), z[f"out_hi_{scheme}"].view(np.int64))
+    olo, ohi = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
+    assert np.array_equal(glo.view(np.int64), olo.view(np.int64))
+    assert np.array_equal(ghi.view(np.int64), ohi.view(np.int64))
