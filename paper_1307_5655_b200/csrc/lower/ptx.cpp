@@ -1927,8 +1927,11 @@ class Emitter {
   // program q(y) = p(-y) at [-hi, -lo] (hi < 0). Statically positive
   // coordinate, no straddle checks (the split kernel classified it).
   std::string point_function(const std::string& name, std::uint32_t role) {
-    const std::uint32_t lanes = P_;
+    const std::uint32_t lanes = P_, sync = sync_every_;
     P_ = 1;
+    // no CTA barriers inside: only the threads holding a packed slot of this
+    // sign call the function (a bar.sync here deadlocks the CTA)
+    sync_every_ = 0;
     reset_entry();
     decls_ << "  .reg .f64 " << xr(0, 0, false) << ", " << xr(0, 0, true) << ";\n"
            << "  .reg .b64 %facc;\n  .reg .pred %pslow;\n  .reg .pred %pb<4>;\n";
@@ -1973,6 +1976,7 @@ class Emitter {
       << "  .reg .pred %p<8>;\n  .reg .b32 %r<8>;\n  .reg .b64 %rd<24>;\n" << decls_.str()
       << body_.str() << "}\n\n";
     P_ = lanes;
+    sync_every_ = sync;
     return f.str();
   }
 
@@ -2059,11 +2063,16 @@ class Emitter {
           << "  add.u64 %sa, %sa, %sb;\n  ld.shared.u32 %r4, [%sa];\n"
           << "  cvt.u64.u32 %rd18, %r4;\n  add.u64 %rd18, %rd1, %rd18;\n"
           << "  setp.lt.u32 %p6, %r3, %r6;\n"
+          // each call binds its own .param arguments (a st.param belongs to
+          // the one call that follows it in its scope)
+          << "  @!%p6 bra $Lsplit_neg;\n"
           << "  {\n  .param .f64 a0;\n  .param .f64 a1;\n"
           << "  st.param.f64 [a0], %sxl;\n  st.param.f64 [a1], %sxh;\n"
-          << "  @!%p6 bra $Lsplit_neg;\n  call (%srl, %srh, %sfl), pe_iv_pos, (a0, a1);\n"
-          << "  bra $Lsplit_called;\n"
-          << "$Lsplit_neg:\n  call (%srl, %srh, %sfl), pe_iv_neg, (a0, a1);\n$Lsplit_called:\n  }\n"
+          << "  call (%srl, %srh, %sfl), pe_iv_pos, (a0, a1);\n  }\n"
+          << "  bra $Lsplit_called;\n$Lsplit_neg:\n"
+          << "  {\n  .param .f64 a0;\n  .param .f64 a1;\n"
+          << "  st.param.f64 [a0], %sxl;\n  st.param.f64 [a1], %sxh;\n"
+          << "  call (%srl, %srh, %sfl), pe_iv_neg, (a0, a1);\n  }\n$Lsplit_called:\n"
           << "  setp.ne.u32 %p7, %sfl, 0;\n";
     append("%p7", "%rd18");
     body_ << "  @%p7 bra $Ldone;\n  shl.b64 %rd18, %rd18, 3;\n"

@@ -282,3 +282,30 @@ def test_interval_injection_of_int64_coefficients_above_2_53():
     q = pe.Polynomial(np.array([[1], [0]]), np.array([2**60, 5], dtype=np.int64))
     ptx = pe.compile(q, pe.builtin_scheme("horner")).ptx(pe.DOMAIN_INTERVAL)
     assert word(2.0**60) in ptx and word(np.nextafter(2.0**60, np.inf)) not in ptx
+
+
+def test_split_kernel_point_functions_are_divergence_safe():
+    # The one-pass sign split calls the program's and the mirrored program's
+    # point functions from threads of one CTA (and, in the boundary warp, of
+    # one warp). Two hazards found on the GPU: a CTA barrier inside a point
+    # function deadlocks the CTA, and .param arguments shared by two calls
+    # bind only to the first call (the second reads stale registers).
+    import re
+    wl = W.c5()
+    ptx = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
+    assert "pe_walk_interval_split" in ptx
+    for name in ("pe_iv_pos", "pe_iv_neg", "pe_fix_point"):
+        start = ptx.index(".func")
+        m = re.search(r"\.func[^\n]*\b%s\(" % name, ptx)
+        assert m, name
+        body = ptx[m.start():ptx.index("\n}\n", m.start())]
+        assert "bar.sync" not in body, name
+    # every call to a point function sits in its own scope with its own
+    # st.param stores
+    entry = ptx[ptx.index(".entry pe_walk_interval_split"):]
+    entry = entry[:entry.index("\n}\n")]
+    scopes = re.findall(r"\{\n(.*?)\n  \}", entry, flags=re.S)
+    calls = [sc for sc in scopes if "call " in sc]
+    assert len(calls) == 2
+    for sc in calls:
+        assert sc.count("call ") == 1 and sc.count("st.param.f64") == 2
