@@ -194,9 +194,10 @@ typedef struct pe_tuning {
                               UINT32_MAX = never) */
   int32_t iv_fast;         /* interval: -1 = bit-level replay only (no fast path) */
   int32_t iv_mid;          /* interval fixup: -1 = skip the finite-case replay */
-  int32_t iv_partition;    /* univariate interval sign partition: -1 = off; 2 = the
-                              classifier + gathered-entries path even where the one-pass
-                              split kernel applies */
+  int32_t iv_partition;    /* univariate interval sign partition: -1 = off; 3 = the
+                              one-pass split kernel (each interval read and written
+                              once) where both coefficient sets fit the constant bank,
+                              instead of the classifier + gathered entries */
   uint32_t group_tiles;    /* sectioned kernels: tiles of points a CTA runs through one
                               section before the next (default 4) */
   int32_t word_layout;     /* sections: -1 = one coefficient block for the whole walk

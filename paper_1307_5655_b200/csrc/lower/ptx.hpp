@@ -92,7 +92,7 @@ struct Tuning {
   std::uint32_t chain_min = 0;    // shortest Hörner run emitted as a loop; UINT32_MAX = never
   std::int32_t iv_fast = 0;       // interval fast path + fixup list (-1 = bit-level replay only)
   std::int32_t iv_mid = 0;        // fixup: finite-case replay first (-1 = bit-level only)
-  std::int32_t iv_partition = 0;  // univariate sign partition (-1 off, 2 = classifier path only)
+  std::int32_t iv_partition = 0;  // univariate sign partition (-1 off, 3 = one-pass split kernel)
   std::uint32_t group_tiles = 0;  // sections: tiles a CTA runs per section pass (default 4)
   std::int32_t word_layout = 0;   // sections: -1 = all uniform-bound words first (no per-section blocks)
   std::int32_t jit_mode = 0;      // 0 walk VM until the kernel is compiled, 1 always wait, 2 VM only

@@ -116,9 +116,11 @@ void emit_interval(const front::FlatProgram<C>& prog, std::uint32_t nvars, const
   const auto s = lower::lower_strict(prog);
   lower::Stream<C> q;
   const bool mirrored = shape.iv_partition == 1 && lower::mirror_stream(s, &q);
-  // tuning iv_partition 2: the classifier path even where the split fits
+  // tuning iv_partition 3: the one-pass split kernel where it fits (reads and
+  // writes each interval once; measured slower than the classifier path on
+  // C5, 12.6 vs 10.5 ms per 1e8: profiles/r2_c5_split_vs_classify.jsonl)
   a.image = lower::emit_ptx(s, lower::Domain::Interval, shape, t,
-                            mirrored && t.iv_partition != 2 ? &q : nullptr);
+                            mirrored && t.iv_partition == 3 ? &q : nullptr);
   // iv_partition 3: the split kernel carries both programs; 1: the
   // classifier path needs the mirrored program's module
   if (a.image.iv_partition != 1 || !mirrored) return;

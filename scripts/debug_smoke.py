@@ -39,8 +39,8 @@ elif piece.startswith("iv"):
     lo, hi = [pts[0]], [pts[0] + 1e-6]
     olo, ohi = pyoracle.Oracle(wl.poly, wl.schemes).eval_interval(lo, hi)
     prog = pe.compile(wl.poly, wl.schemes)
-    tune = {"iv": dict(jit_mode=1), "ivsplit": dict(jit_mode=1, iv_partition_min=1),
-            "ivclassify": dict(jit_mode=1, iv_partition_min=1, iv_partition=2),
+    tune = {"iv": dict(jit_mode=1), "ivsplit": dict(jit_mode=1, iv_partition_min=1, iv_partition=3),
+            "ivclassify": dict(jit_mode=1, iv_partition_min=1),
             "ivnopart": dict(jit_mode=1, iv_partition=-1), "ivvm": dict(jit_mode=2)}[piece]
     prog.set_tuning(**tune)
     prog.compile_only(pe.DOMAIN_INTERVAL)

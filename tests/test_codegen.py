@@ -292,7 +292,9 @@ def test_split_kernel_point_functions_are_divergence_safe():
     # bind only to the first call (the second reads stale registers).
     import re
     wl = W.c5()
-    ptx = pe.compile(wl.poly, wl.schemes).ptx(pe.DOMAIN_INTERVAL)
+    prog = pe.compile(wl.poly, wl.schemes)
+    prog.set_tuning(iv_partition=3)
+    ptx = prog.ptx(pe.DOMAIN_INTERVAL)
     assert "pe_walk_interval_split" in ptx
     for name in ("pe_iv_pos", "pe_iv_neg", "pe_fix_point"):
         start = ptx.index(".func")

@@ -512,8 +512,9 @@ def test_interval_sign_partition_bit_exact(n, scheme, mode, cuda_device):
     # Sign-partitioned fast path: x > 0 intervals run the program, x < 0
     # intervals the mirrored program q(y) = p(-y) at -x, the rest (touching /
     # straddling zero, invalid) the fixup replay — either in one kernel that
-    # packs each CTA's intervals by sign in shared memory ("split", the
-    # default) or through the classifier kernel and two gathered entries.
+    # packs each CTA's intervals by sign in shared memory ("split",
+    # iv_partition=3) or through the classifier kernel and two gathered
+    # entries (the default).
     # Results must equal the unpartitioned kernel and the oracle bit for
     # bit, for every list length (empty lists, partial CTAs, ragged tails).
     rng = np.random.default_rng(1000 + n)
@@ -533,7 +534,7 @@ def test_interval_sign_partition_bit_exact(n, scheme, mode, cuda_device):
         lo[70:80], hi[70:80] = 1e150, 2e150    # overflow
         lo[80:90], hi[80:90] = -2e150, -1e150
     part = pe.compile(p, pe.builtin_scheme(scheme))
-    part.set_tuning(iv_partition_min=1, iv_partition=2 if mode == "classify" else 0)
+    part.set_tuning(iv_partition_min=1, iv_partition=3 if mode == "split" else 0)
     f = pe.Evaluator(pe.IntervalDomain(), part).evaluate(([_t(lo, cuda_device)], [_t(hi, cuda_device)]))
     entry = "pe_walk_interval_pos" if mode == "classify" else "pe_walk_interval_split"
     assert entry in part.ptx(pe.DOMAIN_INTERVAL)
