@@ -295,8 +295,13 @@ void launch(const Artifact& a, int device, const LaunchArgs& la, cudaStream_t st
   const std::uint64_t grid = (la.n + tile - 1) / tile;
   if (grid > 0x7fffffffull) throw std::invalid_argument("batch too large for one launch");
   if (split) {
-    launch_one(a.part_kernel, dev_ok ? a.part_fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
-               dim3(static_cast<unsigned>(block)), args.data(), stream, "launch(walk split)");
+    // persistent: 1024 threads per SM stride over the tiles
+    const std::uint64_t stiles = (la.n + img.block - 1) / img.block;
+    const std::uint64_t sgrid =
+        std::min<std::uint64_t>(stiles, static_cast<std::uint64_t>(1024 / img.block) * sm_count(device));
+    launch_one(a.part_kernel, dev_ok ? a.part_fn[device] : nullptr,
+               dim3(static_cast<unsigned>(sgrid ? sgrid : 1)), dim3(img.block), args.data(), stream,
+               "launch(walk split)");
     launch_counter().fetch_add(1, std::memory_order_relaxed);
   } else if (!part) {
     launch_one(a.kernel, dev_ok ? a.fn[device] : nullptr, dim3(static_cast<unsigned>(grid)),
