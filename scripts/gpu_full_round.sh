@@ -7,15 +7,15 @@
 # to keep into profiles/).
 O=gpurun_out/round
 mkdir -p $O
-python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 600 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 for c in c4 c2 c3 c5 c1; do
   timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 900 python bench.py --impl reference > $O/bench_reference_c4.json 2> $O/bench_reference_c4.err
+timeout 3000 bash scripts/ncu_captures.sh c4 c5 c5split c2e1000 c3
 python scripts/fp64_peaks.py > $O/fp64_peaks.json 2>&1
 PE_CACHE_DIR=off timeout 900 python scripts/first_call.py > $O/first_call.jsonl 2>&1
-timeout 2400 python scripts/fig1_grid.py > $O/fig1_grid.jsonl 2>&1
 timeout 700 python scripts/fuzz_gpu.py 600 200000 > $O/fuzz.json 2>&1
-timeout 3000 bash scripts/ncu_captures.sh c4 c5 c2e1000 c3
+timeout 2400 python scripts/fig1_grid.py > $O/fig1_grid.jsonl 2>&1
 echo done > $O/DONE

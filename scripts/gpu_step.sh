@@ -1,8 +1,9 @@
 # Scratch: the command of the most recent gpurun call (see gpu_full_round.sh for a full round).
-O=gpurun_out/s11; mkdir -p $O
-timeout 150 python scripts/debug_smoke.py ivsplit 1000003 > $O/dbg_ivsplit_1m.log 2>&1; echo "exit $?" >> $O/dbg_ivsplit_1m.log
-grep -q "exact True True" $O/dbg_ivsplit_1m.log || exit 1
-timeout 600 python scripts/profile_one.py --config c5 --points 100000000 --reps 3 \
-  --tune jit_mode=1 --tune jit_mode=1,iv_partition=3 --tune jit_mode=1,iv_partition=3,block=256 \
-  --tune jit_mode=1,iv_partition=3,block=128 --tune jit_mode=1,iv_partition=3,block=64 > $O/c5_modes.jsonl 2> $O/c5_modes.err
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -k "partition" > $O/pytest_part.log 2>&1; echo "pytest exit $?" >> $O/pytest_part.log
+O=gpurun_out/s12; mkdir -p $O
+timeout 1200 python scripts/profile_one.py --config c4 --points 20000000 --reps 3 \
+  --tune jit_mode=1 \
+  --tune jit_mode=1,lanes=2,block=384,section_ops=1500 \
+  --tune jit_mode=1,lanes=2,block=384,section_ops=2500 \
+  --tune jit_mode=1,lanes=2,block=512,section_ops=1600 \
+  --tune jit_mode=1,lanes=2,block=320,section_ops=2000 \
+  > $O/c4_shapes2.jsonl 2> $O/c4_shapes2.err
