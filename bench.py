@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    # plumbing check of the multi-rank path on a box with fewer GPUs than
+    # ranks (tests/test_bench_ranks.py): every rank on cuda:0, gloo for the
+    # barrier / max-reduction. Its numbers are not measurements.
+    ap.add_argument("--ranks-share-gpu0", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -175,15 +179,20 @@ def ncu_traffic(cfg, program, points):
 
 # ----------------------------------------------------------------- dist
 
-def dist_setup():
+def dist_setup(share_gpu0: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share_gpu0:
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu0:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -198,7 +207,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -628,7 +638,7 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         run_reference_arm(args, world, rank)
         return
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.ranks_share_gpu0)
     try:
         run_native(args, world, rank, local)
     finally:
