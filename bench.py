@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--tune", default="", help="pe_tuning fields for every program, e.g. "
+                    "iv_partition=3 (C5 through the one-pass split kernel); recorded in config")
     # plumbing check of the multi-rank path on a box with fewer GPUs than
     # ranks (tests/test_bench_ranks.py): every rank on cuda:0, gloo for the
     # barrier / max-reduction. Its numbers are not measurements.
@@ -145,22 +147,24 @@ class ClockSampler:
 # several rows (the launches of one evaluate call) is summed
 NCU_CAPTURES = {
     ("c4", "C4_trivariate_sparse10k"): "profiles/r2_ncu_c4_raw.csv",
-    ("c5", "C5_interval_estrin_d200"): "profiles/r2_ncu_c5_split_raw.csv",
-    ("c2", "C2_estrin_d1000"): "profiles/r1_ncu_c2_estrin_d1000_raw.csv",
+    ("c5", "C5_interval_estrin_d200"): "profiles/r2_ncu_c5_raw.csv",
+    # the one-pass split kernel (pe_tuning.iv_partition = 3)
+    ("c5", "C5_interval_estrin_d200", "split"): "profiles/r2_ncu_c5_split_raw.csv",
+    ("c2", "C2_estrin_d1000"): "profiles/r2_ncu_c2e1000_raw.csv",
     ("c2", "C2_balanced_d1000"): "profiles/r1_ncu_c2_balanced_d1000_raw.csv",
     ("c2", "C2_estrin_d1023"): "profiles/r1_ncu_c2_estrin_d1023_raw.csv",
     ("c2", "C2_balanced_d1023"): "profiles/r1_ncu_c2_balanced_d1023_raw.csv",
     ("c1", "C1_horner_d1000"): "profiles/r1_ncu_c1_raw.csv",
-    ("c3", "C3_bivariate_td40_i64"): "profiles/r1_ncu_c3_raw.csv",
+    ("c3", "C3_bivariate_td40_i64"): "profiles/r2_ncu_c3_raw.csv",
 }
 
 
-def ncu_traffic(cfg, program, points):
+def ncu_traffic(cfg, program, points, variant=None):
     """(dram__bytes_read.sum + dram__bytes_write.sum per launch, source) from
     the committed ncu capture of this kernel; None when there is no capture
     at this launch size."""
     import csv
-    path = NCU_CAPTURES.get((cfg, program))
+    path = NCU_CAPTURES.get((cfg, program, variant) if variant else (cfg, program))
     if not path or not os.path.exists(os.path.join(ROOT, path)):
         return None, None
     rows = list(csv.reader(open(os.path.join(ROOT, path))))
@@ -380,6 +384,10 @@ def run_native(args, world, rank, local):
     # programs + kernels (compile is setup, outside the timed region)
     t_setup = time.perf_counter()
     progs = [pe.compile(w.poly, w.schemes) for w in wls]
+    tune = {k.strip(): int(v) for k, v in (kv.split("=") for kv in args.tune.split(",") if kv)}
+    for p in progs:
+        if tune:
+            p.set_tuning(**tune)
     if domain == "interval":
         evs = [pe.Evaluator(pe.IntervalDomain(), p, device=local, deferred_checks=True)
                for p in progs]
@@ -510,7 +518,6 @@ def run_native(args, world, rank, local):
     # FLOP accounting: a DFMA is 2 FLOP, an interval endpoint add/mul 1; the
     # FP64 pipe issues one of either per lane per clock
     flop_per_op = 1.0 if domain == "interval" else 2.0
-    traffic, traffic_src = ncu_traffic(args.config, wls[top].name, n)
     sections = progs[top].f64_slices() if domain == "f64" else 1
     kernel_name = f"pe_walk_{domain} [{wls[top].name}]"
     if domain == "f64" and sections > 1:
@@ -523,6 +530,8 @@ def run_native(args, world, rank, local):
     elif "pe_walk_interval_pos" in iv_ptx:
         kernel_name = (f"classify_intervals + pe_walk_interval_pos + pe_walk_interval_neg + "
                        f"pe_walk_interval_fix [{wls[top].name}] (one evaluate call, sign-partitioned)")
+    traffic, traffic_src = ncu_traffic(args.config, wls[top].name, n,
+                                       "split" if "pe_walk_interval_split" in iv_ptx else None)
     roofline = {
         "bound": "fp64" if fp_pipe else "int64_mad",
         "int64_tier": int_tier if domain == "i64" else None,
@@ -616,7 +625,8 @@ def run_native(args, world, rank, local):
                    "global_batch": n_total, "points_per_rank": n, "point_evals_per_step": pts_step,
                    "parallelism": f"global batch in {world} contiguous shard(s), one per rank, "
                                   "no data-path collective",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   **({"tuning": tune} if tune else {})},
         "term_evals_per_s": value * terms,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
