@@ -1,9 +1,10 @@
 # Scratch: the command of the most recent gpurun call (see gpu_full_round.sh for a full round).
-O=gpurun_out/s13; mkdir -p $O
-timeout 900 python -m pytest tests/test_bench_ranks.py -m gpu -q --timeout 600 > $O/pytest_ranks.log 2>&1; echo "pytest exit $?" >> $O/pytest_ranks.log
-for c in c4 c2 c3 c5 c1; do
-  timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err
-done
-timeout 900 python bench.py --config c5 --tune iv_partition=3 > $O/bench_c5_split.json 2> $O/bench_c5_split.err
-timeout 500 python scripts/fuzz_gpu.py 420 300000 jit_mode=1,iv_partition=3,iv_partition_min=1 > $O/fuzz_split.json 2>&1
-timeout 500 python scripts/fuzz_gpu.py 420 310000 jit_mode=1,iv_partition_min=1 > $O/fuzz_partmin1.json 2>&1
+O=gpurun_out/s14; mkdir -p $O
+timeout 150 python scripts/debug_smoke.py ivsplit 4099 > $O/dbg_ivsplit_4k.log 2>&1; echo "exit $?" >> $O/dbg_ivsplit_4k.log
+timeout 150 python scripts/debug_smoke.py ivsplit 1000003 > $O/dbg_ivsplit_1m.log 2>&1; echo "exit $?" >> $O/dbg_ivsplit_1m.log
+grep -q "exact True True" $O/dbg_ivsplit_1m.log || exit 1
+timeout 600 python scripts/profile_one.py --config c5 --points 100000000 --reps 3 \
+  --tune jit_mode=1 --tune jit_mode=1,iv_partition=3 --tune jit_mode=1,iv_partition=3,block=256 \
+  --tune jit_mode=1,iv_partition=3,sync_every=64 --tune jit_mode=1,iv_partition=3,sync_every=16 \
+  --tune jit_mode=1,iv_partition=3,sync_every=128 > $O/c5_modes.jsonl 2> $O/c5_modes.err
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -k "partition" > $O/pytest_part.log 2>&1; echo "pytest exit $?" >> $O/pytest_part.log
