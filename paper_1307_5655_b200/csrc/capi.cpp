@@ -516,8 +516,22 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
       // CTA idle at every barrier); as many CTAs as fit 1024 threads per SM,
       // at most 4 GB of arenas
       const int sms = device_ctx(dev).sms;
-      const unsigned threads = plan->tmp_w <= 64 ? 32 : plan->tmp_w <= 256 ? 64
-                               : plan->tmp_w <= 1024 ? 128 : 256;
+      unsigned threads = plan->tmp_w <= 64 ? 32 : plan->tmp_w <= 256 ? 64
+                         : plan->tmp_w <= 1024 ? 128 : 256;
+      // ... and by batch size: the walk is latency-bound per op (barriers,
+      // dependent loads), so points in flight matter more than threads per
+      // point. A CTA gets more than one warp only when the batch is too
+      // small to fill 1024 threads per SM with one-warp CTAs
+      // (profiles/r2_wide_cta_sweep.jsonl: 64-bit d1000 at 4096 points,
+      // 65.6k -> 135.6k points/s with one-warp CTAs).
+      unsigned by_batch = 32;
+      while (by_batch < 256 && static_cast<std::uint64_t>(n) * by_batch * 2 <= 1024ull * sms) {
+        by_batch *= 2;
+      }
+      threads = std::min(threads, by_batch);
+      if (p.tuning.block >= 32 && p.tuning.block <= 256 && p.tuning.block % 32 == 0) {
+        threads = p.tuning.block;  // pe_tuning.block: CTA size of the wide walk
+      }
       const size_t per_cta = static_cast<size_t>(plan->arena) + 5ull * plan->tmp_w;
       const std::uint64_t by_mem = std::max<std::uint64_t>(1, (std::uint64_t{4} << 30) / (per_cta * 8));
       const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
