@@ -182,8 +182,10 @@ void pe_program_destroy(pe_program* program);
  * measured defaults; every field's 0 means "default". */
 typedef struct pe_tuning {
   uint32_t lanes;          /* points per thread, 1..8 */
-  uint32_t block;          /* threads per CTA, 32..1024 */
-  uint32_t min_ctas;       /* .minnctapersm of the walk kernel */
+  uint32_t block;          /* threads per CTA, 32..1024 (wide programs: threads per
+                              point, 32..256; default by value width and batch size) */
+  uint32_t min_ctas;       /* .minnctapersm of the walk kernel (wide programs: CTAs,
+                              i.e. points in flight, per SM) */
   uint32_t sync_every;     /* walk ops between CTA barriers */
   uint32_t section_ops;    /* long int/fp64 walks: ops per section of the persistent
                               sectioned kernel (default 3000; UINT32_MAX = one plain

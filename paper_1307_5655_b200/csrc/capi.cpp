@@ -534,8 +534,10 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
       }
       const size_t per_cta = static_cast<size_t>(plan->arena) + 5ull * plan->tmp_w;
       const std::uint64_t by_mem = std::max<std::uint64_t>(1, (std::uint64_t{4} << 30) / (per_cta * 8));
+      // pe_tuning.min_ctas: CTAs per SM of the wide walk (default: 1024 threads per SM)
+      const std::uint64_t per_sm = p.tuning.min_ctas ? p.tuning.min_ctas : 1024 / threads;
       const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(
-          {n, static_cast<std::uint64_t>(sms) * (1024 / threads), by_mem}));
+          {n, static_cast<std::uint64_t>(sms) * per_sm, by_mem}));
       void* scratch = nullptr;
       keep_pool_memory(dev);
       check_cuda(cudaMallocAsync(&scratch, grid * per_cta * 8, s), "cudaMallocAsync(wide arena)");

@@ -1,5 +1,5 @@
 """Target process for ncu captures of the wide-integer walk (pe_eval_wide):
-  python scripts/wide_profile.py <bits> <degree> <points> <scheme> [block]
+  python scripts/wide_profile.py <bits> <degree> <points> <scheme> [tuning]
 Device-resident inputs and outputs; prints points/s (CUDA events)."""
 import json
 import os
@@ -21,8 +21,8 @@ scheme = sys.argv[4] if len(sys.argv) > 4 else "balanced"
 exps, coefs, pts = W.fig1(degree, bits, bits, n)
 L = pe.limbs_for(pts)
 prog = pe.compile_wide(exps, coefs, pe.builtin_scheme(scheme))
-if len(sys.argv) > 5:
-    prog.set_tuning(block=int(sys.argv[5]))
+if len(sys.argv) > 5:  # pe_tuning fields, e.g. block=32,min_ctas=8
+    prog.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in sys.argv[5].split(","))})
 k = pe.wide_limbs(prog, L)
 dev = torch.device("cuda:0")
 words = torch.from_numpy(pe.ints_to_words(pts, L).view(np.int64)).to(dev)
@@ -48,4 +48,5 @@ for _ in range(3):
     torch.cuda.synchronize()
     best = min(best, s.elapsed_time(e))
 print(json.dumps({"bits": bits, "degree": degree, "points": n, "scheme": scheme, "result_limbs": k,
+                  "tuning": sys.argv[5] if len(sys.argv) > 5 else "",
                   "ms": best, "points_per_s": n / (best * 1e-3)}))
