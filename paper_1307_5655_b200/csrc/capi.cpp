@@ -554,10 +554,10 @@ pe_status pe_eval_wide(const pe_program* program, const uint64_t* const* coords,
                  "launch(wide walk)");
       launch_counter().fetch_add(1, std::memory_order_relaxed);
       if (kind != MemKind::Device) {
-        check_cuda(cudaMemcpyAsync(out, dout, n * out_limbs * 8, cudaMemcpyDeviceToHost, s), "wide D2H");
+        copy_to_host(out, dout, n * out_limbs * 8, dev, s);  // complete on return
       }
       cleanup();
-      if (kind != MemKind::Device || (exec && exec->synchronize)) {
+      if (kind == MemKind::Device && exec && exec->synchronize) {
         check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
       }
     } catch (...) {

@@ -470,6 +470,40 @@ class CopyPool {
 };
 }  // namespace
 
+void copy_to_host(void* dst, const void* dev_src, size_t bytes, int device, cudaStream_t stream) {
+  constexpr size_t kChunk = size_t{8} << 20;
+  bool pinned = false;
+  classify(dst, nullptr, &pinned);
+  if (pinned || bytes < 2 * kChunk) {
+    check_cuda(cudaMemcpyAsync(dst, dev_src, bytes, cudaMemcpyDeviceToHost, stream), "D2H");
+    check_cuda(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    return;
+  }
+  DeviceCtx& c = device_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  for (int k = 0; k < 2; ++k) {
+    if (!c.d2h_pinned[k]) {
+      check_cuda(cudaHostAlloc(&c.d2h_pinned[k], kChunk, cudaHostAllocDefault), "cudaHostAlloc(D2H chunk)");
+      check_cuda(cudaEventCreateWithFlags(&c.d2h_done[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  const size_t chunks = (bytes + kChunk - 1) / kChunk;
+  auto len = [&](size_t i) { return std::min(kChunk, bytes - i * kChunk); };
+  auto drain = [&](size_t i) {  // chunk i: wait for the copy engine, then the host copy
+    check_cuda(cudaEventSynchronize(c.d2h_done[i & 1]), "cudaEventSynchronize");
+    CopyPool::get().copy(static_cast<char*>(dst) + i * kChunk, c.d2h_pinned[i & 1], len(i));
+  };
+  for (size_t i = 0; i < chunks; ++i) {
+    // (chunk i - 2, the previous user of this page-locked chunk, was drained in the last round)
+    check_cuda(cudaMemcpyAsync(c.d2h_pinned[i & 1], static_cast<const char*>(dev_src) + i * kChunk, len(i),
+                               cudaMemcpyDeviceToHost, stream),
+               "D2H chunk");
+    check_cuda(cudaEventRecord(c.d2h_done[i & 1], stream), "cudaEventRecord");
+    if (i >= 1) drain(i - 1);
+  }
+  drain(chunks - 1);
+}
+
 int resolve_device(const pe_exec* ex, const void* probe, MemKind* kind) {
   int ptr_dev = -1;
   *kind = classify(probe, &ptr_dev);

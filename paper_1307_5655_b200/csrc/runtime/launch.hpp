@@ -66,6 +66,8 @@ struct DeviceCtx {
   std::vector<void*> buffers[kMaxSlots];  // per slot: device arrays of `cap` bytes
   std::vector<void*> pinned[kMaxSlots];   // per slot: page-locked host arrays (pageable callers)
   size_t cap = 0, pinned_cap = 0;
+  void* d2h_pinned[2] = {};  // copy_to_host: two page-locked chunks
+  cudaEvent_t d2h_done[2] = {};
   std::mutex mu;  // serialises host-staged calls on a device
   int sms = 0;
   std::mutex state_mu;
@@ -93,6 +95,13 @@ struct DeviceCtx {
 };
 
 DeviceCtx& device_ctx(int device);
+
+/// Device -> host copy of a large result, ordered after the work queued on
+/// `stream` and complete on return. A pageable destination is filled through
+/// two page-locked chunks: the copy engine writes one while the host copy
+/// pool moves the other into the caller's buffer (a plain cudaMemcpy to
+/// pageable memory runs at a fraction of PCIe speed).
+void copy_to_host(void* dst, const void* dev_src, size_t bytes, int device, cudaStream_t stream);
 
 int resolve_device(const pe_exec* ex, const void* probe, MemKind* kind);
 

@@ -107,6 +107,26 @@ WidePlan plan_wide(const front::FlatProgram<std::int64_t>& fp,
   }
   if (off > UINT32_MAX / 2) throw std::overflow_error("wide evaluation: arena too large");
   p.arena = static_cast<std::uint32_t>(off);
+  // resolve the operands of every op (slot -> arena offset, coefficient ->
+  // offset into coef_words)
+  for (std::uint32_t i = 0; i < p.nops; ++i) {
+    std::uint32_t* c = p.code.data() + 8 * i;
+    std::uint32_t flags = 0;
+    for (int k = 0; k < 2; ++k) {
+      std::uint32_t& o = c[2 + k];
+      if (o & lower::VmProgram::kZero) {
+        o = 0;
+        c[5 + k] = 0;  // width 0: zero operand
+      } else if (o & lower::VmProgram::kCoef) {
+        o = p.coef_off[o & ~lower::VmProgram::kCoef];
+        flags |= 1u << k;
+      } else {
+        o = p.slot_off[o];
+      }
+    }
+    c[1] = p.slot_off[c[1]];
+    c[7] = flags;
+  }
   return p;
 }
 

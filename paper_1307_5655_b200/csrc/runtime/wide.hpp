@@ -13,8 +13,11 @@
 namespace polyeval::rt {
 
 struct WidePlan {
-  // 8 words per op: kind (0 add, 1 mul), dst slot, a, b (VM operands),
-  // result width, width of a, width of b, 0
+  // 8 words per op, operands resolved so the kernel decodes an op from one
+  // 32-byte record: kind (0 add, 1 mul), arena offset of the destination,
+  // offset of a, offset of b (arena limbs, or coef_words limbs for a
+  // coefficient), result width, width of a, width of b (0: the operand is
+  // zero), flags (bit 0: a is a coefficient, bit 1: b is)
   std::vector<std::uint32_t> code;
   std::vector<std::uint32_t> slot_off, slot_w;
   std::vector<std::uint32_t> coef_off, coef_w;

@@ -36,7 +36,7 @@ constexpr std::uint32_t kCoef = 0x80000000u, kZero = 0x40000000u;
 constexpr int kMaxVars = 16;
 
 struct WideArgs {
-  const std::uint32_t* code;     // 8 words per op (kind, dst, a, b, w_r, w_a, w_b, 0)
+  const std::uint32_t* code;     // 8 words per op (runtime/wide.hpp: resolved offsets), 16-byte aligned
   const std::uint32_t* slot_off; // per slot: arena offset (limbs)
   const std::uint32_t* slot_w;   // per slot: width (limbs)
   const std::uint32_t* coef_off; // per coefficient: offset into coef_words
@@ -398,12 +398,18 @@ __global__ void __launch_bounds__(kMaxThreads) wide_walk_kernel(const WideArgs a
       for (std::uint32_t k = threadIdx.x; k < a.slot_w[v]; k += T) d[k] = limb(x, k);
     }
     __syncthreads();
+    const uint4* code = reinterpret_cast<const uint4*>(a.code);
+    uint4 c0 = __ldg(code), c1 = __ldg(code + 1);  // op 0 (one 32-byte record per op)
     for (std::uint32_t op = 0; op < a.nops; ++op) {
-      const std::uint32_t* c = a.code + 8 * op;
-      const std::uint32_t kind = c[0], dst = c[1];
-      std::uint64_t* r = arena + a.slot_off[dst];
-      const std::uint32_t w = c[4];
-      const Num x = operand(a, arena, c[2], c[5]), y = operand(a, arena, c[3], c[6]);
+      // kind, dst offset, a offset, b offset | width, width a, width b, flags
+      const std::uint32_t kind = c0.x, w = c1.x;
+      std::uint64_t* r = arena + c0.y;
+      const Num x{(c1.w & 1u ? a.coef_words : arena) + c0.z, c1.y};
+      const Num y{(c1.w & 2u ? a.coef_words : arena) + c0.w, c1.z};
+      if (op + 1 < a.nops) {  // the next record arrives while this op runs
+        c0 = __ldg(code + 2 * op + 2);
+        c1 = __ldg(code + 2 * op + 3);
+      }
       if (w <= 32 && x.w <= 32 && y.w <= 32) {
         if (threadIdx.x < 32) {
           if (kind == 0) {

@@ -2,8 +2,10 @@
 unmodified reference BigInt walk (oracle/_ref): dense degree-d polynomials
 with 64-bit (run_grid defaults, reference bench.hpp:22-23) or 2048-bit
 (acceptance_test.cpp C09 staircase) coefficients and points, schemes
-balanced / estrin / horner. Per case: GPU points/s over a batch (CUDA
-events, results checked word for word against the reference), reference
+balanced / estrin / horner. Per case: GPU points/s over a batch — the whole
+call with host words in and out (wall clock), and the walk alone with
+device-resident buffers (CUDA events) — results checked word for word
+against the reference, reference
 points/s on 1 thread and on all host threads, and the estrin / balanced
 time ratio — the paper's Figure-1 quantity — on both.
 
@@ -16,10 +18,13 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+import ctypes as C  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1307_5655_b200 as pe  # noqa: E402
+from paper_1307_5655_b200 import _lib as L_  # noqa: E402
 from paper_1307_5655_b200 import workloads as W  # noqa: E402
 import pyoracle  # noqa: E402
 
@@ -48,6 +53,21 @@ for bits, degree, n in grid:
             t = time.perf_counter()
             pe.evaluate_wide(prog, cols, as_words=True)
             gpu_s = min(gpu_s, time.perf_counter() - t)
+        # the walk alone: device-resident words in and out, CUDA events
+        dev_in = torch.from_numpy(cols[0].view(np.int64)).to("cuda:0")
+        dev_out = torch.empty((n, k), dtype=torch.int64, device="cuda:0")
+        ptrs = (C.c_void_p * 1)(dev_in.data_ptr())
+        ex = L_.pe_exec()
+        ex.device = -1
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kern_ms = 1e30
+        for _ in range(3):
+            e0.record()
+            L_.check(L_.lib().pe_eval_wide(prog.handle, ptrs, L, n, dev_out.data_ptr(), k, C.byref(ex)))
+            e1.record()
+            torch.cuda.synchronize()
+            kern_ms = min(kern_ms, e0.elapsed_time(e1))
+        assert np.array_equal(dev_out.cpu().numpy().view(np.uint64), got)
         m = min(n, 64 if bits == 64 else 8)
         sub = [c[:m] for c in cols]
         ref1 = m / ref.seconds(sub, threads=1)
@@ -56,6 +76,7 @@ for bits, degree, n in grid:
         row = {"coeff_bits": bits, "point_bits": bits, "degree": degree, "scheme": scheme,
                "points": n, "result_limbs": k, "mismatches": bad,
                "gpu_points_per_s": n / gpu_s, "gpu_call_s": gpu_s,
+               "gpu_kernel_points_per_s": n / (kern_ms * 1e-3), "gpu_kernel_ms": kern_ms,
                "ref_points_per_s_1thread": ref1, "ref_points_per_s_all": refT,
                "ref_threads": threads}
         rows[(bits, degree, scheme)] = row
