@@ -70,6 +70,7 @@ struct Lowerer {
   const front::FlatProgram<C>& fp;
 
   std::uint8_t cur_odd = 0;  // strict: parity of the record being lowered
+  bool fold_constants = true;
 
   Operand new_reg() { return Operand::reg(s.nregs++); }
   Operand coef(const C& c, std::uint32_t widen = 0) {
@@ -195,7 +196,7 @@ struct Lowerer {
           if (!folded[j]) {
             folded[j] = 1;
             const Operand addend = own(prog, j);
-            if (val.is(Operand::Coef) && addend.is(Operand::Coef)) {
+            if (fold_constants && val.is(Operand::Coef) && addend.is(Operand::Coef)) {
               // constant + constant: fold on the host (same IEEE/int result
               // the device add would produce)
               cur = coef(fold_add(s.coefs[val.id], s.coefs[addend.id]));
@@ -280,19 +281,20 @@ template bool mirror_stream(const Stream<double>&, Stream<double>*);
 template bool mirror_stream(const Stream<std::int64_t>&, Stream<std::int64_t>*);
 
 template <typename C>
-Stream<C> lower_fused(const front::FlatProgram<C>& program) {
+Stream<C> lower_fused(const front::FlatProgram<C>& program, bool fold_constants) {
   Stream<C> s;
   s.strict = false;
   s.nvars = program.nvars;
   const auto pow_of = build_powers(program, s);
   Lowerer<C> L{s, pow_of, program};
+  L.fold_constants = fold_constants;
   s.result = L.fused(0);
   return s;
 }
 
 template Stream<double> lower_strict(const front::FlatProgram<double>&);
 template Stream<std::int64_t> lower_strict(const front::FlatProgram<std::int64_t>&);
-template Stream<double> lower_fused(const front::FlatProgram<double>&);
-template Stream<std::int64_t> lower_fused(const front::FlatProgram<std::int64_t>&);
+template Stream<double> lower_fused(const front::FlatProgram<double>&, bool);
+template Stream<std::int64_t> lower_fused(const front::FlatProgram<std::int64_t>&, bool);
 
 }  // namespace polyeval::lower

@@ -95,8 +95,11 @@ struct Stream {
 template <typename C>
 Stream<C> lower_strict(const front::FlatProgram<C>& program);
 
+/// `fold_constants` = false keeps a constant + constant sum as an op (the
+/// wide-integer plans carry placeholders for their coefficients: nothing may
+/// be computed from them on the host).
 template <typename C>
-Stream<C> lower_fused(const front::FlatProgram<C>& program);
+Stream<C> lower_fused(const front::FlatProgram<C>& program, bool fold_constants = true);
 
 /// The strict stream of q(y) = p(-y): the same walk with the coefficients of
 /// odd-exponent terms negated. Every primitive of the interval walk (RN

@@ -17,7 +17,8 @@ struct WidePlan {
   // 32-byte record: kind (0 add, 1 mul), arena offset of the destination,
   // offset of a, offset of b (arena limbs, or coef_words limbs for a
   // coefficient), result width, width of a, width of b (0: the operand is
-  // zero), flags (bit 0: a is a coefficient, bit 1: b is)
+  // zero), flags (bit 0: a is a coefficient, bit 1: b is; bit 2: a product
+  // read only by the sum in the next record, bit 3: as that sum's b)
   std::vector<std::uint32_t> code;
   std::vector<std::uint32_t> slot_off, slot_w;
   std::vector<std::uint32_t> coef_off, coef_w;

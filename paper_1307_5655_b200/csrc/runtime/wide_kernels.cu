@@ -3,8 +3,9 @@
 // points, reference BigIntDomain, bench.cpp:59-187), one point per CTA.
 //
 // The host (runtime/wide.cpp) lowers the program to the walk-VM op list
-// (lower/vm.hpp, strict stream: the reference's adds and products) and
-// bounds every value's magnitude, so each slot of the per-point arena has a
+// (lower/vm.hpp, fused stream: one multiply-add per record of the reference
+// walk — exact integers give its value in any order) and bounds every
+// value's magnitude, so each slot of the per-point arena has a
 // fixed width in 64-bit limbs, two's complement, little-endian. A CTA walks
 // the op list (warp-uniform) and executes each op cooperatively, one limb per
 // lane:
@@ -189,8 +190,10 @@ struct Tmp {
 
 // r[0, w) = x * y, exact when |x * y| < 2^(64 w - 1); r aliases neither
 // operand nor a scratch buffer.
+// With `addend` (one-warp CTAs only): r = x * y + *addend, the sum taken
+// in the pass that assembles the product.
 __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const Tmp& t,
-                        std::uint32_t* s_pair) {
+                        std::uint32_t* s_pair, const Num* addend = nullptr) {
   const std::uint32_t T = blockDim.x;
   const bool nx = negative(x), ny = negative(y);
   if (nx) {  // magnitudes (the top limb may then use the sign bit: read as unsigned)
@@ -236,7 +239,8 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
     // bottom, as two chained additions whose carries run from block to
     // block; a negative product is negated in the same pass (~m + 1).
     std::uint64_t p1 = 0, p2a = 0, p2b = 0;  // a1 of lane 31, a2 of lanes 30 / 31, previous block
-    bool c1 = false, c2 = false, cn = true;
+    const bool neg = nx != ny;
+    bool c1 = false, c2 = false, cn = neg;
     for (std::uint32_t C = 0; C < nbC; ++C) {
       std::uint64_t a0 = 0, a1 = 0, a2 = 0;
       const std::uint32_t I_lo = C > nbB ? C - nbB : 0, I_hi = min(C + 1, nbA);
@@ -267,12 +271,14 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
       cm = lane_carries_out(sum < s1, sum == ~0ull, c2);
       std::uint64_t m = sum + ((cm >> lane) & 1u);
       c2 = (cm >> 32) & 1u;
-      if (nx != ny) {
-        cm = lane_carries_out(false, m == 0, cn);  // ~m + carry: ripples through all-ones
-        m = ~m + ((cm >> lane) & 1u);
+      const std::uint32_t k = 32 * C + lane;
+      if (neg || addend) {  // (-m = ~m + 1) + addend, one more chained addition
+        const std::uint64_t v = neg ? ~m : m;
+        sum = v + (addend ? limb(*addend, k) : 0);
+        cm = lane_carries_out(sum < v, sum == ~0ull, cn);
+        m = sum + ((cm >> lane) & 1u);
         cn = (cm >> 32) & 1u;
       }
-      const std::uint32_t k = 32 * C + lane;
       if (k < w) r[k] = m;
     }
     __syncthreads();
@@ -338,7 +344,8 @@ __device__ void narrow_add(std::uint64_t* r, std::uint32_t w, const Num& x, cons
 }
 
 // r[0, w) = x * y for w, x.w, y.w <= 32, exact when |x * y| < 2^(64 w - 1)
-__device__ void narrow_mul(std::uint64_t* r, std::uint32_t w, const Num& x, const Num& y) {
+__device__ void narrow_mul(std::uint64_t* r, std::uint32_t w, const Num& x, const Num& y,
+                           const Num* addend = nullptr) {
   const int k = threadIdx.x & 31;
   const bool nx = negative(x), ny = negative(y);
   // magnitudes, limb k in lane k (zero past the operand's width)
@@ -366,7 +373,9 @@ __device__ void narrow_mul(std::uint64_t* r, std::uint32_t w, const Num& x, cons
   if (k < 1) s1 = 0;
   if (k < 2) s2 = 0;
   std::uint64_t m = lanes_add(lanes_add(a0, s1, false), s2, false);
-  if (nx != ny) m = lanes_add(~m, 0, true);
+  if (nx != ny || addend) {  // (-m = ~m + 1) + addend
+    m = lanes_add(nx != ny ? ~m : m, addend ? limb(*addend, k) : 0, nx != ny);
+  }
   if (k < static_cast<int>(w)) r[k] = m;
 }
 
@@ -400,17 +409,44 @@ __global__ void __launch_bounds__(kMaxThreads) wide_walk_kernel(const WideArgs a
     __syncthreads();
     const uint4* code = reinterpret_cast<const uint4*>(a.code);
     uint4 c0 = __ldg(code), c1 = __ldg(code + 1);  // op 0 (one 32-byte record per op)
-    for (std::uint32_t op = 0; op < a.nops; ++op) {
+    for (std::uint32_t op = 0; op < a.nops;) {
       // kind, dst offset, a offset, b offset | width, width a, width b, flags
-      const std::uint32_t kind = c0.x, w = c1.x;
+      const std::uint32_t kind = c0.x, w = c1.x, flags = c1.w;
       std::uint64_t* r = arena + c0.y;
-      const Num x{(c1.w & 1u ? a.coef_words : arena) + c0.z, c1.y};
-      const Num y{(c1.w & 2u ? a.coef_words : arena) + c0.w, c1.z};
+      const Num x{(flags & 1u ? a.coef_words : arena) + c0.z, c1.y};
+      const Num y{(flags & 2u ? a.coef_words : arena) + c0.w, c1.z};
       if (op + 1 < a.nops) {  // the next record arrives while this op runs
         c0 = __ldg(code + 2 * op + 2);
         c1 = __ldg(code + 2 * op + 3);
       }
-      if (w <= 32 && x.w <= 32 && y.w <= 32) {
+      bool narrow = w <= 32 && x.w <= 32 && y.w <= 32;
+      if (flags & 4u) {
+        // a product read only by the sum in the next record (now in c0, c1):
+        // e = x * y + c in one op, the product never written. Narrow pairs
+        // always; wide ones where one warp assembles the product.
+        const bool c_is_a = (flags & 8u) != 0;  // the product is the sum's b
+        const Num c{(c1.w & (c_is_a ? 1u : 2u) ? a.coef_words : arena) + (c_is_a ? c0.z : c0.w),
+                    c_is_a ? c1.y : c1.z};
+        const std::uint32_t we = c1.x;
+        narrow = narrow && we <= 32 && c.w <= 32;
+        if (narrow || T == 32) {
+          std::uint64_t* e = arena + c0.y;
+          if (narrow) {
+            if (threadIdx.x < 32) narrow_mul(e, we, x, y, &c);
+            __syncthreads();
+          } else {
+            big_mul(e, we, x, y, t, s_pair, &c);
+          }
+          op += 2;
+          if (op < a.nops) {
+            c0 = __ldg(code + 2 * op);
+            c1 = __ldg(code + 2 * op + 1);
+          }
+          continue;
+        }
+      }
+      ++op;
+      if (narrow) {
         if (threadIdx.x < 32) {
           if (kind == 0) {
             narrow_add(r, w, x, y);
