@@ -1,6 +1,8 @@
 # Scratch: the command of the most recent gpurun call (see gpu_full_round.sh for a full round).
-O=gpurun_out/s26; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_wide.py -x -q --timeout 600 > $O/pytest_wide.log 2>&1; echo "pytest exit $?" >> $O/pytest_wide.log
-for args in "64 1000 8192 balanced" "64 1000 8192 horner" "64 256 16384 balanced" "64 256 16384 horner" "64 64 65536 balanced" "2048 256 296 balanced" "2048 256 2048 balanced" "2048 256 2048 horner"; do
-  timeout 300 python scripts/wide_profile.py $args >> $O/wide_kernel_only.jsonl 2>> $O/wide.err
+O=gpurun_out/s28; mkdir -p $O
+for c in c2e1000 c2b1000 c2e1023 c2b1023 c3; do
+timeout 600 python scripts/profile_one.py --config $c --points 10000000 --reps 5 \
+  --tune jit_mode=1 --tune jit_mode=1,regbound_smem=1 >> $O/regbound.jsonl 2>> $O/regbound.err
 done
+timeout 300 python scripts/profile_one.py --config c2e1000 --strict --points 10000000 --reps 5 \
+  --tune jit_mode=1 --tune jit_mode=1,regbound_smem=1 >> $O/regbound.jsonl 2>> $O/regbound.err
