@@ -15,6 +15,12 @@ done
 timeout 900 python bench.py --impl reference > $O/bench_reference_c4.json 2> $O/bench_reference_c4.err
 timeout 3000 bash scripts/ncu_captures.sh c4 c5 c5split c2e1000 c3
 python scripts/fp64_peaks.py > $O/fp64_peaks.json 2>&1
+[ -x scripts/probes/dfma_load_mix.bin ] || nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 \
+  -o scripts/probes/dfma_load_mix.bin scripts/probes/dfma_load_mix.cu
+scripts/probes/dfma_load_mix.bin > $O/probe_dfma_load_mix.jsonl 2>&1
+for args in "64 1000 8192 balanced" "64 1000 8192 horner" "64 256 16384 balanced" "2048 256 2048 balanced"; do
+  timeout 300 python scripts/wide_profile.py $args >> $O/wide_kernel_only.jsonl 2>> $O/wide.err
+done
 PE_CACHE_DIR=off timeout 900 python scripts/first_call.py > $O/first_call.jsonl 2>&1
 timeout 700 python scripts/fuzz_gpu.py 600 200000 > $O/fuzz.json 2>&1
 timeout 2400 python scripts/fig1_grid.py > $O/fig1_grid.jsonl 2>&1

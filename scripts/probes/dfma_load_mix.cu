@@ -1,9 +1,13 @@
-// Probe: FP64 FMA-pipe throughput of a DFMA stream interleaved with uniform
-// constant loads (LDCU.128, two coefficients each), as a function of loads
-// per DFMA and warps per SM sub-partition. The sectioned C4 walk issues
-// ~0.40 loads per FP64 instruction at 4 warps per sub-partition; C2 0.125;
-// C3 none. Prints one JSON line per variant.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o dfma_load_mix dfma_load_mix.cu
+// Probe: FP64 FMA-pipe throughput of a DFMA stream (2 or 8 independent chains
+// per thread) with one other instruction per 2, 4 or 8 DFMAs — a uniform
+// constant load (LDCU.64), a shared-memory load (LDS.128), a per-thread
+// constant load (LDC.64), a global load through L1 (LDG.128) or an integer
+// add — at 2, 4 and 8 warps per SM sub-partition. Shows which instructions
+// take FP64 issue cycles: the walk kernels deliver their coefficients with
+// such loads (C4: one LDCU.128 per 3.5 and one LDS.128 per 9 FP64
+// instructions at 4 warps per sub-partition; C2 an eighth of that; C3 none).
+// Prints one JSON line per variant (profiles/r2_probe_dfma_load_mix.jsonl).
+//   nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 -o dfma_load_mix.bin dfma_load_mix.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
