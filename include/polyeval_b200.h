@@ -341,7 +341,7 @@ pe_status pe_eval_interval(const pe_program* program, const double* const* lo,
  *   pe_eval_wide: coords[v][i*point_limbs + k] is word k of coordinate v of
  *     point i; out[i*out_limbs + k] receives word k of the result
  *     (sign-extended; out_limbs must be >= pe_program_wide_limbs, else
- *     PE_EOVERFLOW). Host or device buffers; one CTA per point. */
+ *     PE_EOVERFLOW). Host or device buffers; one CTA (normally one warp) per point. */
 pe_status pe_program_create_wide(const uint32_t* exponents, const uint64_t* coeff_words,
                                  uint32_t coeff_limbs, size_t nterms, uint32_t nvars,
                                  const pe_scheme_desc* schemes, pe_program** out);

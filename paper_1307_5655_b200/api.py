@@ -743,8 +743,8 @@ def wide_limbs(program: CompiledProgram, point_limbs: int) -> int:
 
 def evaluate_wide(program: CompiledProgram, points, point_limbs: int | None = None,
                   device: int = -1, as_words: bool = False):
-    """Exact evaluation at integer points of any size (pe_eval_wide, one CTA
-    per point). points: one sequence of Python ints per variable, or one
+    """Exact evaluation at integer points of any size (pe_eval_wide, one warp
+    per point on large batches). points: one sequence of Python ints per variable, or one
     (n, point_limbs) uint64 word array per variable. Returns Python ints (or
     the (n, out_limbs) result words with as_words=True)."""
     if len(points) != program.nvars:

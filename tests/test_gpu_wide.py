@@ -1,4 +1,4 @@
-"""GPU: arbitrary-width exact evaluation (pe_eval_wide, one CTA per point)
+"""GPU: arbitrary-width exact evaluation (pe_eval_wide, one CTA of 1-8 warps per point)
 against the unmodified reference BigInt walk, word for word — the paper's
 Figure-1 workload (reference bench.cpp run_grid defaults: 64-bit
 coefficients and points; acceptance_test.cpp C09: 2048-bit at degrees
