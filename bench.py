@@ -293,14 +293,16 @@ def calibrate_sample(wls, threads, budget_s):
 def cpu_parallel_rate(wl, workers: int, points: int = 100):
     """The reference's intra-point threading (Evaluator::evaluate_parallel,
     eval.hpp:97-140) on `points` points, `workers` threads: points/s."""
-    if wl.domain != "f64":
-        return None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     if not pyoracle.ref_available():
         return None
     ref = pyoracle.Reference(wl.poly, wl.schemes)
     pts = wl.points(points)
+    if wl.domain == "interval":
+        return points / ref.seconds_parallel_interval(pts[0], pts[1], workers)
+    if wl.domain == "i64":
+        return points / ref.seconds_parallel_i64(pts, workers)
     t = time.perf_counter()
     ref.eval_parallel_f64(pts, workers)
     return points / (time.perf_counter() - t)

@@ -89,6 +89,10 @@ def ref_lib():
         lib.ref_eval_i64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int]
         lib.ref_eval_parallel_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                               C.c_uint]
+        lib.ref_time_parallel_interval.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                                   C.c_uint, C.POINTER(C.c_double)]
+        lib.ref_time_parallel_i64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint,
+                                              C.POINTER(C.c_double)]
         lib.ref_export.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                    C.POINTER(C.c_size_t)]
@@ -265,6 +269,22 @@ class Reference:
         self._check(ref_lib().ref_eval_parallel_f64(self._h, _ptrs(cols), out.shape[0],
                                                     out.ctypes.data, workers))
         return out
+
+    def seconds_parallel_interval(self, lo, hi, workers):
+        """Wall time of evaluate_parallel(workers) over the intervals (reference clock)."""
+        lo = [np.ascontiguousarray(c, dtype=np.float64) for c in lo]
+        hi = [np.ascontiguousarray(c, dtype=np.float64) for c in hi]
+        sec = C.c_double()
+        self._check(ref_lib().ref_time_parallel_interval(self._h, _ptrs(lo), _ptrs(hi), lo[0].shape[0],
+                                                         workers, C.byref(sec)))
+        return sec.value
+
+    def seconds_parallel_i64(self, coords, workers):
+        cols = [np.ascontiguousarray(c, dtype=np.int64) for c in coords]
+        sec = C.c_double()
+        self._check(ref_lib().ref_time_parallel_i64(self._h, _ptrs(cols), cols[0].shape[0], workers,
+                                                    C.byref(sec)))
+        return sec.value
 
     def eval_limbs(self, coords, limbs, threads=1):
         """Exact BigInt results as `limbs` uint64 arrays (two's complement)."""

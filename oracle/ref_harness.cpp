@@ -497,4 +497,43 @@ int ref_eval_parallel_f64(void* h, const double* const* coords, std::size_t n, d
   });
 }
 
+// evaluate_parallel in the interval and BigInt domains: seconds for `n`
+// points (the results are checked elsewhere; this is the CPU-baseline leg)
+int ref_time_parallel_interval(void* h, const double* const* lo, const double* const* hi,
+                               std::size_t n, unsigned workers, double* seconds) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    Evaluator<ScaledIntervalDomain> s(ScaledIntervalDomain{rp.integer ? 0 : rp.shift}, *rp.program);
+    std::vector<Interval> p(rp.nvars);
+    double sink = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (std::size_t i = 0; i < n; ++i) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = Interval(lo[v][i], hi[v][i]);
+      sink += s.evaluate_parallel(std::span<const Interval>(p), workers).lo;
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (sink == 12345.678) *seconds += 0;  // keep the loop
+    return 0;
+  });
+}
+
+int ref_time_parallel_i64(void* h, const std::int64_t* const* coords, std::size_t n,
+                          unsigned workers, double* seconds) {
+  return guarded([&] {
+    const RefProgram& rp = *static_cast<RefProgram*>(h);
+    if (!rp.integer) throw std::invalid_argument("integer evaluation needs integer coefficients");
+    Evaluator<BigIntDomain> s(BigIntDomain{}, *rp.program);
+    std::vector<BigInt> p(rp.nvars);
+    std::size_t sink = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (std::size_t i = 0; i < n; ++i) {
+      for (std::size_t v = 0; v < rp.nvars; ++v) p[v] = BigInt(coords[v][i]);
+      sink += s.evaluate_parallel(std::span<const BigInt>(p), workers).is_zero() ? 1 : 0;
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (sink == static_cast<std::size_t>(-1)) *seconds += 0;
+    return 0;
+  });
+}
+
 }  // extern "C"
