@@ -60,27 +60,23 @@ __device__ __forceinline__ std::uint64_t limb(const Num& x, std::uint32_t k) {
   return x.w && (x.p[x.w - 1] >> 63) ? ~0ull : 0ull;  // sign extension
 }
 
-// ---- narrow values (<= 32 limbs): one limb per lane, in registers -----------
-// Most ops of a walk are narrow (a dense polynomial's leaves and low tree
-// levels), and the general path above pays ~10 dependent memory round trips
-// and as many barriers per op whatever the width. Here warp 0 loads the
-// operands once (lane k holds limb k), works in registers with shuffles and
-// ballots, and stores the result: one round trip per op.
+// ---- one limb per lane: warp-wide helpers -----------------------------------
 
 // Carries of a 32-lane addition: lane k generates (g) or propagates (p, with
-// g and p exclusive); bit k of the result is the carry INTO lane k. The chain
-// c(k+1) = g(k) | (p(k) & c(k)) is the carry chain of the binary addition
-// (G|P) + G + cin, and a sum's carries are sum ^ x ^ y.
-__device__ __forceinline__ std::uint32_t lane_carries(bool g, bool p, bool cin) {
+// g and p exclusive). Bit k of the result is the carry INTO lane k, bit 32
+// the carry out of lane 31. The chain c(k+1) = g(k) | (p(k) & c(k)) is the
+// carry chain of the binary addition (G|P) + G + cin, and a sum's carries are
+// sum ^ x ^ y.
+__device__ __forceinline__ std::uint64_t lane_carries_out(bool g, bool p, bool cin) {
   const std::uint32_t G = __ballot_sync(0xffffffffu, g), P = __ballot_sync(0xffffffffu, p);
-  const std::uint32_t X = G | P;
+  const std::uint64_t X = G | P;
   return (X + G + (cin ? 1u : 0u)) ^ X ^ G;
 }
 
 // lane k: limb k of a + b + cin (mod 2^(64*32))
 __device__ __forceinline__ std::uint64_t lanes_add(std::uint64_t a, std::uint64_t b, bool cin) {
   const std::uint64_t s = a + b;
-  const std::uint32_t c = lane_carries(s < a, s == ~0ull, cin);
+  const std::uint64_t c = lane_carries_out(s < a, s == ~0ull, cin);
   return s + ((c >> (threadIdx.x & 31)) & 1u);
 }
 
@@ -88,13 +84,6 @@ __device__ __forceinline__ std::uint64_t shfl64(std::uint64_t v, int src) {
   const std::uint32_t lo = __shfl_sync(0xffffffffu, static_cast<std::uint32_t>(v), src);
   const std::uint32_t hi = __shfl_sync(0xffffffffu, static_cast<std::uint32_t>(v >> 32), src);
   return (static_cast<std::uint64_t>(hi) << 32) | lo;
-}
-
-// Carries of a 32-lane addition plus the carry out of lane 31 (bit 32).
-__device__ __forceinline__ std::uint64_t lane_carries_out(bool g, bool p, bool cin) {
-  const std::uint32_t G = __ballot_sync(0xffffffffu, g), P = __ballot_sync(0xffffffffu, p);
-  const std::uint64_t X = G | P;
-  return (X + G + (cin ? 1u : 0u)) ^ X ^ G;
 }
 
 // (a2, a1, a0) += u * v: 128-bit product into a 192-bit accumulator on the
@@ -335,6 +324,12 @@ __device__ void big_mul(std::uint64_t* r, std::uint32_t w, Num x, Num y, const T
     big_neg(r, w, Num{t.c0, w}, s_pair);
   }
 }
+
+// ---- narrow values (<= 32 limbs) ---------------------------------------------
+// Most ops of a walk are narrow (a dense polynomial's leaves and low tree
+// levels). Warp 0 loads the operands once (lane k holds limb k), works in
+// registers with shuffles and ballots, and stores the result: one memory
+// round trip per op.
 
 // r[0, w) = x + y for w <= 32 (called by the 32 lanes of warp 0)
 __device__ void narrow_add(std::uint64_t* r, std::uint32_t w, const Num& x, const Num& y) {
