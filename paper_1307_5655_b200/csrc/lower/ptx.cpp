@@ -866,12 +866,19 @@ class Emitter {
           continue;
         }
         if (d_ == Domain::Interval && fast_) {
-          // a product of non-straddling intervals cannot straddle (a zero
-          // endpoint is caught by the nextafter "no move" test), so only the
-          // coordinates need the straddle check; signs are tracked statically
+          // A product of non-straddling intervals does not straddle — unless
+          // it underflows: RN gives a zero endpoint and the outward step takes
+          // it across. With both factor signs known the step is the integer
+          // one, which turns a zero into a NaN (caught below); with an
+          // unknown factor sign it is the directed add (fnext), which moves
+          // a zero to -/+dmin like std::nextafter does, so the power must be
+          // checked before anything trusts its sign (squares are "positive",
+          // other powers take their sign from the upper endpoint): a power
+          // that straddles sends the point to the exact replay.
           fast_mul(pw(id, k, false), pw(id, k, true), {pw(p.lo, k, false), pw(p.lo, k, true)},
                    {pw(p.hi, k, false), pw(p.hi, k, true)}, false, false, psign_[p.lo],
                    psign_[p.hi]);
+          if (psign_[p.lo] * psign_[p.hi] == 0) fcheck_straddle({pw(id, k, false), pw(id, k, true)});
           fcheck_finite(pw(id, k, false));
           fcheck_finite(pw(id, k, true));
         } else if (d_ == Domain::Interval && medium_) {
@@ -1737,8 +1744,10 @@ class Emitter {
   // Static sign of an operand in the fast path: +1 / -1 when every
   // unflagged evaluation has that sign on both endpoints, 0 when unknown.
   // Coefficients are nonzero non-straddling (host-checked); squares are
-  // positive; products and same-sign sums keep known signs (a zero endpoint
-  // is caught by the nextafter "no move" test, so "known" never hides one).
+  // positive; products and same-sign sums keep known signs (a known-sign
+  // step turns a zero endpoint into a NaN, and powers stepped with the
+  // unknown-sign step are straddle-checked where they are computed, so
+  // "known" never hides a zero crossing).
   int sgn(const Operand& o) const {
     switch (o.kind) {
       case Operand::Coef: return ivcoef(o.id).lo > 0 ? 1 : -1;

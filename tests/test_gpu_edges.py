@@ -592,3 +592,38 @@ def test_interval_int64_coefficients_above_2_53_bit_exact(scheme, mode, cuda_dev
     olo, ohi = pyoracle.Oracle(p, [pe.builtin_scheme(scheme)]).eval_interval([lo], [hi])
     assert np.array_equal(glo.view(np.int64), olo.view(np.int64))
     assert np.array_equal(ghi.view(np.int64), ohi.view(np.int64))
+
+
+@pytest.mark.parametrize("nvars", [1, 2])
+@pytest.mark.parametrize("scheme", ["horner", "estrin", "balanced"])
+def test_interval_fast_path_power_underflow_bit_exact(nvars, scheme, cuda_device):
+    # Powers of tiny coordinates underflow: RN gives a zero endpoint and the
+    # outward nextafter carries it across zero, so x^k straddles although x
+    # does not (and although "squares are positive"). The fast path must send
+    # such points to the exact replay instead of trusting the static sign
+    # (found by scripts/fuzz_gpu.py seed 410119: results narrower than the
+    # reference's). Unpartitioned and partitioned kernels, 1 and 2 variables.
+    rng = np.random.default_rng(410119 + nvars)
+    n = 2048
+    if nvars == 1:
+        ex = np.array([[29], [14], [7], [2], [1], [0]])
+    else:
+        ex = np.array([[29, 3], [14, 26], [6, 0], [2, 2], [1, 5], [0, 0]])
+    p = pe.Polynomial(ex, rng.normal(size=len(ex)))
+    x = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-320, 2, n)   # down to subnormals
+    w = np.abs(x) * 10.0 ** rng.uniform(-17, 0, n) * (rng.random(n) < 0.7)
+    lo, hi = [x.copy()], [x + w]
+    if nvars == 2:
+        y = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-3, 9, n)
+        lo.append(y.copy())
+        hi.append(y + np.abs(y) * 1e-9)
+    sch = [pe.builtin_scheme(scheme)] * nvars
+    olo, ohi = pyoracle.Oracle(p, sch).eval_interval(lo, hi)
+    for tune in (dict(jit_mode=1), dict(jit_mode=1, iv_partition=-1),
+                 dict(jit_mode=1, iv_partition_min=1), dict(jit_mode=1, iv_partition=3, iv_partition_min=1)):
+        prog = pe.compile(p, sch)
+        prog.set_tuning(**tune)
+        glo, ghi = pe.Evaluator(pe.IntervalDomain(), prog).evaluate(
+            ([_t(a, cuda_device) for a in lo], [_t(a, cuda_device) for a in hi]))
+        assert np.array_equal(glo.cpu().numpy().view(np.int64), olo.view(np.int64)), tune
+        assert np.array_equal(ghi.cpu().numpy().view(np.int64), ohi.view(np.int64)), tune
