@@ -1,5 +1,9 @@
 # Scratch: the command of the most recent gpurun call (see gpu_full_round.sh for a full round).
-O=gpurun_out/s31; mkdir -p $O
-timeout 600 python scripts/fuzz_repro.py 410119 > $O/repro_410119.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -k "interval or partition" > $O/pytest_iv.log 2>&1; echo "pytest exit $?" >> $O/pytest_iv.log
-timeout 300 python scripts/profile_one.py --config c5 --points 100000000 --reps 3 --tune jit_mode=1 --tune jit_mode=1,iv_partition=-1 > $O/c5.jsonl 2> $O/c5.err
+O=gpurun_out/s32; mkdir -p $O
+for c in c5 c3; do
+  timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err
+done
+timeout 700 python scripts/fuzz_gpu.py 600 500000 > $O/fuzz_a.json 2>&1
+timeout 700 python scripts/fuzz_gpu.py 600 510000 jit_mode=1,iv_partition_min=1 > $O/fuzz_b.json 2>&1
+timeout 700 python scripts/fuzz_gpu.py 600 520000 jit_mode=1,iv_partition=3,iv_partition_min=1 > $O/fuzz_c.json 2>&1
+timeout 700 python scripts/fuzz_gpu.py 600 530000 jit_mode=1,section_ops=200,group_tiles=3 > $O/fuzz_d.json 2>&1
