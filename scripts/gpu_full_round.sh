@@ -22,6 +22,7 @@ for args in "64 1000 8192 balanced" "64 1000 8192 horner" "64 256 16384 balanced
   timeout 300 python scripts/wide_profile.py $args >> $O/wide_kernel_only.jsonl 2>> $O/wide.err
 done
 PE_CACHE_DIR=off timeout 900 python scripts/first_call.py > $O/first_call.jsonl 2>&1
-timeout 700 python scripts/fuzz_gpu.py 600 200000 > $O/fuzz.json 2>&1
+timeout 700 python scripts/fuzz_gpu.py 600 600000 > $O/fuzz.json 2>&1
+timeout 700 python scripts/fuzz_wide.py 600 700000 > $O/fuzz_wide.json 2>&1
 timeout 2400 python scripts/fig1_grid.py > $O/fig1_grid.jsonl 2>&1
 echo done > $O/DONE
