@@ -20,5 +20,6 @@ for c in "${@:-c4 c5}"; do
   ncu -i $O/ncu_${c}.ncu-rep --page raw --csv > $O/r2_ncu_${c}_raw.csv 2>/dev/null
   ncu -i $O/ncu_${c}.ncu-rep --page details --csv > $O/r2_ncu_${c}_details.csv 2>/dev/null
   echo $pts > $O/r2_ncu_${c}_points.txt
+  rm -f $O/ncu_${c}.ncu-rep  # gpurun copies back at most 64 MiB: keep the CSV exports only
 done
 echo done > $O/DONE
