@@ -70,8 +70,12 @@ def check(seed):
     if n <= 3:  # and against Python's own integers
         ints = pe.words_to_ints(got)
         for i in range(n):
-            want = sum(c * np.prod([int(pts[v][i]) ** int(e[v]) for v in range(nv)], dtype=object)
-                       for c, e in zip(coefs, ex))
+            want = 0
+            for c, e in zip(coefs, ex):
+                t = c
+                for v in range(nv):
+                    t *= int(pts[v][i]) ** int(e[v])
+                want += t
             assert ints[i] == want, "python integer cross-check"
     return block
 
